@@ -1,0 +1,276 @@
+/*
+ * qcb200.h -- C ABI of the B200-native QuantCache hot path (libqcb200.so).
+ *
+ * Plain pointers, sizes and a cudaStream_t passed as void*; no torch types.
+ * All pointers are DEVICE pointers unless stated; the caller owns every
+ * buffer (no allocation inside hot-path calls; workspaces are passed in).
+ * Every entry point returns a status code (QCB_OK == 0).  The Python mirror
+ * (paper_2503_06545_b200/_native.py) maps codes onto the reference's
+ * exception types (errors.py:4-21):
+ *     QCB_ERR_DIM -> DimensionError, QCB_ERR_CONFIG / QCB_ERR_OVERFLOW ->
+ *     ConfigurationError, QCB_ERR_VALUE -> ValueError, QCB_ERR_TYPE ->
+ *     TypeError, QCB_ERR_CUDA -> RuntimeError.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/ditrt):
+ *   qcb_gemm_u8        tensor.py:68-112   matmul_int (+ model.py:187-198 epilogues)
+ *   qcb_gemm_f64       tensor.py:43-65    mm / matmul_fp (FP sites, head)
+ *   qcb_act_quant      quant.py:83-123,163-165  compute_minmax_params + quantize
+ *                      on BalanceTransform.apply_to_activation, with the
+ *                      LN/modulation prologue of model.py:182,189,196
+ *   qcb_weight_prep    runtime.py:40-61   QuantRuntime.__init__ weight prep
+ *   qcb_attention_f64  model.py:150-156, tensor.py:115-132  _mha / attention
+ *   qcb_ln_mod         model.py:137-142 (+182,196)  _ln and modulation
+ *   qcb_ddpm_step      sampler.py:59-88   reverse_step / final_step
+ *   qcb_reduce_hlc     schedule.py:67-82  divergence_score partial sums
+ *   qcb_reduce_srap    schedule.py:108-116 layer_similarity partial sums
+ *   qcb_reduce_var     schedule.py:128-133 cumulative_variation
+ *   qcb_policy_*       schedule.py:281-351 Scheduler.plan_step / observe_block
+ */
+#ifndef QCB200_H_
+#define QCB200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  QCB_OK = 0,
+  QCB_ERR_DIM = 1,
+  QCB_ERR_CONFIG = 2,
+  QCB_ERR_OVERFLOW = 3,
+  QCB_ERR_VALUE = 4,
+  QCB_ERR_TYPE = 5,
+  QCB_ERR_CUDA = 6
+};
+
+/* GEMM epilogues (model.py:183-198). */
+enum {
+  QCB_EPI_STORE = 0,      /* out = y                         (q, k, v, ca_q/k/v)  */
+  QCB_EPI_GELU = 1,       /* out = f32(gelu_f64(y))          (ffn1)               */
+  QCB_EPI_GATE_RESID = 2, /* out = resid + gate * y (f32)    (sta_o, ffn2)        */
+  QCB_EPI_RESID = 3,      /* out = resid + y (f32)           (ca_o)               */
+  QCB_EPI_ACC = 4,        /* out = exact s32 accumulator (debug / parity)         */
+  QCB_EPI_BIAS = 5        /* out = y + bias[n] (f32)         (head, gemm_f64 only) */
+};
+
+/* Activation prologues. */
+enum { QCB_PRO_NONE = 0, QCB_PRO_LN_MOD = 1 };
+
+#define QCB_MAX_LAYERS 64
+#define QCB_MAX_HIST 8
+
+/* ---------------------------------------------------------------- GEMMs */
+typedef struct QcbGemm {
+  int M, N, K;            /* K = true reduction length                         */
+  int seg_rows;           /* rows per activation segment (video); 0 = M        */
+  int seg_valid;          /* valid rows per segment (others are padding); 0=all */
+  const uint8_t* a_codes; /* [M][lda] u8, lda % 16 == 0                         */
+  long long lda;
+  const double* a_scale;  /* [segments] per-tensor activation scale            */
+  const int* a_zero;      /* [segments]                                        */
+  const int* a_rowsum;    /* [M] sum_k a_codes                                 */
+  const uint8_t* w_codes; /* [N][ldw] u8 (K-major, i.e. W^T), ldw % 16 == 0     */
+  long long ldw;
+  const double* w_scale;  /* [N] per-output-channel scale                      */
+  const int* w_zero;      /* [N]                                               */
+  const int* w_colsum;    /* [N] sum_k w_codes                                 */
+  float* out;             /* [M][ldo] f32 (or s32 for QCB_EPI_ACC)             */
+  long long ldo;
+  const long long* out_row0;   /* nullable: first output row per segment        */
+  const float* resid;          /* residual input for *_RESID (may alias out)   */
+  long long ldr;
+  const long long* resid_row0; /* nullable: first residual row per segment     */
+  const float* gate;           /* nullable: per-segment gate                    */
+  float gate_scalar;
+  int epilogue;
+  int block_n;                 /* 0 = auto                                      */
+  const int* seg_active;       /* nullable: per-segment flag, skip inactive     */
+} QcbGemm;
+
+int qcb_gemm_u8(const QcbGemm* g, void* stream);
+
+/* Plain f64-accumulating FP GEMM, ascending k (tensor.py:43-60), f32 out.
+ * A [M][lda] f32 (rows via a_row0 per segment), W [K][ldw] f32 row-major. */
+typedef struct QcbGemmF64 {
+  int M, N, K;
+  int seg_rows, seg_valid;
+  const float* a;
+  long long lda;
+  const long long* a_row0;
+  const float* w;
+  long long ldw;
+  float* out;
+  long long ldo;
+  const long long* out_row0;
+  const float* resid;
+  long long ldr;
+  const long long* resid_row0;
+  const float* bias;
+  float gate_scalar;
+  int epilogue;
+} QcbGemmF64;
+
+int qcb_gemm_f64(const QcbGemmF64* g, void* stream);
+
+/* ---------------------------------------------------------------- quantizer */
+typedef struct QcbActQuant {
+  const float* x;            /* input rows [.][ldx]                             */
+  long long ldx;
+  const long long* x_row0;   /* nullable: first input row per segment           */
+  int K, seg_rows, seg_valid, nseg;
+  int prologue;              /* QCB_PRO_*                                        */
+  const float* ln_g;         /* nullable (= ones)                               */
+  const float* ln_b;         /* nullable (= zeros)                              */
+  float mod_scale1;          /* f32(1 + scale) ; 1 for no modulation             */
+  float mod_shift;           /* shift ; 0 for no modulation                      */
+  int n_out;                 /* 1..3 outputs sharing the prologue                */
+  int bits;                  /* activation bit-width                             */
+  const double* chan_scale[3]; /* nullable: balance scales c (no rotation)       */
+  const float* signs[3];     /* [b] +-1 of the randomized Hadamard block         */
+  uint8_t* codes[3];         /* [nseg*seg_rows][ldc] outputs                     */
+  long long ldc;
+  int* rowsum[3];            /* [nseg*seg_rows]                                  */
+  double* scale[3];          /* [nseg]                                           */
+  int* zero[3];              /* [nseg]                                           */
+  float* xe_out[3];          /* nullable: rotated activations (debug / FP modes) */
+  long long ldxe;
+  float* deq_out[3];         /* nullable: f32(s*(code-z)) fake-quant outputs     */
+  void* workspace;           /* >= 8*n_out*nseg bytes                            */
+} QcbActQuant;
+
+int qcb_act_quant(const QcbActQuant* q, void* stream);
+
+typedef struct QcbWeightPrep {
+  const float* w;            /* [K][N] f32, reference layout                     */
+  int K, N, bits;
+  const double* chan_scale;  /* nullable: no balance / rotation                  */
+  const float* signs;        /* [b]                                              */
+  uint8_t* codes;            /* [N][ldk] K-major                                 */
+  long long ldk;
+  double* scale;             /* [N]                                              */
+  int* zero;                 /* [N]                                              */
+  int* colsum;               /* [N]                                              */
+  float* w_eff;              /* nullable [K][N]: rotated weights                 */
+  float* w_deq;              /* nullable [K][N]: dequantized weights             */
+} QcbWeightPrep;
+
+int qcb_weight_prep(const QcbWeightPrep* q, void* stream);
+
+/* ---------------------------------------------------------------- FP helpers */
+typedef struct QcbLnMod {
+  const float* x; long long ldx; const long long* x_row0;
+  float* out; long long ldo; const long long* out_row0;
+  int K, seg_rows, seg_valid, nseg;
+  const float* ln_g; const float* ln_b;
+  float mod_scale1, mod_shift;
+} QcbLnMod;
+
+int qcb_ln_mod(const QcbLnMod* q, void* stream);
+
+/* Per-head softmax(q k^T / sqrt(dh)) v with f64 softmax; q [S][ldq], k/v [Skv][.]. */
+typedef struct QcbAttention {
+  const float* q; long long ldq;
+  const float* k; long long ldk;
+  const float* v; long long ldv;
+  float* out; long long ldo;
+  int S, Skv, heads, dh, nseg;   /* segments stacked along rows                 */
+  long long q_seg_stride, kv_seg_stride, o_seg_stride; /* rows between segments */
+  int seg_valid;
+} QcbAttention;
+
+int qcb_attention_f64(const QcbAttention* a, void* stream);
+
+/* x_{t-1} = f32((x - c1*eps)/c2 + c3*noise) in f64 (c3 = 0: no noise). */
+typedef struct QcbDdpm {
+  const float* x; const float* eps; const float* noise; float* out;
+  long long n;
+  double c1, c2, c3;
+} QcbDdpm;
+
+int qcb_ddpm_step(const QcbDdpm* d, void* stream);
+
+/* ---------------------------------------------------------------- reductions */
+/* Segmented f64 reductions over f32 feature maps, one result per segment.
+ * A segment is `rows` rows of `cols` floats starting at base + row0[seg]*ld.
+ * Results are deterministic (fixed-order two-stage reduction). */
+typedef struct QcbFeat {
+  const float* base; long long ld; const long long* row0;
+} QcbFeat;
+
+/* sum|out-ref| and sum (out-prev)^2 per segment -> res[seg*2 + {0,1}] */
+int qcb_reduce_hlc(QcbFeat out, QcbFeat ref, QcbFeat prev, int rows, int cols, int nseg,
+                   const int* seg_active, double* res, void* workspace, void* stream);
+/* <a,b>, <a,a>, <b,b> per segment -> res[seg*3 + {0,1,2}] */
+int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nseg,
+                    const int* seg_active, double* res, void* workspace, void* stream);
+/* sum|x - h| per segment -> res[seg] */
+int qcb_reduce_l1(QcbFeat x, QcbFeat h, int rows, int cols, int nseg, double* res,
+                  void* workspace, void* stream);
+
+size_t qcb_reduce_workspace_bytes(int nseg);
+
+/* ---------------------------------------------------------------- policy */
+typedef struct QcbThresholds {  /* schedule.py:22-42 */
+  double delta1, delta2;
+  int tau_max, tau_mid, tau_min;
+  double theta1, theta2;
+  int bit_max, bit_mid, bit_min;
+  double tau_high, tau_low, p_base, v_low, v_high;
+  int history_k;
+  double prune_adjust;
+  int hlc, aigq_w, aigq_a, srap;  /* Toggles (schedule.py:213-221) */
+} QcbThresholds;
+
+/* Device-resident per-video Scheduler state (schedule.py:243-269) plus the
+ * current step's decision (ScheduleDecision, schedule.py:176-184). */
+typedef struct QcbPolicyVideo {
+  int seen, n_d, boundary, long_skip;
+  int abits, forced, pad0, pad1;
+  int cache_valid[QCB_MAX_LAYERS];
+  int cache_step[QCB_MAX_LAYERS];
+  int cache_tau[QCB_MAX_LAYERS];
+  int prev_valid[QCB_MAX_LAYERS];
+  int d_order[QCB_MAX_LAYERS];      /* insertion order of last_divergences   */
+  int has_d[QCB_MAX_LAYERS];
+  int action[QCB_MAX_LAYERS];       /* 0 recompute, 1 reuse, 2 prune          */
+  int sim_valid[QCB_MAX_LAYERS];
+  int d_valid[QCB_MAX_LAYERS];      /* D computed this step                   */
+  int ref_kind[QCB_MAX_LAYERS];     /* 0 none, 1 cache, 2 prev (this step)    */
+  double last_d[QCB_MAX_LAYERS];
+  double sim[QCB_MAX_LAYERS];
+  double d_now[QCB_MAX_LAYERS];
+  double v;
+} QcbPolicyVideo;
+
+enum { QCB_ACT_RECOMPUTE = 0, QCB_ACT_REUSE = 1, QCB_ACT_PRUNE = 2 };
+
+/* plan_step part 1: boundary, HLC reuse (cache liveness), long-skip flag. */
+int qcb_policy_plan_reuse(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
+                          void* stream);
+/* Which (video, layer) pairs need an SRAP similarity this step:
+ * flags[v*L + l] = 1 iff srap on, not boundary, l >= 1, action recompute and
+ * both previous features exist (schedule.py:296-304). */
+int qcb_policy_sim_mask(const QcbPolicyVideo* st, int nvid, int L, QcbThresholds th,
+                        int* flags, void* stream);
+/* plan_step part 2: SRAP prune decisions from srap sums [v][L][3] and the
+ * variation v_sum[v], activation bits (schedule.py:293-326). draws: [L] f64
+ * (prune_draw(seed, t, l) for this t), per video row stride L. */
+int qcb_policy_plan_finish(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
+                           const double* srap_sums, const double* v_sum, const double* draws,
+                           long long draws_vid_stride, void* stream);
+/* observe_block for layer l: hlc sums [v][2] (valid where ref_kind != 0),
+ * k per video from cache step; tau / cache / prev / last_d updates
+ * (schedule.py:330-351). */
+int qcb_policy_observe(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
+                       const double* hlc_sums, void* stream);
+
+/* ---------------------------------------------------------------- misc */
+int qcb_device_sm_count(void);
+const char* qcb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QCB200_H_ */

@@ -1,0 +1,395 @@
+// Quantized linear for the QuantCache hot path: u8 x u8 -> s32 on the sm_100a
+// tensor cores (tcgen05.mma kind::i8, accumulator in TMEM, operands staged by
+// TMA with 128-byte swizzle), followed by an exact epilogue.
+//
+// Replaces the reference's emulated integer GEMM `matmul_int`
+// (/root/reference/pkg/src/ditrt/tensor.py:68-112) as called from the GEMM
+// hook `QuantRuntime.gemm_fn` (runtime.py:63-81) at every quantized site of
+// `block_forward` (model.py:183-198).
+//
+// Numerics.  Codes are unsigned with zero points (quant.py:113-123), so the
+// MMA computes raw = sum_k a*w and the epilogue recovers the reference's exact
+// integer accumulator
+//     acc = raw - zw[n]*rowsum_a[m] - za*colsum_w[n] + K*za*zw[n]
+// (exact modulo 2^32; |acc| <= K*255^2 < 2^31 for K <= 33025).  The output is
+// f32(f64(sa*sw[n]) * f64(acc)): the joint scale has a <=32-bit significand
+// (16-bit scales, quant.py:1-8) so this equals the reference's ascending-k f64
+// sum whenever its partial sums are exact (tests pin it on the fixtures).
+//
+// Fused epilogues (model.py:187-198): plain store (q/k/v, ca_*), exact-erf GELU
+// in f64 (ffn1), x + gate*y (sta_o, ffn2) and x + y (ca_o), with the f32
+// roundings of the reference (no FMA contraction).
+#include <cudaTypedefs.h>
+
+#include "qc_common.cuh"
+#include "qc_api_internal.h"
+
+namespace qc {
+
+constexpr int kBlockM = 128;
+constexpr int kBlockK = 128;  // bytes == u8 elements
+constexpr int kUmmaK = 32;    // K per tcgen05.mma kind::i8
+constexpr int kThreads = 256;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN >= 192 ? 5 : (BN >= 128 ? 6 : 8);
+  static constexpr int kABytes = kBlockM * kBlockK;
+  static constexpr int kBBytes = BN * kBlockK;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32
+                                        : (2 * BN <= 64) ? 64
+                                        : (2 * BN <= 128) ? 128
+                                        : (2 * BN <= 256) ? 256
+                                                          : 512;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct GemmParams {
+  int M, N, K;
+  int seg_rows;    // rows per activation segment (video); params are per segment
+  int seg_valid;   // valid rows per segment (rows >= seg_valid are padding)
+  int num_m_tiles, num_n_tiles;
+  const double* sa;
+  const int* za;
+  const int* rowsum;
+  const double* sw;
+  const int* zw;
+  const int* colsum;
+  float* out;
+  long long ldo;
+  const long long* out_row0;  // nullable: per-segment first row of the output
+  const float* resid;
+  long long ldr;
+  const long long* resid_row0;  // nullable
+  const float* gate;            // nullable: per-segment gate; else gate_scalar
+  float gate_scalar;
+  int mode;
+  const int* seg_active;  // nullable: skip tiles of inactive segments
+};
+
+QC_DEV double gelu_exact(double x) {
+  // 0.5 x (1 + erf(x / sqrt(2))) in f64 (model.py:145-147)
+  return 0.5 * x * (1.0 + erf(x / 1.4142135623730951));
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_u8_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + Cfg::kStages * Cfg::kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + Cfg::kStages;
+  uint64_t* tfull_bar = empty_bar + Cfg::kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  const int num_kb = (p.K + kBlockK - 1) / kBlockK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_active = [&](int tile) -> bool {
+    if (p.seg_active == nullptr) return true;
+    int mt = tile / p.num_n_tiles;
+    return p.seg_active[(mt * kBlockM) / p.seg_rows] != 0;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        if (!tile_active(tile)) continue;
+        const int m0 = (tile / p.num_n_tiles) * kBlockM;
+        const int n0 = (tile % p.num_n_tiles) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+          tma_load_2d(&map_a, &full_bar[stage], smem_a + stage * Cfg::kABytes, kb * kBlockK, m0);
+          tma_load_2d(&map_b, &full_bar[stage], smem_b + stage * Cfg::kBBytes, kb * kBlockK, n0);
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_u8(kBlockM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        if (!tile_active(tile)) continue;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBlockK / kUmmaK; ++k) {
+            umma_u8(d_tmem, smem_desc_sw128(a_addr + k * kUmmaK),
+                    smem_desc_sw128(b_addr + k * kUmmaK), idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (TMEM -> regs -> global)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      if (!tile_active(tile)) continue;
+      const int m0 = (tile / p.num_n_tiles) * kBlockM;
+      const int n0 = (tile % p.num_n_tiles) * BN;
+      const int m = m0 + q * 32 + lane;
+      const int seg = m / p.seg_rows;
+      const int mrow = m - seg * p.seg_rows;
+      const bool row_ok = (m < p.M) && (mrow < p.seg_valid);
+      double sa = 0.0;
+      int za = 0, rs = 0;
+      float gate = p.gate_scalar;
+      long long orow = m, rrow = m;
+      if (row_ok) {
+        sa = p.sa[seg];
+        za = p.za[seg];
+        rs = p.rowsum[m];
+        if (p.gate) gate = p.gate[seg];
+        if (p.out_row0) orow = p.out_row0[seg] + mrow;
+        if (p.resid_row0) rrow = p.resid_row0[seg] + mrow;
+      }
+      const int kzz = p.K * za;
+
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld_wait();
+        const int nb = n0 + c * 32;
+        if (row_ok && nb < p.N) {
+          float* orow_ptr = p.out + orow * p.ldo;
+          const float* rrow_ptr = p.resid ? p.resid + rrow * p.ldr : nullptr;
+#pragma unroll
+          for (int j4 = 0; j4 < 32; j4 += 4) {
+            float v[4];
+            float rv[4] = {0.f, 0.f, 0.f, 0.f};
+            const int n4 = nb + j4;
+            const bool full4 = (n4 + 3 < p.N);
+            if (rrow_ptr && (p.mode == QCB_EPI_GATE_RESID || p.mode == QCB_EPI_RESID)) {
+              if (full4 && ((reinterpret_cast<uintptr_t>(rrow_ptr + n4) & 15) == 0)) {
+                float4 t = *reinterpret_cast<const float4*>(rrow_ptr + n4);
+                rv[0] = t.x; rv[1] = t.y; rv[2] = t.z; rv[3] = t.w;
+              } else {
+                for (int e = 0; e < 4; ++e)
+                  if (n4 + e < p.N) rv[e] = rrow_ptr[n4 + e];
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int n = n4 + e;
+              float y = 0.f;
+              if (n < p.N) {
+                const int zw = __ldg(p.zw + n);
+                const int raw = (int)r[j4 + e];
+                const int accv = raw - zw * rs - za * __ldg(p.colsum + n) + kzz * zw;
+                if (p.mode == QCB_EPI_ACC) {
+                  y = __int_as_float(accv);
+                } else {
+                  const double joint = __dmul_rn(sa, __ldg(p.sw + n));
+                  y = __double2float_rn(__dmul_rn(joint, (double)accv));
+                  if (p.mode == QCB_EPI_GELU) {
+                    y = __double2float_rn(gelu_exact((double)y));
+                  } else if (p.mode == QCB_EPI_GATE_RESID) {
+                    y = __fadd_rn(rv[e], __fmul_rn(gate, y));
+                  } else if (p.mode == QCB_EPI_RESID) {
+                    y = __fadd_rn(rv[e], y);
+                  }
+                }
+              }
+              v[e] = y;
+            }
+            if (full4 && ((reinterpret_cast<uintptr_t>(orow_ptr + n4) & 15) == 0)) {
+              *reinterpret_cast<float4*>(orow_ptr + n4) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+              for (int e = 0; e < 4; ++e)
+                if (n4 + e < p.N) orow_ptr[n4 + e] = v[e];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_free<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D u8 K-major operand [rows][ld] (K valid columns), box 128 bytes x box_rows.
+static int make_map_u8(CUtensorMap* map, const void* base, int rows, int K, long long ld,
+                       int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return QCB_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? QCB_OK : QCB_ERR_CUDA;
+}
+
+static int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+template <int BN>
+static int launch_bn(const QcbGemm* g, cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  CUtensorMap ma, mb;
+  int rc = make_map_u8(&ma, g->a_codes, g->M, g->K, g->lda, kBlockM);
+  if (rc) return rc;
+  rc = make_map_u8(&mb, g->w_codes, g->N, g->K, g->ldw, BN);
+  if (rc) return rc;
+  GemmParams p{};
+  p.M = g->M;
+  p.N = g->N;
+  p.K = g->K;
+  p.seg_rows = g->seg_rows > 0 ? g->seg_rows : g->M;
+  p.seg_valid = g->seg_valid > 0 ? g->seg_valid : p.seg_rows;
+  p.num_m_tiles = (g->M + kBlockM - 1) / kBlockM;
+  p.num_n_tiles = (g->N + BN - 1) / BN;
+  p.sa = g->a_scale;
+  p.za = g->a_zero;
+  p.rowsum = g->a_rowsum;
+  p.sw = g->w_scale;
+  p.zw = g->w_zero;
+  p.colsum = g->w_colsum;
+  p.out = g->out;
+  p.ldo = g->ldo;
+  p.out_row0 = g->out_row0;
+  p.resid = g->resid;
+  p.ldr = g->ldr;
+  p.resid_row0 = g->resid_row0;
+  p.gate = g->gate;
+  p.gate_scalar = g->gate_scalar;
+  p.mode = g->epilogue;
+  p.seg_active = g->seg_active;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_u8_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::kSmemBytes);
+    attr_set = true;
+  }
+  int tiles = p.num_m_tiles * p.num_n_tiles;
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_u8_tcgen05<BN><<<grid, kThreads, Cfg::kSmemBytes, st>>>(ma, mb, p);
+  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+}
+
+int pick_block_n(int N) {
+  // Largest legal UMMA N (multiple of 16, <= 256) minimising padded columns.
+  static const int cands[] = {256, 192, 128, 64, 32};
+  int best = 32;
+  long best_waste = 1L << 40;
+  for (int bn : cands) {
+    long tiles = (N + bn - 1) / bn;
+    long waste = tiles * bn - N;
+    if (waste < best_waste) {
+      best_waste = waste;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+int gemm_u8_launch(const QcbGemm* g, cudaStream_t st) {
+  int bn = g->block_n > 0 ? g->block_n : pick_block_n(g->N);
+  switch (bn) {
+    case 256: return launch_bn<256>(g, st);
+    case 192: return launch_bn<192>(g, st);
+    case 128: return launch_bn<128>(g, st);
+    case 64: return launch_bn<64>(g, st);
+    case 32: return launch_bn<32>(g, st);
+    default: return QCB_ERR_CONFIG;
+  }
+}
+
+}  // namespace qc

@@ -1,0 +1,360 @@
+// HLC / SRAP device reductions and the device-resident decision engine.
+//
+// Reductions (HBM-bound, f64 accumulation, deterministic fixed-order two-stage
+// tree so repeated runs are byte-identical like the reference, criterion 9):
+//   hlc  : sum|out - ref|, sum (out - prev)^2   -> divergence_score (schedule.py:67-82)
+//   srap : <a,b>, <a,a>, <b,b>                  -> layer_similarity (schedule.py:108-116)
+//   l1   : sum|x - h|                           -> cumulative_variation (schedule.py:128-133)
+// Policy kernels restate Scheduler.plan_step / observe_block
+// (schedule.py:281-351) on device state (QcbPolicyVideo), one thread per video.
+#include "qc_common.cuh"
+#include "qc_api_internal.h"
+
+namespace qc {
+
+constexpr int kRThreads = 256;
+constexpr int kMaxChunks = 64;
+
+struct FeatP {
+  const float* base;
+  long long ld;
+  const long long* row0;
+};
+
+QC_DEV const float* feat_row(const FeatP& f, int seg, int rows, int r) {
+  const long long r0 = f.row0 ? f.row0[seg] : (long long)seg * rows;
+  return f.base + (r0 + r) * f.ld;
+}
+
+template <int NV>
+QC_DEV void block_sum_vec(double (&v)[NV], double* scratch /*[NV][8]*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[i * 8 + warp] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double s = 0.0;
+      for (int w = 0; w < kRThreads / 32; ++w) s += scratch[i * 8 + w];
+      v[i] = s;
+    }
+  }
+}
+
+// kind 0: hlc (2 sums), 1: srap (3 sums), 2: l1 (1 sum).
+template <int KIND, int NV>
+__global__ void __launch_bounds__(kRThreads)
+    seg_reduce(FeatP f0, FeatP f1, FeatP f2, int rows, int cols, const int* seg_active,
+               double* partials, int* tickets, double* res, int chunks) {
+  __shared__ double scratch[NV * 8];
+  __shared__ bool last;
+  const int seg = blockIdx.y;
+  if (seg_active && !seg_active[seg]) return;
+  const int chunk = blockIdx.x;
+  const int r0 = (int)((long long)rows * chunk / chunks);
+  const int r1 = (int)((long long)rows * (chunk + 1) / chunks);
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  const bool vec = (cols % 4 == 0) && (f0.ld % 4 == 0) && (f1.ld % 4 == 0) &&
+                   (KIND != 0 || f2.ld % 4 == 0);
+  for (int r = r0; r < r1; ++r) {
+    const float* a = feat_row(f0, seg, rows, r);
+    const float* b = feat_row(f1, seg, rows, r);
+    const float* c = KIND == 0 ? feat_row(f2, seg, rows, r) : nullptr;
+    if (vec) {
+      for (int j = threadIdx.x; j < cols / 4; j += kRThreads) {
+        const float4 x = reinterpret_cast<const float4*>(a)[j];
+        const float4 y = reinterpret_cast<const float4*>(b)[j];
+        const float xa[4] = {x.x, x.y, x.z, x.w}, ya[4] = {y.x, y.y, y.z, y.w};
+        float za[4] = {0.f, 0.f, 0.f, 0.f};
+        if (KIND == 0) {
+          const float4 z = reinterpret_cast<const float4*>(c)[j];
+          za[0] = z.x; za[1] = z.y; za[2] = z.z; za[3] = z.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double xd = xa[e], yd = ya[e];
+          if (KIND == 0) {
+            acc[0] += fabs(xd - yd);
+            const double d = xd - (double)za[e];
+            acc[1] += d * d;
+          } else if (KIND == 1) {
+            acc[0] += xd * yd;
+            acc[1] += xd * xd;
+            acc[2 % NV] += yd * yd;
+          } else {
+            acc[0] += fabs(xd - yd);
+          }
+        }
+      }
+    } else {
+      for (int j = threadIdx.x; j < cols; j += kRThreads) {
+        const double xd = a[j], yd = b[j];
+        if (KIND == 0) {
+          acc[0] += fabs(xd - yd);
+          const double d = xd - (double)c[j];
+          acc[1] += d * d;
+        } else if (KIND == 1) {
+          acc[0] += xd * yd;
+          acc[1] += xd * xd;
+          acc[2 % NV] += yd * yd;
+        } else {
+          acc[0] += fabs(xd - yd);
+        }
+      }
+    }
+  }
+  block_sum_vec<NV>(acc, scratch);
+  if (threadIdx.x == 0) {
+    double* pp = partials + ((size_t)seg * kMaxChunks + chunk) * NV;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) pp[i] = acc[i];
+    __threadfence();
+    const int done = atomicAdd(&tickets[seg], 1);
+    last = (done == chunks - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double tot[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) tot[i] = 0.0;
+    for (int ch = 0; ch < chunks; ++ch) {
+      const volatile double* pp = partials + ((size_t)seg * kMaxChunks + ch) * NV;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) tot[i] += pp[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) res[(size_t)seg * NV + i] = tot[i];
+    tickets[seg] = 0;
+  }
+}
+
+static int chunks_for(int rows, int cols, int nseg) {
+  long long elems = (long long)rows * cols;
+  int ch = (int)((elems + 32767) / 32768);  // ~32K elements per CTA
+  int per_seg_target = (4 * num_sms() + nseg - 1) / nseg;
+  if (ch > per_seg_target) ch = per_seg_target;
+  if (ch > kMaxChunks) ch = kMaxChunks;
+  if (ch > rows) ch = rows;
+  return ch < 1 ? 1 : ch;
+}
+
+static FeatP fp(QcbFeat f) { return FeatP{f.base, f.ld, f.row0}; }
+
+}  // namespace qc
+
+using namespace qc;
+
+extern "C" size_t qcb_reduce_workspace_bytes(int nseg) {
+  return (size_t)nseg * kMaxChunks * 3 * sizeof(double) + (size_t)nseg * sizeof(int) + 256;
+}
+
+template <int KIND, int NV>
+static int launch_reduce(QcbFeat a, QcbFeat b, QcbFeat c, int rows, int cols, int nseg,
+                         const int* seg_active, double* res, void* ws, void* stream) {
+  if (rows <= 0 || cols <= 0 || nseg <= 0) return QCB_ERR_DIM;
+  double* partials = reinterpret_cast<double*>(ws);
+  int* tickets = reinterpret_cast<int*>(partials + (size_t)nseg * kMaxChunks * 3);
+  const int ch = chunks_for(rows, cols, nseg);
+  seg_reduce<KIND, NV><<<dim3(ch, nseg), kRThreads, 0, (cudaStream_t)stream>>>(
+      fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch);
+  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+}
+
+extern "C" int qcb_reduce_hlc(QcbFeat out, QcbFeat ref, QcbFeat prev, int rows, int cols,
+                              int nseg, const int* seg_active, double* res, void* ws,
+                              void* stream) {
+  return launch_reduce<0, 2>(out, ref, prev, rows, cols, nseg, seg_active, res, ws, stream);
+}
+
+extern "C" int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nseg,
+                               const int* seg_active, double* res, void* ws, void* stream) {
+  return launch_reduce<1, 3>(a, b, a, rows, cols, nseg, seg_active, res, ws, stream);
+}
+
+extern "C" int qcb_reduce_l1(QcbFeat x, QcbFeat h, int rows, int cols, int nseg, double* res,
+                             void* ws, void* stream) {
+  return launch_reduce<2, 1>(x, h, x, rows, cols, nseg, nullptr, res, ws, stream);
+}
+
+// ------------------------------------------------------------------ policy
+
+namespace qc {
+
+// numpy's pairwise summation of a short f64 vector (np.add.reduce, n <= 128),
+// so redundancy_metric's np.mean is reproduced bit-for-bit.
+QC_DEV double np_pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += a[i];
+  return res;
+}
+
+QC_DEV bool live(const QcbPolicyVideo& s, int l, int t) {
+  return s.cache_valid[l] && (s.cache_step[l] - t) < s.cache_tau[l];
+}
+
+__global__ void plan_reuse_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvid) return;
+  QcbPolicyVideo& s = st[v];
+  s.boundary = (s.seen == 0 || t == 0);
+  s.long_skip = 0;
+  for (int l = 0; l < L; ++l) {
+    s.sim_valid[l] = 0;
+    s.d_valid[l] = 0;
+    s.ref_kind[l] = 0;
+    if (th.hlc && !s.boundary && live(s, l, t)) {
+      s.action[l] = QCB_ACT_REUSE;
+    } else {
+      if (th.hlc && s.cache_valid[l] && !live(s, l, t) && s.cache_tau[l] == th.tau_max)
+        s.long_skip = 1;
+      s.action[l] = QCB_ACT_RECOMPUTE;
+    }
+  }
+}
+
+__global__ void sim_mask_k(const QcbPolicyVideo* st, int nvid, int L, QcbThresholds th,
+                           int* flags) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvid) return;
+  const QcbPolicyVideo& s = st[v];
+  for (int l = 0; l < L; ++l) {
+    flags[v * L + l] = (th.srap && !s.boundary && l >= 1 && s.action[l] == QCB_ACT_RECOMPUTE &&
+                        s.prev_valid[l - 1] && s.prev_valid[l])
+                           ? 1
+                           : 0;
+  }
+}
+
+__global__ void plan_finish_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
+                              const double* srap, const double* vsum, const double* draws,
+                              long long dstride) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvid) return;
+  QcbPolicyVideo& s = st[v];
+  s.v = vsum ? vsum[v] : 0.0;
+  if (th.srap && !s.boundary) {
+    // adapt_prune_rate (schedule.py:136-141)
+    double peff;
+    if (s.v < th.v_low) peff = fmin(1.0, th.p_base * th.prune_adjust);
+    else if (s.v > th.v_high) peff = th.p_base / th.prune_adjust;
+    else peff = th.p_base;
+    for (int l = 1; l < L; ++l) {
+      if (s.action[l] != QCB_ACT_RECOMPUTE || !s.prev_valid[l - 1] || !s.prev_valid[l]) continue;
+      const double* r = srap + ((size_t)v * L + l) * 3;
+      const double na = sqrt(r[1]), nb = sqrt(r[2]);
+      const double sim = (na == 0.0 || nb == 0.0) ? 0.0 : r[0] / (na * nb);
+      s.sim[l] = sim;
+      s.sim_valid[l] = 1;
+      double p = sim > th.tau_high ? 1.0 : (sim >= th.tau_low ? peff : 0.0);
+      if (p >= 1.0 || draws[v * dstride + l] < p) s.action[l] = QCB_ACT_PRUNE;
+    }
+  }
+  s.forced = 0;
+  if (!th.aigq_a) {
+    s.abits = 32;
+  } else if (s.boundary || s.n_d == 0) {
+    s.abits = th.bit_max;
+  } else if (s.long_skip) {
+    s.abits = th.bit_max;
+    s.forced = 1;
+  } else {
+    double vals[QCB_MAX_LAYERS];
+    for (int i = 0; i < s.n_d; ++i) vals[i] = s.last_d[s.d_order[i]];
+    const double mean = np_pairwise_sum(vals, s.n_d) / (double)s.n_d;
+    const double r = 1.0 / (1.0 + mean);
+    s.abits = r >= th.theta2 ? th.bit_min : (r >= th.theta1 ? th.bit_mid : th.bit_max);
+  }
+  s.seen += 1;
+}
+
+__global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
+                          const double* hlc) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvid) return;
+  QcbPolicyVideo& s = st[v];
+  if (s.action[l] == QCB_ACT_RECOMPUTE) {
+    int k = 1;
+    int ref = 0;
+    if (s.cache_valid[l]) {
+      ref = 1;
+      k = s.cache_step[l] - t;
+      if (k < 1) k = 1;
+    } else if (s.prev_valid[l]) {
+      ref = 2;
+    }
+    int tau;
+    if (ref != 0 && s.prev_valid[l]) {
+      const double l1 = hlc[(size_t)v * 2 + 0];
+      const double l2 = sqrt(hlc[(size_t)v * 2 + 1]);
+      const double d = (l1 / (double)k) * l2;
+      if (!s.has_d[l]) {
+        s.has_d[l] = 1;
+        s.d_order[s.n_d++] = l;
+      }
+      s.last_d[l] = d;
+      tau = d < th.delta1 ? th.tau_max : (d < th.delta2 ? th.tau_mid : th.tau_min);
+      s.d_now[l] = d;
+      s.d_valid[l] = 1;
+    } else {
+      tau = 1;
+    }
+    s.ref_kind[l] = ref;
+    if (t > 0) {
+      s.cache_valid[l] = 1;
+      s.cache_step[l] = t;
+      s.cache_tau[l] = tau;
+    }
+  }
+  s.prev_valid[l] = 1;
+}
+
+}  // namespace qc
+
+static int launch_ok() { return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA; }
+
+extern "C" int qcb_policy_plan_reuse(QcbPolicyVideo* st, int nvid, int L, int t,
+                                     QcbThresholds th, void* stream) {
+  if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
+  plan_reuse_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, t, th);
+  return launch_ok();
+}
+
+extern "C" int qcb_policy_sim_mask(const QcbPolicyVideo* st, int nvid, int L, QcbThresholds th,
+                                   int* flags, void* stream) {
+  if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
+  sim_mask_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, th, flags);
+  return launch_ok();
+}
+
+extern "C" int qcb_policy_plan_finish(QcbPolicyVideo* st, int nvid, int L, int t,
+                                      QcbThresholds th, const double* srap, const double* vsum,
+                                      const double* draws, long long dstride, void* stream) {
+  if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
+  plan_finish_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, t, th, srap,
+                                                                   vsum, draws, dstride);
+  return launch_ok();
+}
+
+extern "C" int qcb_policy_observe(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
+                                  const double* hlc, void* stream) {
+  if (l < 0 || l >= QCB_MAX_LAYERS || nvid <= 0) return QCB_ERR_DIM;
+  observe_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, l, t, th, hlc);
+  return launch_ok();
+}

@@ -1,0 +1,296 @@
+"""Typed wrappers of the C ABI on CUDA torch tensors.
+
+PyTorch is used only for device memory and streams; every computation below is
+one of our sm_100a kernels in libqcb200.so.  Layout conventions:
+  * activation codes  u8  [rows][ldc], ldc = K rounded up to 16 (TMA stride)
+  * weight codes      u8  [N][ldk]   (K-major, i.e. W^T), ldk = roundup(K, 16)
+  * per-tensor activation params are per *segment* (video): f64 scale, i32 zero
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import DimensionError
+
+
+def round16(k: int) -> int:
+    return (k + 15) // 16 * 16
+
+
+def pow2_floor(n: int) -> int:
+    return 1 << (int(n).bit_length() - 1)
+
+
+def _dev() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("QuantCache B200 kernels need a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass
+class PackedWeight:
+    """Prepared quantized weight of one (layer, site) (runtime.py:40-61)."""
+    codes: torch.Tensor      # u8 [N][ldk]
+    scale: torch.Tensor      # f64 [N]
+    zero: torch.Tensor       # i32 [N]
+    colsum: torch.Tensor     # i32 [N]
+    K: int
+    N: int
+    bits: int
+    chan_scale: Optional[torch.Tensor] = None   # f64 [K] balance c (None: no transform)
+    signs: Optional[torch.Tensor] = None        # f32 [b]
+    w_deq: Optional[torch.Tensor] = None        # f32 [K][N] dequantized (weight-only mode)
+    w_eff: Optional[torch.Tensor] = None
+
+
+def weight_prep(w: torch.Tensor, bits: int, chan_scale: Optional[torch.Tensor] = None,
+                signs: Optional[torch.Tensor] = None, keep_deq: bool = False,
+                keep_eff: bool = False, stream=None) -> PackedWeight:
+    dev = _dev()
+    w = w.to(dev, torch.float32).contiguous()
+    K, Nn = w.shape
+    ldk = round16(K)
+    codes = torch.zeros((Nn, ldk), dtype=torch.uint8, device=dev)
+    scale = torch.empty(Nn, dtype=torch.float64, device=dev)
+    zero = torch.empty(Nn, dtype=torch.int32, device=dev)
+    colsum = torch.empty(Nn, dtype=torch.int32, device=dev)
+    w_deq = torch.empty((K, Nn), dtype=torch.float32, device=dev) if keep_deq else None
+    w_eff = torch.empty((K, Nn), dtype=torch.float32, device=dev) if keep_eff else None
+    if chan_scale is not None:
+        chan_scale = chan_scale.to(dev, torch.float64).contiguous()
+        signs = signs.to(dev, torch.float32).contiguous()
+    d = N.QcbWeightPrep(N.ptr(w), K, Nn, bits, N.ptr(chan_scale), N.ptr(signs), N.ptr(codes),
+                        ldk, N.ptr(scale), N.ptr(zero), N.ptr(colsum), N.ptr(w_eff),
+                        N.ptr(w_deq))
+    N.check(N.lib().qcb_weight_prep(C.byref(d), N.stream_ptr(stream)), "weight_prep")
+    return PackedWeight(codes, scale, zero, colsum, K, Nn, bits, chan_scale, signs, w_deq, w_eff)
+
+
+@dataclass
+class ActCodes:
+    codes: Optional[torch.Tensor]   # u8 [rows][ldc]
+    rowsum: Optional[torch.Tensor]  # i32 [rows]
+    scale: torch.Tensor             # f64 [nseg]
+    zero: torch.Tensor              # i32 [nseg]
+    K: int
+    xe: Optional[torch.Tensor] = None
+    deq: Optional[torch.Tensor] = None
+
+
+class Workspace:
+    """Grow-only device scratch for min/max keys and reduction partials."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=_dev())
+        return self.buf
+
+
+_WS = Workspace()
+_RWS = Workspace()
+
+
+def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
+              seg_rows: Optional[int] = None, seg_valid: Optional[int] = None,
+              nseg: int = 1, x_row0: Optional[torch.Tensor] = None,
+              ln: Optional[tuple] = None, mod: tuple = (1.0, 0.0), want_codes: bool = True,
+              want_xe: bool = False, want_deq: bool = False,
+              out: Optional[List[ActCodes]] = None, stream=None) -> List[ActCodes]:
+    """Fused [LN+mod] -> balance/rotate -> per-segment min/max -> codes.
+
+    transforms[o] = (chan_scale f64 [K], signs f32 [b]) or None (no transform).
+    ln = (gamma, beta) enables the LN prologue (None = raw rows)."""
+    dev = _dev()
+    assert x.dtype == torch.float32 and x.is_cuda
+    K = x.shape[-1]
+    ldx = x.stride(0) if x.dim() == 2 else K
+    rows_total = x.shape[0] if x.dim() == 2 else x.numel() // K
+    if seg_rows is None:
+        seg_rows = rows_total // nseg
+    seg_valid = seg_valid or seg_rows
+    if seg_rows * nseg * K == 0:
+        raise ValueError("cannot calibrate an empty tensor")
+    n_out = len(transforms)
+    rows = seg_rows * nseg
+    ldc = round16(K)
+    res = out or []
+    if not res:
+        for _ in range(n_out):
+            res.append(ActCodes(
+                torch.empty((rows, ldc), dtype=torch.uint8, device=dev) if want_codes else None,
+                torch.empty(rows, dtype=torch.int32, device=dev) if want_codes else None,
+                torch.empty(nseg, dtype=torch.float64, device=dev),
+                torch.empty(nseg, dtype=torch.int32, device=dev), K,
+                torch.empty((rows, K), dtype=torch.float32, device=dev) if want_xe else None,
+                torch.empty((rows, K), dtype=torch.float32, device=dev) if want_deq else None))
+    q = N.QcbActQuant()
+    q.x, q.ldx, q.x_row0 = N.ptr(x), ldx, N.ptr(x_row0)
+    q.K, q.seg_rows, q.seg_valid, q.nseg = K, seg_rows, seg_valid, nseg
+    if ln is not None:
+        q.prologue = N.PRO_LN_MOD
+        q.ln_g, q.ln_b = N.ptr(ln[0]), N.ptr(ln[1])
+    else:
+        q.prologue = N.PRO_NONE
+    q.mod_scale1, q.mod_shift = float(mod[0]), float(mod[1])
+    q.n_out, q.bits = n_out, bits
+    for o, tr in enumerate(transforms):
+        if tr is not None:
+            q.chan_scale[o], q.signs[o] = N.ptr(tr[0]), N.ptr(tr[1])
+        r = res[o]
+        q.codes[o], q.rowsum[o] = N.ptr(r.codes), N.ptr(r.rowsum)
+        q.scale[o], q.zero[o] = N.ptr(r.scale), N.ptr(r.zero)
+        q.xe_out[o], q.deq_out[o] = N.ptr(r.xe), N.ptr(r.deq)
+    q.ldc, q.ldxe = ldc, K
+    q.workspace = N.ptr(_WS.get(8 * 3 * nseg + 64))
+    N.check(N.lib().qcb_act_quant(C.byref(q), N.stream_ptr(stream)), "act_quant")
+    return res
+
+
+def gemm_u8(a: ActCodes, w: PackedWeight, M: Optional[int] = None, out=None,
+            epilogue: int = N.EPI_STORE, resid=None, gate: float = 1.0,
+            seg_rows: Optional[int] = None, seg_valid: Optional[int] = None,
+            out_row0=None, resid_row0=None, gate_vec=None, seg_active=None, ldo=None,
+            block_n: int = 0, stream=None) -> torch.Tensor:
+    """Quantized linear y = epilogue(f32(sa*sw[n] * acc)) on tcgen05."""
+    dev = _dev()
+    if a.K != w.K:
+        raise DimensionError(f"matmul shapes (M,{a.K}) x ({w.K},{w.N})")
+    M = M if M is not None else a.codes.shape[0]
+    if out is None:
+        dt = torch.int32 if epilogue == N.EPI_ACC else torch.float32
+        out = torch.empty((M, w.N), dtype=dt, device=dev)
+    g = N.QcbGemm()
+    g.M, g.N, g.K = M, w.N, w.K
+    g.seg_rows, g.seg_valid = seg_rows or 0, seg_valid or 0
+    g.a_codes, g.lda = N.ptr(a.codes), a.codes.stride(0)
+    g.a_scale, g.a_zero, g.a_rowsum = N.ptr(a.scale), N.ptr(a.zero), N.ptr(a.rowsum)
+    g.w_codes, g.ldw = N.ptr(w.codes), w.codes.stride(0)
+    g.w_scale, g.w_zero, g.w_colsum = N.ptr(w.scale), N.ptr(w.zero), N.ptr(w.colsum)
+    g.out, g.ldo = N.ptr(out), ldo if ldo is not None else out.stride(0)
+    g.out_row0, g.resid, g.resid_row0 = N.ptr(out_row0), N.ptr(resid), N.ptr(resid_row0)
+    g.ldr = resid.stride(0) if resid is not None else 0
+    g.gate, g.gate_scalar = N.ptr(gate_vec), float(gate)
+    g.epilogue, g.block_n, g.seg_active = epilogue, block_n, N.ptr(seg_active)
+    N.check(N.lib().qcb_gemm_u8(C.byref(g), N.stream_ptr(stream)), "gemm_u8")
+    return out
+
+
+def gemm_f64(a: torch.Tensor, w: torch.Tensor, out=None, epilogue: int = N.EPI_STORE,
+             resid=None, gate: float = 1.0, bias=None, seg_rows=None, seg_valid=None,
+             a_row0=None, out_row0=None, resid_row0=None, M=None, stream=None):
+    """Reference `mm` on device: ascending-k f64 accumulation, f32 out."""
+    dev = _dev()
+    K = a.shape[-1]
+    if w.shape[0] != K:
+        raise DimensionError(f"matmul shapes {tuple(a.shape)} x {tuple(w.shape)}")
+    M = M if M is not None else a.shape[0]
+    Nn = w.shape[1]
+    if out is None:
+        out = torch.empty((M, Nn), dtype=torch.float32, device=dev)
+    g = N.QcbGemmF64()
+    g.M, g.N, g.K = M, Nn, K
+    g.seg_rows, g.seg_valid = seg_rows or 0, seg_valid or 0
+    g.a, g.lda, g.a_row0 = N.ptr(a), a.stride(0), N.ptr(a_row0)
+    g.w, g.ldw = N.ptr(w), w.stride(0)
+    g.out, g.ldo, g.out_row0 = N.ptr(out), out.stride(0), N.ptr(out_row0)
+    g.resid, g.ldr = N.ptr(resid), resid.stride(0) if resid is not None else 0
+    g.resid_row0, g.bias = N.ptr(resid_row0), N.ptr(bias)
+    g.gate_scalar, g.epilogue = float(gate), epilogue
+    N.check(N.lib().qcb_gemm_f64(C.byref(g), N.stream_ptr(stream)), "gemm_f64")
+    return out
+
+
+def ln_mod(x: torch.Tensor, gamma=None, beta=None, scale1: float = 1.0, shift: float = 0.0,
+           out=None, seg_rows=None, seg_valid=None, nseg: int = 1, x_row0=None,
+           out_row0=None, stream=None):
+    dev = _dev()
+    K = x.shape[-1]
+    rows = seg_rows * nseg if seg_rows else x.shape[0]
+    if out is None:
+        out = torch.empty((rows, K), dtype=torch.float32, device=dev)
+    q = N.QcbLnMod(N.ptr(x), x.stride(0), N.ptr(x_row0), N.ptr(out), out.stride(0),
+                   N.ptr(out_row0), K, seg_rows or rows // nseg, seg_valid or 0, nseg,
+                   N.ptr(gamma), N.ptr(beta), float(scale1), float(shift))
+    N.check(N.lib().qcb_ln_mod(C.byref(q), N.stream_ptr(stream)), "ln_mod")
+    return out
+
+
+def attention_f64(q, k, v, heads: int, out=None, nseg: int = 1, S=None, Skv=None,
+                  seg_valid=None, stream=None):
+    """Per-head attention with f64 softmax (reference _mha)."""
+    dev = _dev()
+    d = q.shape[-1]
+    S = S or q.shape[0] // nseg
+    Skv = Skv or k.shape[0] // nseg
+    if out is None:
+        out = torch.empty((S * nseg, d), dtype=torch.float32, device=dev)
+    a = N.QcbAttention(N.ptr(q), q.stride(0), N.ptr(k), k.stride(0), N.ptr(v), v.stride(0),
+                       N.ptr(out), out.stride(0), S, Skv, heads, d // heads, nseg, S, Skv, S,
+                       seg_valid or 0)
+    N.check(N.lib().qcb_attention_f64(C.byref(a), N.stream_ptr(stream)), "attention")
+    return out
+
+
+def ddpm(x, eps, c1: float, c2: float, noise=None, c3: float = 0.0, out=None, stream=None):
+    if out is None:
+        out = torch.empty_like(x)
+    d = N.QcbDdpm(N.ptr(x), N.ptr(eps), N.ptr(noise), N.ptr(out), x.numel(), c1, c2, c3)
+    N.check(N.lib().qcb_ddpm_step(C.byref(d), N.stream_ptr(stream)), "ddpm_step")
+    return out
+
+
+def feat(t: Optional[torch.Tensor], row0=None, ld=None) -> N.QcbFeat:
+    if t is None:
+        return N.QcbFeat(0, 0, 0)
+    return N.QcbFeat(N.ptr(t), ld if ld is not None else t.stride(0), N.ptr(row0))
+
+
+def _rws(nseg):
+    return N.ptr(_RWS.get(int(N.lib().qcb_reduce_workspace_bytes(nseg))))
+
+
+def reduce_hlc(out: N.QcbFeat, ref: N.QcbFeat, prev: N.QcbFeat, rows: int, cols: int,
+               nseg: int, res: torch.Tensor, seg_active=None, stream=None):
+    N.check(N.lib().qcb_reduce_hlc(out, ref, prev, rows, cols, nseg, N.ptr(seg_active),
+                                   N.ptr(res), _rws(nseg), N.stream_ptr(stream)), "reduce_hlc")
+    return res
+
+
+def reduce_srap(a: N.QcbFeat, b: N.QcbFeat, rows: int, cols: int, nseg: int,
+                res: torch.Tensor, seg_active=None, stream=None):
+    N.check(N.lib().qcb_reduce_srap(a, b, rows, cols, nseg, N.ptr(seg_active), N.ptr(res),
+                                    _rws(nseg), N.stream_ptr(stream)), "reduce_srap")
+    return res
+
+
+def reduce_l1(x: N.QcbFeat, h: N.QcbFeat, rows: int, cols: int, nseg: int,
+              res: torch.Tensor, stream=None):
+    N.check(N.lib().qcb_reduce_l1(x, h, rows, cols, nseg, N.ptr(res), _rws(nseg),
+                                  N.stream_ptr(stream)), "reduce_l1")
+    return res
+
+
+def thresholds_struct(th, toggles) -> N.QcbThresholds:
+    return N.QcbThresholds(
+        float(th.delta1), float(th.delta2), int(th.tau_max), int(th.tau_mid), int(th.tau_min),
+        float(th.theta1), float(th.theta2), int(th.bit_max), int(th.bit_mid), int(th.bit_min),
+        float(th.tau_high), float(th.tau_low), float(th.p_base), float(th.v_low),
+        float(th.v_high), int(th.history_k), float(th.prune_adjust), int(toggles.hlc),
+        int(toggles.aigq_weights), int(toggles.aigq_acts), int(toggles.srap))
+
+
+def sign_vector(seed: int, b: int) -> np.ndarray:
+    """+-1 signs of the randomized Hadamard block (reference quant.py:155-158);
+    NumPy's PCG64 is the RNG source so the block matches the reference."""
+    u = np.random.default_rng(seed).random(b)
+    return np.where(u < 0.5, -1.0, 1.0).astype(np.float32)

@@ -1,0 +1,322 @@
+"""Device kernels vs the CPU oracle / reference golden fixtures, through the C ABI.
+
+Bar: bit-exact for codes, params and integer accumulators; bit-exact f32
+outputs for the GEMM epilogue (the reference's f64 sum equals the single
+rounding whenever its partial sums are exact -- pinned on these fixtures)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import qc_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def D(cuda_dev):
+    from paper_2503_06545_b200 import device
+    return device
+
+
+def t(a, dt=None):
+    x = torch.from_numpy(np.ascontiguousarray(a))
+    if dt is not None:
+        x = x.to(dt)
+    return x.cuda()
+
+
+def act_from_codes(D, codes, s, z):
+    """Device ActCodes from host codes (test-side construction)."""
+    M, K = codes.shape
+    buf = np.zeros((M, D.round16(K)), np.uint8)
+    buf[:, :K] = codes
+    return D.ActCodes(t(buf), t(codes.astype(np.int64).sum(1).astype(np.int32)),
+                      t(np.array([s], np.float64)), t(np.array([z], np.int32)), K)
+
+
+def packed_from_codes(D, codes_kn, s, z, bits=8):
+    """Device PackedWeight from host [K][N] codes."""
+    K, Nn = codes_kn.shape
+    buf = np.zeros((Nn, D.round16(K)), np.uint8)
+    buf[:, :K] = codes_kn.T
+    return D.PackedWeight(t(buf), t(np.asarray(s, np.float64)), t(np.asarray(z, np.int32)),
+                          t(codes_kn.astype(np.int64).sum(0).astype(np.int32)), K, Nn, bits)
+
+
+class TestGemmU8:
+    def test_criterion5_fixtures_exact(self, D, golden_dir):
+        f = np.load(os.path.join(golden_dir, "matmul_int.npz"))
+        from paper_2503_06545_b200 import _native as N
+        for n in range(int(f["count"])):
+            ca, cw = f[f"ca{n}"], f[f"cw{n}"]
+            sa, za = float(f[f"sa{n}"]), int(f[f"za{n}"])
+            a = act_from_codes(D, ca, sa, za)
+            w = packed_from_codes(D, cw, f[f"sw{n}"], f[f"zw{n}"])
+            acc = D.gemm_u8(a, w, epilogue=N.EPI_ACC).cpu().numpy()
+            assert np.array_equal(acc, O.int_acc(ca, za, cw, f[f"zw{n}"])), n
+            out = D.gemm_u8(a, w).cpu().numpy()
+            assert np.array_equal(out, f[f"out{n}"]), n
+
+    @pytest.mark.parametrize("name", ["qkv", "fc1", "fc2", "w4a6"])
+    def test_c2_slices_exact(self, D, golden_dir, name):
+        f = np.load(os.path.join(golden_dir, "matmul_int.npz"))
+        ca, cw = f[f"{name}_ca"], f[f"{name}_cw"]
+        a = act_from_codes(D, ca, float(f[f"{name}_sa"]), int(f[f"{name}_za"]))
+        w = packed_from_codes(D, cw, f[f"{name}_sw"], f[f"{name}_zw"])
+        out = D.gemm_u8(a, w).cpu().numpy()
+        assert np.array_equal(out, f[f"{name}_out"])
+
+    @pytest.mark.parametrize("M,K,N,bn", [(2048, 1152, 1152, 0), (1024, 4608, 1152, 0),
+                                          (640, 1152, 4608, 256), (300, 200, 72, 0),
+                                          (256, 1152, 1152, 128), (256, 1152, 1152, 64)])
+    def test_random_accumulators_exact(self, D, M, K, N, bn):
+        from paper_2503_06545_b200 import _native as Nat
+        rng = np.random.default_rng(M + K + N)
+        ca = rng.integers(0, 256, size=(M, K), dtype=np.int64)
+        cw = rng.integers(0, 256, size=(K, N), dtype=np.int64)
+        za, zw = 117, rng.integers(0, 256, size=N)
+        a = act_from_codes(D, ca.astype(np.uint8), 0.01, za)
+        w = packed_from_codes(D, cw.astype(np.uint8), np.full(N, 0.02), zw)
+        acc = D.gemm_u8(a, w, epilogue=Nat.EPI_ACC, block_n=bn).cpu().numpy()
+        rows = np.r_[0:64, M - 64:M]
+        assert np.array_equal(acc[rows], O.int_acc(ca[rows], za, cw, zw))
+        # full check via exact f64 products of integers (< 2^53)
+        full = (torch.from_numpy((ca - za).astype(np.float64)).cuda() @
+                torch.from_numpy((cw - zw[None]).astype(np.float64)).cuda()).cpu().numpy()
+        assert np.array_equal(acc.astype(np.float64), full)
+
+    def test_segments_and_epilogues(self, D):
+        """Per-video params, padded segments, GELU / gate+residual / residual."""
+        from paper_2503_06545_b200 import _native as Nat
+        rng = np.random.default_rng(3)
+        S, Spad, nseg, K, N = 100, 128, 3, 256, 96
+        ca = rng.integers(0, 64, size=(nseg * Spad, K)).astype(np.uint8)
+        cw = rng.integers(0, 64, size=(K, N)).astype(np.uint8)
+        sa = np.array([2.0 ** -7, 3.0 * 2.0 ** -9, 0.015625], np.float64)
+        za = np.array([3, 40, 17], np.int32)
+        sw = O.scale_up16(rng.uniform(1e-3, 1e-2, size=N))
+        zw = rng.integers(0, 64, size=N).astype(np.int32)
+        a = D.ActCodes(t(np.pad(ca, ((0, 0), (0, D.round16(K) - K)))),
+                       t(ca.astype(np.int64).sum(1).astype(np.int32)), t(sa), t(za), K)
+        w = packed_from_codes(D, cw, sw, zw)
+        resid = rng.standard_normal((nseg * Spad, N)).astype(np.float32)
+        want_y = np.concatenate([O.matmul_int_single_rounding(
+            ca[v * Spad:(v + 1) * Spad], sa[v], za[v], cw, sw, zw) for v in range(nseg)])
+        for mode in (Nat.EPI_STORE, Nat.EPI_GELU, Nat.EPI_GATE_RESID, Nat.EPI_RESID):
+            out = torch.zeros((nseg * Spad, N), dtype=torch.float32, device="cuda")
+            D.gemm_u8(a, w, out=out, epilogue=mode, resid=t(resid), gate=np.float32(0.37),
+                      seg_rows=Spad, seg_valid=S)
+            got = out.cpu().numpy()
+            if mode == Nat.EPI_STORE:
+                want = want_y
+            elif mode == Nat.EPI_GELU:
+                want = O.gelu64(want_y)
+            elif mode == Nat.EPI_GATE_RESID:
+                want = resid + np.float32(0.37) * want_y
+            else:
+                want = resid + want_y
+            for v in range(nseg):
+                sl = slice(v * Spad, v * Spad + S)
+                assert np.array_equal(got[sl], want[sl]), (mode, v)
+                assert not got[v * Spad + S:(v + 1) * Spad].any()   # padding untouched
+
+    def test_overflow_guard(self, D):
+        from paper_2503_06545_b200.errors import ConfigurationError
+        K = 40000
+        a = D.ActCodes(torch.zeros((128, D.round16(K)), dtype=torch.uint8, device="cuda"),
+                       torch.zeros(128, dtype=torch.int32, device="cuda"),
+                       torch.ones(1, dtype=torch.float64, device="cuda"),
+                       torch.zeros(1, dtype=torch.int32, device="cuda"), K)
+        w = D.PackedWeight(torch.zeros((32, D.round16(K)), dtype=torch.uint8, device="cuda"),
+                           torch.ones(32, dtype=torch.float64, device="cuda"),
+                           torch.zeros(32, dtype=torch.int32, device="cuda"),
+                           torch.zeros(32, dtype=torch.int32, device="cuda"), K, 32, 8)
+        with pytest.raises(ConfigurationError):
+            D.gemm_u8(a, w)
+
+
+class TestActQuant:
+    def test_quantizer_fixtures(self, D, golden_dir):
+        f = np.load(os.path.join(golden_dir, "quantizer.npz"))
+        cases = json.load(open(os.path.join(golden_dir, "quantizer_cases.json")))
+        for c in cases:
+            i = c["i"]
+            x = f["ties_x"].reshape(1, -1) if i == "ties" else f[f"x{i}"]
+            want = (f["ties_codes"].reshape(1, -1) if i == "ties" else f[f"codes{i}"])
+            (r,) = D.act_quant(t(x), c["bits"], [None], want_deq=True)
+            assert float(r.scale.item()) == c["s"] and int(r.zero.item()) == c["z"], i
+            K = x.shape[1]
+            assert np.array_equal(r.codes.cpu().numpy()[:, :K], want), i
+            assert np.array_equal(r.rowsum.cpu().numpy(), want.astype(np.int64).sum(1)), i
+            if i != "ties":
+                assert np.array_equal(r.deq.cpu().numpy(), f[f"deq{i}"]), i
+
+    def test_rotation_fixtures(self, D, golden_dir):
+        f = np.load(os.path.join(golden_dir, "rotation.npz"))
+        i = 0
+        while f"x{i}" in f:
+            x, c, seed = f[f"x{i}"], f[f"c{i}"], int(f[f"seed{i}"])
+            K = x.shape[1]
+            signs = D.sign_vector(seed, D.pow2_floor(K))
+            for bits in (8, 6, 4):
+                (r,) = D.act_quant(t(x), bits, [(t(c), t(signs))], want_xe=True)
+                xe = r.xe.cpu().numpy()
+                assert np.array_equal(xe, f[f"xe{i}"]), (i, bits)
+                s, z = O.act_params(xe, bits)
+                assert (float(r.scale.item()), int(r.zero.item())) == (s, z)
+                assert np.array_equal(r.codes.cpu().numpy()[:, :K], O.codes_of(xe, s, z, bits))
+            i += 1
+
+    def test_ln_mod_prologue_three_outputs(self, D):
+        rng = np.random.default_rng(11)
+        S, K, nseg = 64, 1152, 2
+        x = (rng.standard_normal((nseg * S, K)) * 3 + 0.5).astype(np.float32)
+        g = rng.uniform(0.5, 1.5, K).astype(np.float32)
+        b = rng.standard_normal(K).astype(np.float32) * 0.1
+        s1, sh = np.float32(1.0) + np.float32(0.173), np.float32(-0.31)
+        trs = []
+        for o in range(3):
+            c = rng.uniform(0.1, 4.0, K)
+            trs.append((c, D.sign_vector(7 + o, 1024)))
+        res = D.act_quant(t(x), 6, [(t(c), t(sg)) for c, sg in trs], nseg=nseg,
+                          ln=(t(g), t(b)), mod=(s1, sh), want_xe=True)
+        for v in range(nseg):
+            xv = x[v * S:(v + 1) * S]
+            h = O.ln64(xv, g, b) * s1 + sh
+            for o, (c, sg) in enumerate(trs):
+                xe_want = O.rotate_act_fwht(h, c, 7 + o)
+                xe = res[o].xe.cpu().numpy()[v * S:(v + 1) * S]
+                assert np.array_equal(xe, xe_want), (v, o)
+                s, z = O.act_params(xe_want, 6)
+                assert float(res[o].scale[v]) == s and int(res[o].zero[v]) == z
+                codes = res[o].codes.cpu().numpy()[v * S:(v + 1) * S, :K]
+                assert np.array_equal(codes, O.codes_of(xe_want, s, z, 6))
+
+
+class TestWeightPrep:
+    def test_rotation_and_channel_quant(self, D, golden_dir):
+        f = np.load(os.path.join(golden_dir, "rotation.npz"))
+        i = 0
+        while f"x{i}" in f:
+            if f"we{i}" in f:
+                w, c, seed = f[f"w{i}"], f[f"c{i}"], int(f[f"seed{i}"])
+                K = w.shape[0]
+                signs = D.sign_vector(seed, D.pow2_floor(K))
+                for bits in (8, 6, 4):
+                    pw = D.weight_prep(t(w), bits, t(c), t(signs), keep_eff=True, keep_deq=True)
+                    weff = pw.w_eff.cpu().numpy()
+                    assert np.array_equal(weff, f[f"we{i}"]), (i, bits)
+                    s, z = O.chan_params(weff, bits)
+                    assert np.array_equal(pw.scale.cpu().numpy(), s)
+                    assert np.array_equal(pw.zero.cpu().numpy(), z)
+                    codes = O.codes_of(weff, s[None], z[None], bits)
+                    assert np.array_equal(pw.codes.cpu().numpy()[:, :K], codes.T)
+                    assert np.array_equal(pw.colsum.cpu().numpy(), codes.sum(0))
+                    assert np.array_equal(pw.w_deq.cpu().numpy(), O.dequant(codes, s[None], z[None]))
+            i += 1
+
+
+class TestSiteFixtures:
+    def test_every_hook_call_of_a_quantized_step(self, D, golden_dir):
+        """The reference's QuantRuntime.gemm_fn outputs on the small config,
+        reproduced by weight_prep -> act_quant -> gemm_u8 on identical inputs."""
+        f = np.load(os.path.join(golden_dir, "gemm_sites.npz"))
+        meta = json.load(open(os.path.join(golden_dir, "gemm_sites.json")))
+        seed = meta["sign_seed"]
+        blocks, _, _ = O.init_weights(O.ModelDims(3, 16, 2, 4, 2, 8, 3))
+        packed = {}
+        for call in meta["calls"]:
+            l, site, ab = call["layer"], call["site"], call["abits"]
+            key = (l, site)
+            c = f[f"w_{l}_{site}_c"]
+            K = c.shape[0]
+            signs = D.sign_vector(seed, D.pow2_floor(K))
+            if key not in packed:
+                packed[key] = D.weight_prep(t(blocks[l][site]), call["wbits"], t(c), t(signs))
+                assert np.array_equal(packed[key].codes.cpu().numpy()[:, :K],
+                                      f[f"w_{l}_{site}_codes"].T)
+            k = call["key"]
+            (a,) = D.act_quant(t(f[k + "_x"]), ab, [(t(c), t(signs))])
+            assert float(a.scale.item()) == call["s"] and int(a.zero.item()) == call["z"]
+            assert np.array_equal(a.codes.cpu().numpy()[:, :K], f[k + "_codes"])
+            out = D.gemm_u8(a, packed[key]).cpu().numpy()
+            assert np.array_equal(out, f[k + "_out"]), (l, site, ab)
+
+
+class TestFp:
+    def test_gemm_f64_matches_seq_mm(self, D):
+        rng = np.random.default_rng(5)
+        for (m, k, n) in [(3, 4, 5), (64, 64, 256), (70, 256, 64), (1, 8, 16)]:
+            a = rng.standard_normal((m, k)).astype(np.float32)
+            w = rng.standard_normal((k, n)).astype(np.float32)
+            assert np.array_equal(D.gemm_f64(t(a), t(w)).cpu().numpy(), O.seq_mm(a, w))
+
+    def test_attention_matches_reference(self, D):
+        rng = np.random.default_rng(6)
+        for S, Skv, d, h in [(8, 8, 16, 2), (64, 64, 64, 4), (64, 1, 64, 4), (200, 200, 32, 2)]:
+            q, k, v = (rng.standard_normal((n, d)).astype(np.float32) for n in (S, Skv, Skv))
+            got = D.attention_f64(t(q), t(k), t(v), h).cpu().numpy()
+            want = O.attention_heads(q, k, v, h)
+            np.testing.assert_allclose(got, want, rtol=0, atol=2e-7 * np.abs(want).max())
+
+    def test_ln_mod(self, D):
+        rng = np.random.default_rng(7)
+        x = rng.standard_normal((64, 64)).astype(np.float32) * 2
+        got = D.ln_mod(t(x), scale1=np.float32(1.25), shift=np.float32(0.5)).cpu().numpy()
+        want = O.ln64(x, np.ones(64, np.float32), np.zeros(64, np.float32)) * np.float32(1.25) \
+            + np.float32(0.5)
+        assert np.array_equal(got, want)
+
+    def test_ddpm(self, D):
+        rng = np.random.default_rng(8)
+        ab = O.alpha_bar(10)
+        x, e, n = (rng.standard_normal((4, 16, 8)).astype(np.float32) for _ in range(3))
+        for tt in (9, 5, 2, 1):
+            a_t, a_p = ab[tt], ab[tt - 1]
+            alpha = a_t / a_p
+            beta = 1.0 - alpha
+            c3 = float(np.sqrt((1.0 - a_p) / (1.0 - a_t) * beta)) if tt > 1 else 0.0
+            got = D.ddpm(t(x), t(e), beta / np.sqrt(1.0 - a_t), float(np.sqrt(alpha)),
+                         t(n) if tt > 1 else None, c3).cpu().numpy()
+            assert np.array_equal(got, O.ddpm_step(x, tt, e, ab, n))
+        got = D.ddpm(t(x), t(e), float(np.sqrt(1.0 - ab[0])), float(np.sqrt(ab[0]))).cpu().numpy()
+        assert np.array_equal(got, O.ddpm_final(x, e, ab))
+
+
+class TestReductions:
+    def test_hlc_srap_l1(self, D):
+        rng = np.random.default_rng(9)
+        S, d, nseg = 4096, 1152, 2
+        a, b, c = (rng.standard_normal((nseg * S, d)).astype(np.float32) for _ in range(3))
+        res = torch.zeros(nseg * 3, dtype=torch.float64, device="cuda")
+        D.reduce_hlc(D.feat(t(a)), D.feat(t(b)), D.feat(t(c)), S, d, nseg, res)
+        r = res.cpu().numpy()
+        for v in range(nseg):
+            sl = slice(v * S, (v + 1) * S)
+            dd = O.divergence(a[sl], b[sl], 3, c[sl])
+            assert (r[2 * v] / 3) * np.sqrt(r[2 * v + 1]) == pytest.approx(dd, rel=1e-12)
+        D.reduce_srap(D.feat(t(a)), D.feat(t(b)), S, d, nseg, res)
+        r = res.cpu().numpy()
+        for v in range(nseg):
+            sl = slice(v * S, (v + 1) * S)
+            s = r[3 * v] / (np.sqrt(r[3 * v + 1]) * np.sqrt(r[3 * v + 2]))
+            assert s == pytest.approx(O.similarity(a[sl], b[sl]), rel=1e-12, abs=1e-15)
+        D.reduce_l1(D.feat(t(a)), D.feat(t(b)), S, d, nseg, res)
+        r = res.cpu().numpy()
+        for v in range(nseg):
+            sl = slice(v * S, (v + 1) * S)
+            assert r[v] == pytest.approx(O.variation([b[sl]], a[sl]), rel=1e-12)
+
+    def test_deterministic(self, D):
+        rng = np.random.default_rng(10)
+        a, b, c = (t(rng.standard_normal((4096, 1152)).astype(np.float32)) for _ in range(3))
+        r1 = torch.zeros(2, dtype=torch.float64, device="cuda")
+        r2 = torch.zeros(2, dtype=torch.float64, device="cuda")
+        D.reduce_hlc(D.feat(a), D.feat(b), D.feat(c), 4096, 1152, 1, r1)
+        D.reduce_hlc(D.feat(a), D.feat(b), D.feat(c), 4096, 1152, 1, r2)
+        assert torch.equal(r1, r2)
