@@ -250,16 +250,18 @@ enum { QCB_ACT_RECOMPUTE = 0, QCB_ACT_REUSE = 1, QCB_ACT_PRUNE = 2 };
 int qcb_policy_plan_reuse(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
                           void* stream);
 /* Which (video, layer) pairs need an SRAP similarity this step:
- * flags[v*L + l] = 1 iff srap on, not boundary, l >= 1, action recompute and
- * both previous features exist (schedule.py:296-304). */
+ * flags[l*nvid + v] = 1 iff srap on, not boundary, l >= 1, action recompute
+ * and both previous features exist (schedule.py:296-304). */
 int qcb_policy_sim_mask(const QcbPolicyVideo* st, int nvid, int L, QcbThresholds th,
                         int* flags, void* stream);
-/* plan_step part 2: SRAP prune decisions from srap sums [v][L][3] and the
- * variation v_sum[v], activation bits (schedule.py:293-326). draws: [L] f64
- * (prune_draw(seed, t, l) for this t), per video row stride L. */
+/* plan_step part 2: SRAP prune decisions from srap sums [L][nvid][3], the
+ * variation V = sum_j hist_l1[j*nvid + v] over the n_hist history latents in
+ * insertion order (schedule.py:128-133), and the activation bits
+ * (schedule.py:293-326).  draws: prune_draw(seed_v, t, l) at
+ * draws[v*draws_vid_stride + l]. */
 int qcb_policy_plan_finish(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
-                           const double* srap_sums, const double* v_sum, const double* draws,
-                           long long draws_vid_stride, void* stream);
+                           const double* srap_sums, const double* hist_l1, int n_hist,
+                           const double* draws, long long draws_vid_stride, void* stream);
 /* observe_block for layer l: hlc sums [v][2] (valid where ref_kind != 0),
  * k per video from cache step; tau / cache / prev / last_d updates
  * (schedule.py:330-351). */
@@ -269,6 +271,7 @@ int qcb_policy_observe(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds
 /* ---------------------------------------------------------------- misc */
 int qcb_device_sm_count(void);
 const char* qcb_version(void);
+const char* qcb_last_error(void);
 
 #ifdef __cplusplus
 }

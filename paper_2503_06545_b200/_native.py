@@ -128,7 +128,7 @@ def lib():
         "qcb_reduce_l1": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp],
         "qcb_policy_plan_reuse": [vp, i32, i32, i32, QcbThresholds, vp],
         "qcb_policy_sim_mask": [vp, i32, i32, QcbThresholds, vp, vp],
-        "qcb_policy_plan_finish": [vp, i32, i32, i32, QcbThresholds, vp, vp, vp, i64, vp],
+        "qcb_policy_plan_finish": [vp, i32, i32, i32, QcbThresholds, vp, vp, i32, vp, i64, vp],
         "qcb_policy_observe": [vp, i32, i32, i32, QcbThresholds, vp, vp],
     }
     for name, args in sigs.items():
@@ -139,6 +139,7 @@ def lib():
     h.qcb_reduce_workspace_bytes.restype = C.c_size_t
     h.qcb_device_sm_count.restype = C.c_int
     h.qcb_version.restype = C.c_char_p
+    h.qcb_last_error.restype = C.c_char_p
     _lib = h
     return h
 
@@ -147,7 +148,7 @@ EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_act_quant", "qcb_weight_prep", "
             "qcb_attention_f64", "qcb_ddpm_step", "qcb_reduce_hlc", "qcb_reduce_srap",
             "qcb_reduce_l1", "qcb_reduce_workspace_bytes", "qcb_policy_plan_reuse",
             "qcb_policy_sim_mask", "qcb_policy_plan_finish", "qcb_policy_observe",
-            "qcb_device_sm_count", "qcb_version")
+            "qcb_device_sm_count", "qcb_version", "qcb_last_error")
 
 
 def check(rc: int, what: str):
@@ -164,7 +165,8 @@ def check(rc: int, what: str):
         raise ValueError(msg)
     if rc == QCB_ERR_TYPE:
         raise TypeError(msg)
-    raise RuntimeError(msg + " (CUDA error)")
+    err = _lib.qcb_last_error().decode() if _lib is not None else "?"
+    raise RuntimeError(msg + f" (CUDA error: {err})")
 
 
 def ptr(t) -> int:

@@ -83,3 +83,7 @@ extern "C" int qcb_ddpm_step(const QcbDdpm* d, void* stream) {
 extern "C" int qcb_device_sm_count(void) { return num_sms(); }
 
 extern "C" const char* qcb_version(void) { return "qcb200 0.1.0 sm_100a"; }
+
+extern "C" const char* qcb_last_error(void) {
+  return cudaGetErrorString(cudaPeekAtLastError());
+}

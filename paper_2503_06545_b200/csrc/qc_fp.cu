@@ -19,7 +19,6 @@ struct GemmF64P {
   QcbGemmF64 g;
 };
 
-QC_DEV double gelu64(double x) { return 0.5 * x * (1.0 + erf(x / 1.4142135623730951)); }
 
 __global__ void __launch_bounds__(256) gemm_f64_k(const GemmF64P P) {
   const QcbGemmF64& g = P.g;
@@ -77,7 +76,7 @@ __global__ void __launch_bounds__(256) gemm_f64_k(const GemmF64P P) {
       if (n >= g.N) continue;
       float y = __double2float_rn(acc[i][j]);
       switch (g.epilogue) {
-        case QCB_EPI_GELU: y = __double2float_rn(gelu64((double)y)); break;
+        case QCB_EPI_GELU: y = __double2float_rn(gelu_ref((double)y)); break;
         case QCB_EPI_GATE_RESID:
           y = __fadd_rn(g.resid[rrow * g.ldr + n], __fmul_rn(g.gate_scalar, y));
           break;

@@ -33,7 +33,7 @@ constexpr int kThreads = 256;
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN >= 192 ? 5 : (BN >= 128 ? 6 : 8);
+  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 192 ? 5 : (BN >= 128 ? 6 : 8));
   static constexpr int kABytes = kBlockM * kBlockK;
   static constexpr int kBBytes = BN * kBlockK;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -68,10 +68,6 @@ struct GemmParams {
   const int* seg_active;  // nullable: skip tiles of inactive segments
 };
 
-QC_DEV double gelu_exact(double x) {
-  // 0.5 x (1 + erf(x / sqrt(2))) in f64 (model.py:145-147)
-  return 0.5 * x * (1.0 + erf(x / 1.4142135623730951));
-}
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -243,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const double joint = __dmul_rn(sa, __ldg(p.sw + n));
                   y = __double2float_rn(__dmul_rn(joint, (double)accv));
                   if (p.mode == QCB_EPI_GELU) {
-                    y = __double2float_rn(gelu_exact((double)y));
+                    y = __double2float_rn(gelu_ref((double)y));
                   } else if (p.mode == QCB_EPI_GATE_RESID) {
                     y = __fadd_rn(rv[e], __fmul_rn(gate, y));
                   } else if (p.mode == QCB_EPI_RESID) {
@@ -352,10 +348,12 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st) {
   p.gate_scalar = g->gate_scalar;
   p.mode = g->epilogue;
   p.seg_active = g->seg_active;
+  static_assert(Cfg::kSmemBytes <= 227 * 1024, "GEMM smem budget exceeds 227 KB");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_u8_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg::kSmemBytes);
+    if (cudaFuncSetAttribute(gemm_u8_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::kSmemBytes) != cudaSuccess)
+      return QCB_ERR_CUDA;
     attr_set = true;
   }
   int tiles = p.num_m_tiles * p.num_n_tiles;

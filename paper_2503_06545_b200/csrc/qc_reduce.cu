@@ -235,7 +235,7 @@ __global__ void sim_mask_k(const QcbPolicyVideo* st, int nvid, int L, QcbThresho
   if (v >= nvid) return;
   const QcbPolicyVideo& s = st[v];
   for (int l = 0; l < L; ++l) {
-    flags[v * L + l] = (th.srap && !s.boundary && l >= 1 && s.action[l] == QCB_ACT_RECOMPUTE &&
+    flags[l * nvid + v] = (th.srap && !s.boundary && l >= 1 && s.action[l] == QCB_ACT_RECOMPUTE &&
                         s.prev_valid[l - 1] && s.prev_valid[l])
                            ? 1
                            : 0;
@@ -243,12 +243,14 @@ __global__ void sim_mask_k(const QcbPolicyVideo* st, int nvid, int L, QcbThresho
 }
 
 __global__ void plan_finish_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
-                              const double* srap, const double* vsum, const double* draws,
-                              long long dstride) {
+                              const double* srap, const double* hist_l1, int n_hist,
+                              const double* draws, long long dstride) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nvid) return;
   QcbPolicyVideo& s = st[v];
-  s.v = vsum ? vsum[v] : 0.0;
+  double total = 0.0;
+  for (int j = 0; j < n_hist; ++j) total += hist_l1[(size_t)j * nvid + v];
+  s.v = total;
   if (th.srap && !s.boundary) {
     // adapt_prune_rate (schedule.py:136-141)
     double peff;
@@ -257,7 +259,7 @@ __global__ void plan_finish_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThr
     else peff = th.p_base;
     for (int l = 1; l < L; ++l) {
       if (s.action[l] != QCB_ACT_RECOMPUTE || !s.prev_valid[l - 1] || !s.prev_valid[l]) continue;
-      const double* r = srap + ((size_t)v * L + l) * 3;
+      const double* r = srap + ((size_t)l * nvid + v) * 3;
       const double na = sqrt(r[1]), nb = sqrt(r[2]);
       const double sim = (na == 0.0 || nb == 0.0) ? 0.0 : r[0] / (na * nb);
       s.sim[l] = sim;
@@ -344,11 +346,12 @@ extern "C" int qcb_policy_sim_mask(const QcbPolicyVideo* st, int nvid, int L, Qc
 }
 
 extern "C" int qcb_policy_plan_finish(QcbPolicyVideo* st, int nvid, int L, int t,
-                                      QcbThresholds th, const double* srap, const double* vsum,
-                                      const double* draws, long long dstride, void* stream) {
-  if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
-  plan_finish_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, t, th, srap,
-                                                                   vsum, draws, dstride);
+                                      QcbThresholds th, const double* srap,
+                                      const double* hist_l1, int n_hist, const double* draws,
+                                      long long dstride, void* stream) {
+  if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0 || n_hist < 0) return QCB_ERR_DIM;
+  plan_finish_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(
+      st, nvid, L, t, th, srap, hist_l1, n_hist, draws, dstride);
   return launch_ok();
 }
 

@@ -150,7 +150,15 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
         q.codes[o], q.rowsum[o] = N.ptr(r.codes), N.ptr(r.rowsum)
         q.scale[o], q.zero[o] = N.ptr(r.scale), N.ptr(r.zero)
         q.xe_out[o], q.deq_out[o] = N.ptr(r.xe), N.ptr(r.deq)
-    q.ldc, q.ldxe = ldc, K
+    if res[0].codes is not None:
+        ldc = res[0].codes.stride(0)
+        assert all(r.codes is None or r.codes.stride(0) == ldc for r in res)
+    ldxe = K
+    for r in res:
+        for buf in (r.xe, r.deq):
+            if buf is not None:
+                ldxe = buf.stride(0)
+    q.ldc, q.ldxe = ldc, ldxe
     q.workspace = N.ptr(_WS.get(8 * 3 * nseg + 64))
     N.check(N.lib().qcb_act_quant(C.byref(q), N.stream_ptr(stream)), "act_quant")
     return res

@@ -1,0 +1,529 @@
+"""Device engine for QuantCache sampling: the reference's `generate` loop
+(sampler.py:91-134) with `Scheduler` decisions (schedule.py:281-351) and the
+`QuantRuntime` GEMM hook (runtime.py:63-81) executed by libqcb200 kernels.
+
+Data layout in HBM
+  * residual-stream ARENA  f32 [nvid * P * S_pad][d]: every block output, cache
+    entry, previous-step feature and latent lives in a slot of S_pad rows.
+    Cache reuse and layer pruning are zero-copy: the host refcounts slots per
+    video exactly like the reference's Python references (a pruned layer's
+    `prev` aliases its input, a reused layer's output *is* the cache entry;
+    schedule.py:337-351, sampler.py:150-156).  No buffer is mutated while a
+    cache entry or prev feature refers to it.
+  * per-step scratch for the active videos: u8 codes [rows][roundup16(K)],
+    f32 q/k/v/attention/hidden, row sums, per-video scale/zero.
+  * device policy state QcbPolicyVideo[nvid] (cache steps/taus, last D, prev
+    flags, the step's actions) + prune-draw table + reduction results.
+
+Per step: V reductions -> plan_reuse -> SRAP reductions -> plan_finish on the
+device, ONE device->host copy of the plan (actions, bits) so the host can
+dispatch only recomputed blocks, then per layer the block kernels for the
+recomputing videos, the HLC reduction and the device observe kernel.  Trace
+values (D, S, V) stay on device until the end of the run.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as Dv
+from .model import QUANT_SITES, DiTModel, block_mac_cost, head_mac_cost, timestep_embedding
+from .schedule import FP_BITS, ThresholdConfig, Toggles, TraceRecord, billed_macs, \
+    prune_draw_table
+
+ACTION_NAMES = ("recompute", "reuse", "prune")
+
+
+def balance_scales(w: np.ndarray, act_absmax: np.ndarray) -> np.ndarray:
+    """c_j = clip(sqrt(absmax_x / absmax_w), 1e-3, 1e3), 1 for dead channels
+    (reference quant.py:179-200); host-side offline prep of K scalars."""
+    w64 = np.asarray(w, np.float64)
+    st = np.asarray(act_absmax, np.float64)
+    if st.shape != (w64.shape[0],):
+        from .errors import ConfigurationError
+        raise ConfigurationError(
+            f"balance stats shape {st.shape} does not match weight rows {w64.shape}")
+    wa = np.abs(w64).max(axis=1)
+    ok = (st > 0) & (wa > 0)
+    c = np.ones_like(st)
+    c[ok] = np.clip(np.sqrt(st[ok] / wa[ok]), 1e-3, 1e3)
+    return c
+
+
+class SlotPool:
+    """Refcounted residual-stream slots of one video."""
+
+    def __init__(self, first: int, count: int):
+        self.free = list(range(first + count - 1, first - 1, -1))
+        self.ref: Dict[int, int] = {}
+
+    def alloc(self) -> int:
+        if not self.free:
+            raise RuntimeError("residual-stream arena exhausted")
+        s = self.free.pop()
+        self.ref[s] = 1
+        return s
+
+    def inc(self, s: int) -> int:
+        self.ref[s] += 1
+        return s
+
+    def dec(self, s: Optional[int]):
+        if s is None:
+            return
+        self.ref[s] -= 1
+        if self.ref[s] == 0:
+            del self.ref[s]
+            self.free.append(s)
+
+
+@dataclass
+class VideoState:
+    pool: SlotPool
+    rng: np.random.Generator
+    x: int = -1                         # slot of the current latent x_t
+    cache: List[Optional[int]] = field(default_factory=list)
+    prev: List[Optional[int]] = field(default_factory=list)
+    hist: List[int] = field(default_factory=list)
+    seen: int = 0
+    trace: List[TraceRecord] = field(default_factory=list)
+
+
+@dataclass
+class EngineOptions:
+    attention: str = "precise"     # "precise" (f64 softmax kernel) | "fast" (bf16 SDPA)
+    noise: str = "numpy"           # "numpy" (reference RNG stream) | "device" (Philox)
+    record_features: bool = False
+
+
+class QuantCacheEngine:
+    """Batched, per-video-decision QuantCache sampler on one GPU."""
+
+    def __init__(self, model: DiTModel, alpha_bar: np.ndarray, toggles: Toggles,
+                 thresholds: ThresholdConfig, weight_bits: Optional[Dict[int, int]] = None,
+                 act_absmax: Optional[Dict[int, Dict[str, np.ndarray]]] = None,
+                 sign_seed: int = 0, prune_seed: int = 0, max_videos: int = 1,
+                 options: Optional[EngineOptions] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("QuantCacheEngine needs a CUDA device (no CPU fallback)")
+        N.lib()
+        thresholds.validate()
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.current_stream()
+        self.model, self.cfg = model, model.cfg
+        self.opts = options or EngineOptions()
+        self.tog, self.th = toggles, thresholds
+        self.thc = Dv.thresholds_struct(thresholds, toggles)
+        self.ab = np.asarray(alpha_bar, np.float64)
+        self.T = len(self.ab)
+        self.L = self.cfg.num_blocks
+        if self.L > N.MAX_LAYERS:
+            raise ValueError(f"at most {N.MAX_LAYERS} blocks")
+        self.S = self.cfg.seq_len
+        self.Sp = (self.S + 127) // 128 * 128
+        self.d = self.cfg.model_dim
+        self.H = self.cfg.num_heads
+        self.c = self.cfg.cond_dim
+        self.nv = max_videos
+        self.weight_bits = dict(weight_bits or {})
+        self.sign_seed, self.prune_seed = sign_seed, prune_seed
+        self.block_cost = block_mac_cost(self.cfg)
+        self.head_macs = head_mac_cost(self.cfg)
+        self._upload_weights(act_absmax or {})
+        self._alloc()
+
+    # ------------------------------------------------------------------ setup
+    def _t(self, a, dt=torch.float32):
+        return torch.as_tensor(np.ascontiguousarray(a)).to(self.dev, dt)
+
+    def _upload_weights(self, act_absmax):
+        m, tog = self.model, self.tog
+        self.fpw = []          # per layer: dict site -> f32 [K][N] (FP / act-only modes)
+        self.packed = []       # per layer: dict site -> PackedWeight
+        self.ln = []
+        signs_by_b = {}
+        need_fp = not tog.aigq_weights
+        for l, blk in enumerate(m.blocks):
+            self.ln.append(tuple(self._t(getattr(blk, n)) for n in
+                                 ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "ln3_g", "ln3_b")))
+            fp, pk = {}, {}
+            for site in QUANT_SITES:
+                w = getattr(blk, site)
+                if need_fp:
+                    fp[site] = self._t(w)
+                if tog.aigq_weights:
+                    stats = act_absmax.get(l, {}).get(site)
+                    K = w.shape[0]
+                    if stats is not None:
+                        b = Dv.pow2_floor(K)
+                        if b not in signs_by_b:
+                            signs_by_b[b] = self._t(Dv.sign_vector(self.sign_seed, b))
+                        tr = (self._t(balance_scales(w, stats), torch.float64), signs_by_b[b])
+                    else:
+                        tr = (None, None)
+                    pk[site] = Dv.weight_prep(self._t(w), self.weight_bits[l], tr[0], tr[1],
+                                              keep_deq=not tog.aigq_acts)
+            self.fpw.append(fp)
+            self.packed.append(pk)
+        self.head_w = self._t(m.head_w)
+        self.head_b = self._t(m.head_b)
+        # modulation scalars for every (t, layer): t_emb @ mod on device (f64 acc)
+        temb = self._t(np.stack([timestep_embedding(t, self.d) for t in range(self.T)]))
+        mods = []
+        for blk in m.blocks:
+            mods.append(Dv.gemm_f64(temb, self._t(blk.mod)).cpu().numpy())
+        self.mod = np.stack(mods)            # [L][T][6] f32
+        self.draws = self._t(prune_draw_table(self.prune_seed, self.T, self.L), torch.float64)
+
+    def _alloc(self):
+        nv, Sp, d, L = self.nv, self.Sp, self.d, self.L
+        self.P = 2 * L + self.th.history_k + 6
+        dev = self.dev
+        self.arena = torch.zeros((nv * self.P * Sp, d), dtype=torch.float32, device=dev)
+        rows = nv * Sp
+        K4 = 4 * d
+        self.codes = [torch.zeros((rows, Dv.round16(K4)), dtype=torch.uint8, device=dev)
+                      for _ in range(3)]
+        self.q = torch.zeros((rows, d), dtype=torch.float32, device=dev)
+        self.k = torch.zeros_like(self.q)
+        self.v = torch.zeros_like(self.q)
+        self.att = torch.zeros_like(self.q)
+        self.xe = torch.zeros((rows, K4), dtype=torch.float32, device=dev)
+        self.hid = torch.zeros((rows, K4), dtype=torch.float32, device=dev)
+        self.eps = torch.zeros((rows, d), dtype=torch.float32, device=dev)
+        self.q2 = torch.zeros_like(self.q)
+        self.k2 = torch.zeros((nv, d), dtype=torch.float32, device=dev)
+        self.v2 = torch.zeros_like(self.k2)
+        self.cond = torch.zeros((nv, self.c), dtype=torch.float32, device=dev)
+        self.ac = [Dv.ActCodes(self.codes[o][:, :Dv.round16(d)],
+                               torch.zeros(rows, dtype=torch.int32, device=dev),
+                               torch.zeros(nv, dtype=torch.float64, device=dev),
+                               torch.zeros(nv, dtype=torch.int32, device=dev), d)
+                   for o in range(3)]
+        self.noise_dev = torch.zeros((nv, self.S, d), dtype=torch.float32, device=dev)
+        self.noise_host = torch.zeros((nv, self.S, d), dtype=torch.float32).pin_memory()
+        self.pol_size = C.sizeof(N.QcbPolicyVideo)
+        self.pol = torch.zeros(nv * self.pol_size, dtype=torch.uint8, device=dev)
+        self.pol_host = torch.zeros(nv * self.pol_size, dtype=torch.uint8).pin_memory()
+        self.pol_trace = torch.zeros((self.T, nv * self.pol_size), dtype=torch.uint8, device=dev)
+        self.srap = torch.zeros((L, nv, 3), dtype=torch.float64, device=dev)
+        self.mask = torch.zeros((L, nv), dtype=torch.int32, device=dev)
+        self.hist_l1 = torch.zeros((self.th.history_k + 1, nv), dtype=torch.float64, device=dev)
+        self.hlc = torch.zeros((nv, 2), dtype=torch.float64, device=dev)
+        self.idx_host = torch.zeros(1 << 16, dtype=torch.int64).pin_memory()
+        self.idx_dev = torch.zeros(1 << 16, dtype=torch.int64, device=dev)
+
+    # ------------------------------------------------------------------ index tables
+    def _upload_idx(self, arrays: Sequence[Sequence[int]]) -> List[torch.Tensor]:
+        """Pack small int64 row tables into one pinned buffer, one H2D copy."""
+        sizes = [len(a) for a in arrays]
+        total = sum(sizes)
+        if total > self.idx_host.numel():
+            raise RuntimeError("index table overflow")
+        flat = np.concatenate([np.asarray(a, np.int64) for a in arrays]) if total else \
+            np.zeros(0, np.int64)
+        self.idx_host[:total].numpy()[:] = flat
+        self.idx_dev[:total].copy_(self.idx_host[:total], non_blocking=True)
+        out, off = [], 0
+        for n in sizes:
+            out.append(self.idx_dev[off:off + n])
+            off += n
+        return out
+
+    def rows(self, slot: int) -> int:
+        return slot * self.Sp
+
+    def slot_view(self, slot: int) -> torch.Tensor:
+        return self.arena[slot * self.Sp: slot * self.Sp + self.S]
+
+    # ------------------------------------------------------------------ sites
+    def _site(self, l, site, bits, x, nseg, *, x_row0=None, seg_rows=None, seg_valid=None,
+              ln=None, mod=(1.0, 0.0), epi=N.EPI_STORE, out=None, out_row0=None,
+              resid=None, resid_row0=None, gate=1.0, outs=None, sites=None):
+        """One GEMM site (or a fused group sharing the same input) through the
+        mode the reference's QuantRuntime.gemm_fn would pick (runtime.py:69-79)."""
+        tog = self.tog
+        sites = sites or (site,)
+        seg_rows = seg_rows or self.Sp
+        seg_valid = seg_valid or self.S
+        M = nseg * seg_rows
+        quant_acts = tog.aigq_acts and bits < FP_BITS
+        if tog.aigq_weights and quant_acts:
+            pws = [self.packed[l][s] for s in sites]
+            trs = [(p.chan_scale, p.signs) if p.chan_scale is not None else None for p in pws]
+            acs = []
+            for o, p in enumerate(pws):
+                a = self.ac[o]
+                acs.append(Dv.ActCodes(self.codes[o][:M, :Dv.round16(p.K)],
+                                       a.rowsum[:M], a.scale[:nseg], a.zero[:nseg], p.K))
+            Dv.act_quant(x, bits, trs, seg_rows=seg_rows, seg_valid=seg_valid, nseg=nseg,
+                         x_row0=x_row0, ln=ln, mod=mod, out=acs)
+            targets = outs or [out]
+            for o, p in enumerate(pws):
+                Dv.gemm_u8(acs[o], p, M=M, out=targets[o], epilogue=epi, resid=resid,
+                           gate=gate, seg_rows=seg_rows, seg_valid=seg_valid,
+                           out_row0=out_row0, resid_row0=resid_row0)
+            return
+        # full-precision GEMMs (weight-only, act-only or plain)
+        for o, s in enumerate(sites):
+            target = (outs or [out])[o]
+            if tog.aigq_weights:
+                p = self.packed[l][s]
+                w = p.w_deq
+                if p.chan_scale is not None:
+                    (r,) = Dv.act_quant(x, 8, [(p.chan_scale, p.signs)], seg_rows=seg_rows,
+                                        seg_valid=seg_valid, nseg=nseg, x_row0=x_row0, ln=ln,
+                                        mod=mod, want_codes=False, want_xe=True)
+                    a, a_row0 = r.xe, None
+                else:
+                    a, a_row0 = self._prologue(x, ln, mod, nseg, seg_rows, seg_valid, x_row0,
+                                               p.K)
+            elif quant_acts:   # activation-only fake quantization (runtime.py:78-79)
+                w = self.fpw[l][s]
+                (r,) = Dv.act_quant(x, bits, [None], seg_rows=seg_rows, seg_valid=seg_valid,
+                                    nseg=nseg, x_row0=x_row0, ln=ln, mod=mod,
+                                    want_codes=False, want_deq=True)
+                a, a_row0 = r.deq, None
+            else:
+                w = self.fpw[l][s]
+                a, a_row0 = self._prologue(x, ln, mod, nseg, seg_rows, seg_valid, x_row0,
+                                           w.shape[0])
+            Dv.gemm_f64(a, w, out=target, epilogue=epi, resid=resid, gate=gate,
+                        seg_rows=seg_rows, seg_valid=seg_valid, a_row0=a_row0,
+                        out_row0=out_row0, resid_row0=resid_row0, M=M)
+
+    def _prologue(self, x, ln, mod, nseg, seg_rows, seg_valid, x_row0, K):
+        if ln is None:
+            return x, x_row0
+        h = self.xe[:nseg * seg_rows, :K]
+        Dv.ln_mod(x, ln[0], ln[1], mod[0], mod[1], out=h, seg_rows=seg_rows,
+                  seg_valid=seg_valid, nseg=nseg, x_row0=x_row0)
+        return h, None
+
+    def _attention(self, q, k, v, out, nseg, Skv, kv_stride):
+        S, Sp, d, H = self.S, self.Sp, self.d, self.H
+        if self.opts.attention == "fast" and Skv > 1:
+            dh = d // H
+            qq = q[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].permute(0, 2, 1, 3)
+            kk = k[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].permute(0, 2, 1, 3)
+            vv = v[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].permute(0, 2, 1, 3)
+            o = torch.nn.functional.scaled_dot_product_attention(
+                qq.to(torch.bfloat16), kk.to(torch.bfloat16), vv.to(torch.bfloat16))
+            out[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].copy_(o.permute(0, 2, 1, 3))
+            return
+        a = N.QcbAttention(N.ptr(q), q.stride(0), N.ptr(k), k.stride(0), N.ptr(v), v.stride(0),
+                           N.ptr(out), out.stride(0), S, Skv, H, d // H, nseg, Sp, kv_stride,
+                           Sp, S)
+        N.check(N.lib().qcb_attention_f64(C.byref(a), N.stream_ptr()), "attention")
+
+    def _block(self, l, t, vids, bits, xin_row0, out_row0, cond_row0):
+        """block_forward (model.py:159-199) for the videos `vids` at one bits."""
+        n = len(vids)
+        m = self.mod[l, t]
+        one = np.float32(1.0)
+        sh1, sc1, g1 = m[0], one + m[1], m[2]
+        sh3, sc3, g3 = m[3], one + m[4], m[5]
+        ln1g, ln1b, ln2g, ln2b, ln3g, ln3b = self.ln[l]
+        A = self.arena
+        # spatial-temporal self-attention
+        self._site(l, None, bits, A, n, x_row0=xin_row0, ln=(ln1g, ln1b), mod=(sc1, sh1),
+                   outs=[self.q, self.k, self.v], sites=("sta_q", "sta_k", "sta_v"))
+        self._attention(self.q, self.k, self.v, self.att, n, self.S, self.Sp)
+        self._site(l, "sta_o", bits, self.att, n, epi=N.EPI_GATE_RESID, out=A,
+                   out_row0=out_row0, resid=A, resid_row0=xin_row0, gate=g1)
+        # cross-attention on the single cond token
+        self._site(l, "ca_q", bits, A, n, x_row0=out_row0, ln=(ln2g, ln2b), out=self.q2)
+        self._site(l, None, bits, self.cond, n, x_row0=cond_row0, seg_rows=1, seg_valid=1,
+                   outs=[self.k2, self.v2], sites=("ca_k", "ca_v"))
+        self._attention(self.q2, self.k2, self.v2, self.att, n, 1, 1)
+        self._site(l, "ca_o", bits, self.att, n, epi=N.EPI_RESID, out=A, out_row0=out_row0,
+                   resid=A, resid_row0=out_row0)
+        # FFN
+        self._site(l, "ffn1", bits, A, n, x_row0=out_row0, ln=(ln3g, ln3b), mod=(sc3, sh3),
+                   epi=N.EPI_GELU, out=self.hid)
+        self._site(l, "ffn2", bits, self.hid, n, epi=N.EPI_GATE_RESID, out=A,
+                   out_row0=out_row0, resid=A, resid_row0=out_row0, gate=g3)
+
+    # ------------------------------------------------------------------ run
+    def generate(self, seeds: Sequence[int], device_noise_seed: Optional[int] = None):
+        """Run the full reverse trajectory for len(seeds) videos (one per seed).
+
+        Returns (latents f32 [nv][F][T][d] on host, traces per video)."""
+        nv = len(seeds)
+        if nv > self.nv:
+            raise ValueError(f"engine sized for {self.nv} videos")
+        L, S, d, T = self.L, self.S, self.d, self.T
+        F, Tk = self.cfg.frames, self.cfg.tokens_per_frame
+        st = self.stream
+        self.pol.zero_()
+        vids = []
+        for v, seed in enumerate(seeds):
+            vs = VideoState(SlotPool(v * self.P, self.P), np.random.default_rng(seed),
+                            cache=[None] * L, prev=[None] * L)
+            x0 = vs.rng.standard_normal((F, Tk, d)).astype(np.float32)
+            cond = vs.rng.standard_normal(self.c).astype(np.float32)
+            vs.x = vs.pool.alloc()
+            self.slot_view(vs.x).copy_(torch.from_numpy(x0.reshape(S, d)))
+            self.cond[v].copy_(torch.from_numpy(cond))
+            vids.append(vs)
+        gen = None
+        if self.opts.noise == "device":
+            gen = torch.Generator(device=self.dev)
+            gen.manual_seed(int(device_noise_seed if device_noise_seed is not None else seeds[0]))
+        pol = self.pol.data_ptr()
+        lib = N.lib()
+        sp = N.stream_ptr()
+        for t in range(T - 1, -1, -1):
+            # ---------------- plan (device) ----------------
+            nh = len(vids[0].hist)
+            srap_layers = []
+            pre = []
+            for j in range(nh):
+                pre.append([self.rows(vs.x) for vs in vids])
+                pre.append([self.rows(vs.hist[j]) for vs in vids])
+            boundary = vids[0].seen == 0 or t == 0
+            if self.tog.srap and not boundary:
+                for l in range(1, L):
+                    if any(vs.prev[l - 1] is not None and vs.prev[l] is not None for vs in vids):
+                        srap_layers.append(l)
+                        pre.append([self.rows(vs.prev[l - 1]) if vs.prev[l - 1] is not None
+                                    else 0 for vs in vids])
+                        pre.append([self.rows(vs.prev[l]) if vs.prev[l] is not None else 0
+                                    for vs in vids])
+            tabs = self._upload_idx(pre)
+            for j in range(nh):
+                Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]), Dv.feat(self.arena, tabs[2 * j + 1]),
+                             S, d, nv, self.hist_l1[j])
+            N.check(lib.qcb_policy_plan_reuse(pol, nv, L, t, self.thc, sp), "plan_reuse")
+            if srap_layers:
+                N.check(lib.qcb_policy_sim_mask(pol, nv, L, self.thc, N.ptr(self.mask), sp),
+                        "sim_mask")
+                for i, l in enumerate(srap_layers):
+                    a, b = tabs[2 * nh + 2 * i], tabs[2 * nh + 2 * i + 1]
+                    Dv.reduce_srap(Dv.feat(self.arena, a), Dv.feat(self.arena, b), S, d, nv,
+                                   self.srap[l], seg_active=self.mask[l])
+            N.check(lib.qcb_policy_plan_finish(pol, nv, L, t, self.thc, N.ptr(self.srap),
+                                               N.ptr(self.hist_l1), nh,
+                                               N.ptr(self.draws[t]), 0, sp), "plan_finish")
+            self.pol_host.copy_(self.pol, non_blocking=True)
+            st.synchronize()
+            plans = [N.QcbPolicyVideo.from_buffer_copy(
+                self.pol_host.numpy()[v * self.pol_size:(v + 1) * self.pol_size].tobytes())
+                for v in range(nv)]
+            for vs in vids:
+                vs.seen += 1
+            # ---------------- execute blocks ----------------
+            cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
+            for l in range(L):
+                outs = list(cur)
+                rec = [v for v in range(nv) if plans[v].action[l] == N.ACT_RECOMPUTE]
+                for v in range(nv):
+                    a = plans[v].action[l]
+                    if a == N.ACT_REUSE:
+                        outs[v] = vids[v].pool.inc(vids[v].cache[l])
+                    elif a == N.ACT_PRUNE:
+                        outs[v] = vids[v].pool.inc(cur[v])
+                    else:
+                        outs[v] = vids[v].pool.alloc()
+                # group recomputing videos by activation bits
+                groups: Dict[int, List[int]] = {}
+                for v in rec:
+                    groups.setdefault(plans[v].abits, []).append(v)
+                need_d = [v in rec and (vids[v].cache[l] is not None or vids[v].prev[l] is not None)
+                          and vids[v].prev[l] is not None for v in range(nv)]
+                tabl = []
+                for bits, g in groups.items():
+                    tabl += [[self.rows(cur[v]) for v in g], [self.rows(outs[v]) for v in g],
+                             g]
+                if any(need_d):
+                    tabl += [[self.rows(outs[v]) for v in range(nv)],
+                             [self.rows(vids[v].cache[l] if vids[v].cache[l] is not None
+                                        else (vids[v].prev[l] or 0)) for v in range(nv)],
+                             [self.rows(vids[v].prev[l] or 0) for v in range(nv)],
+                             [int(x) for x in need_d]]
+                tl = self._upload_idx(tabl)
+                for gi, (bits, g) in enumerate(groups.items()):
+                    self._block(l, t, g, bits, tl[3 * gi], tl[3 * gi + 1], tl[3 * gi + 2])
+                if any(need_d):
+                    base = 3 * len(groups)
+                    act = tl[base + 3].to(torch.int32)
+                    Dv.reduce_hlc(Dv.feat(self.arena, tl[base]), Dv.feat(self.arena, tl[base + 1]),
+                                  Dv.feat(self.arena, tl[base + 2]), S, d, nv, self.hlc,
+                                  seg_active=act)
+                N.check(lib.qcb_policy_observe(pol, nv, l, t, self.thc, N.ptr(self.hlc), sp),
+                        "observe")
+                # host mirror of the cache / prev references (schedule.py:349-351)
+                for v, vs in enumerate(vids):
+                    if plans[v].action[l] == N.ACT_RECOMPUTE and t > 0:
+                        vs.pool.dec(vs.cache[l])
+                        vs.cache[l] = vs.pool.inc(outs[v])
+                    vs.pool.dec(vs.prev[l])
+                    vs.prev[l] = vs.pool.inc(outs[v])
+                    vs.pool.dec(cur[v])
+                cur = outs
+            # ---------------- head + sampler update ----------------
+            tabh = self._upload_idx([[self.rows(c) for c in cur]])
+            Dv.gemm_f64(self.arena, self.head_w, out=self.eps, epilogue=N.EPI_BIAS,
+                        bias=self.head_b, seg_rows=self.Sp, seg_valid=S, a_row0=tabh[0],
+                        M=nv * self.Sp)
+            self.pol_trace[t].copy_(self.pol, non_blocking=True)
+            if t > 0:
+                if self.opts.noise == "numpy":
+                    for v, vs in enumerate(vids):
+                        self.noise_host[v].numpy()[:] = vs.rng.standard_normal(
+                            (F, Tk, d)).astype(np.float32).reshape(S, d)
+                    self.noise_dev[:nv].copy_(self.noise_host[:nv], non_blocking=True)
+                else:
+                    self.noise_dev[:nv].normal_(generator=gen)
+            a_t = self.ab[t]
+            for v, vs in enumerate(vids):
+                new = vs.pool.alloc()
+                eps_v = self.eps[v * self.Sp: v * self.Sp + S]
+                if t > 0:
+                    a_p = self.ab[t - 1]
+                    alpha = a_t / a_p
+                    beta = 1.0 - alpha
+                    c3 = float(np.sqrt((1.0 - a_p) / (1.0 - a_t) * beta)) if t > 1 else 0.0
+                    Dv.ddpm(self.slot_view(vs.x), eps_v, float(beta / np.sqrt(1.0 - a_t)),
+                            float(np.sqrt(alpha)), self.noise_dev[v] if t > 1 else None, c3,
+                            out=self.slot_view(new))
+                else:
+                    Dv.ddpm(self.slot_view(vs.x), eps_v, float(np.sqrt(1.0 - self.ab[0])),
+                            float(np.sqrt(self.ab[0])), out=self.slot_view(new))
+                vs.pool.dec(cur[v])
+                # finalize_step: latent history window (schedule.py:353-357)
+                vs.hist.append(vs.x)
+                if len(vs.hist) > self.th.history_k:
+                    vs.pool.dec(vs.hist.pop(0))
+                vs.x = new
+        out = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
+        traces = self._collect_traces(vids)
+        # release everything for the next call
+        return out.reshape(nv, F, Tk, d), traces
+
+    def _collect_traces(self, vids) -> List[List[TraceRecord]]:
+        raw = self.pol_trace.cpu().numpy()
+        nv = len(vids)
+        traces = [[] for _ in range(nv)]
+        wb_of = lambda l: self.weight_bits.get(l, FP_BITS) if self.tog.aigq_weights else FP_BITS
+        for t in range(self.T - 1, -1, -1):
+            for v in range(nv):
+                p = N.QcbPolicyVideo.from_buffer_copy(
+                    raw[t, v * self.pol_size:(v + 1) * self.pol_size].tobytes())
+                for l in range(self.L):
+                    a = p.action[l]
+                    wb = wb_of(l)
+                    macs = billed_macs(self.block_cost, wb, p.abits) if a == N.ACT_RECOMPUTE else 0
+                    traces[v].append(TraceRecord(
+                        t, l, ACTION_NAMES[a], float(p.d_now[l]) if p.d_valid[l] else None,
+                        float(p.sim[l]) if p.sim_valid[l] else None, int(p.abits), wb, macs,
+                        float(p.v)))
+                traces[v].append(TraceRecord(t, "head", "recompute", None, None, FP_BITS,
+                                             FP_BITS, self.head_macs * FP_BITS * FP_BITS))
+        return traces

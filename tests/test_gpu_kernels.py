@@ -293,20 +293,21 @@ class TestReductions:
         rng = np.random.default_rng(9)
         S, d, nseg = 4096, 1152, 2
         a, b, c = (rng.standard_normal((nseg * S, d)).astype(np.float32) for _ in range(3))
+        ta, tb, tc = t(a), t(b), t(c)   # keep the device copies alive across the calls
         res = torch.zeros(nseg * 3, dtype=torch.float64, device="cuda")
-        D.reduce_hlc(D.feat(t(a)), D.feat(t(b)), D.feat(t(c)), S, d, nseg, res)
+        D.reduce_hlc(D.feat(ta), D.feat(tb), D.feat(tc), S, d, nseg, res)
         r = res.cpu().numpy()
         for v in range(nseg):
             sl = slice(v * S, (v + 1) * S)
             dd = O.divergence(a[sl], b[sl], 3, c[sl])
             assert (r[2 * v] / 3) * np.sqrt(r[2 * v + 1]) == pytest.approx(dd, rel=1e-12)
-        D.reduce_srap(D.feat(t(a)), D.feat(t(b)), S, d, nseg, res)
+        D.reduce_srap(D.feat(ta), D.feat(tb), S, d, nseg, res)
         r = res.cpu().numpy()
         for v in range(nseg):
             sl = slice(v * S, (v + 1) * S)
             s = r[3 * v] / (np.sqrt(r[3 * v + 1]) * np.sqrt(r[3 * v + 2]))
             assert s == pytest.approx(O.similarity(a[sl], b[sl]), rel=1e-12, abs=1e-15)
-        D.reduce_l1(D.feat(t(a)), D.feat(t(b)), S, d, nseg, res)
+        D.reduce_l1(D.feat(ta), D.feat(tb), S, d, nseg, res)
         r = res.cpu().numpy()
         for v in range(nseg):
             sl = slice(v * S, (v + 1) * S)
