@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""QuantCache B200 benchmark -- prints ONE JSON line (driver contract).
+
+Headline workload (BASELINE.json configs[2], "C3"): STDiT-XL/2 dimensions in the
+reference block (28 blocks, hidden 1152, 16 heads, FFN 4608, cond width 4096),
+16 frames of 256x256 (S = 16 x 16 x 16 = 4096 tokens), 100 DDPM steps with full
+QuantCache (HLC + AIGQ W6 / mixed-bit activations + SRAP), random-init weights,
+synthetic latents.  A bench "step" = one batch of videos sampled end to end.
+
+  metric  videos/s (higher is better); s/video is reported alongside
+  roofline  the dominant kernel (tcgen05 u8 GEMM) in TOP/s vs the int8 peak
+  e2e     the same runs through the engine's public generate() with host
+          latents in and out (H2D/D2H inside the timed region)
+
+Multi-GPU: one process per GPU (torchrun); videos are sharded across ranks
+with no collective in the sampling loop (per-video decisions, reference
+semantics) -> "scaling": "weak"; the timed region is bracketed by barriers and
+the max elapsed over ranks is reported.
+
+`--impl reference` times the CPU oracle restatement of the reference's hot path
+(oracle/qc_oracle.py: quantizer + integer GEMMs of a recomputed block) on a
+bounded row slice, on all host cores, extrapolated to the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C3 = dict(num_blocks=28, model_dim=1152, num_heads=16, tokens_per_frame=256, frames=16,
+          cond_dim=4096)
+SITES_KN = {"sta_q": (1152, 1152), "sta_k": (1152, 1152), "sta_v": (1152, 1152),
+            "sta_o": (1152, 1152), "ca_q": (1152, 1152), "ca_o": (1152, 1152),
+            "ffn1": (1152, 4608), "ffn2": (4608, 1152)}
+NOMINAL_INT8_TOPS = 4500.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--videos", type=int, default=2, help="videos per GPU per step")
+    ap.add_argument("--timesteps", type=int, default=100)
+    ap.add_argument("--wbits", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the oracle restatement of the reference's quantized block, on rows
+
+
+def _cpu_block_sample(rows: int, seed: int = 0) -> float:
+    """Seconds for the reference algorithm's hot path of ONE recomputed C3 block
+    (per-tensor AIGQ quantizer with the sequential f64 rotation + the 8 large
+    integer-GEMM sites, tensor.py:68-112 / quant.py:83-165) on `rows` rows."""
+    from oracle import qc_oracle as O
+    rng = np.random.default_rng(seed)
+    rot = {}
+    t0 = time.perf_counter()
+    for site, (K, N) in SITES_KN.items():
+        x = rng.standard_normal((rows, K)).astype(np.float32)
+        w = (rng.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32)
+        c = np.ones(K)
+        if K not in rot:
+            rot[K] = O.rotation_dense(K, 0).astype(np.float32)
+        y = (x.astype(np.float64) / c[None, :]).astype(np.float32)
+        xe = O.seq_mm(y, rot[K])
+        sa, za = O.act_params(xe, 8)
+        ca = O.codes_of(xe, sa, za, 8)
+        sw, zw = O.chan_params(w, 6)
+        cw = O.codes_of(w, sw[None], zw[None], 6)
+        O.matmul_int_seq(ca, sa, za, cw, sw, zw)
+    return time.perf_counter() - t0
+
+
+def _videos_per_s_from_sample(t_sample: float, rows: int, S: int, L: int, T: int,
+                              frac: float) -> float:
+    sec_per_video = t_sample * (S / rows) * L * T * frac
+    return 1.0 / sec_per_video
+
+
+def _pool_worker(args):
+    rows, seed = args
+    return _cpu_block_sample(rows, seed)
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on all host threads (one process per core,
+    each on its own row slice), extrapolated to videos/s of the C3 workload."""
+    import multiprocessing as mp
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    rows = 8
+    S = C3["tokens_per_frame"] * C3["frames"]
+    frac = 1.0   # every block recomputed (the CPU path has no cache hits to exploit here)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_pool_worker, [(rows, i) for i in range(cores)])
+        times = []
+        for k in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_pool_worker, [(rows, 100 + k * cores + i) for i in range(cores)])
+            times.append(time.perf_counter() - t0)
+    step = statistics.median(times)
+    # cores row-slices of `rows` rows each finished in `step` seconds
+    vps = _videos_per_s_from_sample(step, rows * cores, S, C3["num_blocks"], args.timesteps,
+                                    frac)
+    line = {
+        "impl": "reference", "metric": "videos_per_s", "value": vps, "unit": "videos/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "C3 STDiT-XL/2 16x256^2 T=100 (CPU oracle sample)",
+                   "timesteps": args.timesteps},
+        "cpu_baseline": {"value": vps, "unit": "videos/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle quantizer+8 int GEMM sites of one C3 block on "
+                                   f"{rows} rows per core x {cores} cores, extrapolated x"
+                                   f"{S}/rows x 28 blocks x {args.timesteps} steps, all blocks "
+                                   f"recomputed, attention excluded"},
+        "e2e": {"value": vps, "unit": "videos/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_int8_peak(torch) -> dict:
+    """Library int8 GEMM (cuBLASLt via torch._int_mm, s8 x s8 -> s32, 8192^3) as the
+    measured tensor-pipe reference; MEASURED_PEAKS.json carries bf16 only."""
+    try:
+        n = 8192
+        a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        return {"tops": 2.0 * n ** 3 / best / 1e12, "source": "measured torch._int_mm "
+                "(cuBLASLt) s8 8192^3 burst, best of 10"}
+    except Exception as exc:  # pragma: no cover - library path absent
+        return {"tops": None, "source": f"unavailable: {type(exc).__name__}"}
+
+
+def fast_model(torch, cfg):
+    """Random-init weights of the C3 architecture (N(0, fan_in^-1/2), like
+    init_model) drawn with NumPy's float32 normal generator for speed; C3 has no
+    CPU oracle so the reference draw order is not needed here."""
+    from paper_2503_06545_b200.model import BlockWeights, DiTModel, _shapes
+    rng = np.random.default_rng(cfg.seed)
+    blocks = []
+    for _ in range(cfg.num_blocks):
+        vals = {}
+        for name, shape, fan in _shapes(cfg):
+            if fan == "one":
+                vals[name] = np.ones(shape, np.float32)
+            elif fan == "zero":
+                vals[name] = np.zeros(shape, np.float32)
+            else:
+                vals[name] = rng.standard_normal(shape, dtype=np.float32) * np.float32(fan ** -0.5)
+        blocks.append(BlockWeights(**vals))
+    d = cfg.model_dim
+    return DiTModel(cfg, blocks,
+                    rng.standard_normal((d, d), dtype=np.float32) * np.float32(d ** -0.5),
+                    rng.standard_normal(d, dtype=np.float32) * np.float32(d ** -0.5))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_06545_b200 import device as Dv
+    from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
+    from paper_2503_06545_b200.model import DiTConfig
+    from paper_2503_06545_b200.sampler import linear_beta_schedule
+    from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B, T = args.videos, args.timesteps
+    cfg = DiTConfig(seed=0, **C3)
+    S, d = cfg.seq_len, cfg.model_dim
+    model = fast_model(torch, cfg)
+    # Synthetic calibration (no reference calibration exists at this size):
+    # activation absmax := weight row absmax gives balance scales c == 1 while the
+    # randomized Hadamard rotation stays on (quant.py:179-200).
+    absmax = {l: {s: np.abs(getattr(b, s)).max(axis=1).astype(np.float64)
+                  for s in ("sta_q", "sta_k", "sta_v", "sta_o", "ca_q", "ca_k", "ca_v",
+                            "ca_o", "ffn1", "ffn2")}
+              for l, b in enumerate(model.blocks)}
+    wbits = {l: args.wbits for l in range(cfg.num_blocks)}
+    sched = linear_beta_schedule(T)
+    opts = EngineOptions(attention="fast", noise="device")
+    # Threshold calibration pass (harness.py:319-345 procedure on the quantized
+    # path): every block recomputed, D/V recorded, delta = p33/p66, v = p25/p75.
+    tog_cal = Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=False)
+    th0 = ThresholdConfig(delta1=0.0, delta2=0.0)
+    eng = QuantCacheEngine(model, sched.alpha_bar, tog_cal, th0, wbits, absmax, sign_seed=0,
+                           prune_seed=0, max_videos=B, options=opts)
+    _, tr = eng.generate([1000 + rank], device_noise_seed=1000 + rank)
+    ds = [r.d for r in tr[0] if r.d is not None]
+    vs = [r.v for r in tr[0] if r.layer == 0 and r.v is not None and r.v > 0]
+    th = ThresholdConfig(delta1=float(np.percentile(ds, 33)), delta2=float(np.percentile(ds, 66)),
+                         v_low=float(np.percentile(vs, 25)), v_high=float(np.percentile(vs, 75)))
+    del eng
+    torch.cuda.empty_cache()
+    tog = Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=True)
+    eng = QuantCacheEngine(model, sched.alpha_bar, tog, th, wbits, absmax, sign_seed=0,
+                           prune_seed=0, max_videos=B, options=opts)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7 + rank)
+    x0 = torch.randn((B, S, d), device="cuda", generator=gen)
+    cond = torch.randn((B, cfg.cond_dim), device="cuda", generator=gen)
+    seeds = lambda k: [10_000 * rank + 100 * k + v for v in range(B)]
+    for k in range(args.warmup):
+        eng.generate(seeds(k), device_noise_seed=k, x0_dev=x0, cond_dev=cond,
+                     return_device=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    eng.gemm_profile = []
+    launches0 = Dv.LAUNCHES[0]
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    vids_all = []
+    for k in range(args.steps):
+        _, vids = eng.generate(seeds(args.warmup + k), device_noise_seed=args.warmup + k,
+                               x0_dev=x0, cond_dev=cond, return_device=True)
+        vids_all.append(vids)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    launches = Dv.LAUNCHES[0] - launches0
+    clk = clocks.stop()
+    prof = eng.gemm_profile
+    eng.gemm_profile = None
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    # recompute fraction / decisions of the timed runs
+    traces = [eng.traces_of(v) for v in vids_all]
+    recs = [r for trs in traces for tv in trs for r in tv if r.layer != "head"]
+    frac = sum(r.action == "recompute" for r in recs) / max(1, len(recs))
+    executed = sum(r.macs for trs in traces for tv in trs for r in tv)
+    # GEMM roofline (CUDA events around every u8 GEMM launch, same stream)
+    g_ops = sum(p[2] for p in prof)
+    g_time = sum(p[0].elapsed_time(p[1]) for p in prof) / 1e3
+    per_site = {}
+    for e_s, e_e, ops, site in prof:
+        a = per_site.setdefault(site, [0, 0.0, 0])
+        a[0] += ops
+        a[1] += e_s.elapsed_time(e_e) / 1e3
+        a[2] += 1
+    peak = measured_int8_peak(torch) if rank == 0 else {"tops": None}
+    # e2e through the public API (host latents in, host latents out)
+    e2e_vps = None
+    h2d = B * (S * d + cfg.cond_dim) * 4
+    d2h = B * S * d * 4
+    if rank == 0:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            eng.generate(seeds(500 + k), device_noise_seed=500 + k)
+        torch.cuda.synchronize()
+        e2e_vps = args.steps * B * world / (time.perf_counter() - t0)
+    value = args.steps * B * world / elapsed
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rows = 4
+        ts = _cpu_block_sample(rows, 0)
+        cpu = {"value": _videos_per_s_from_sample(ts, rows, S, cfg.num_blocks, T, frac),
+               "unit": "videos/s", "cores": 1, "kind": "port",
+               "sample": f"oracle quantizer + 8 int GEMM sites of one C3 block on {rows} rows "
+                         f"({ts:.1f} s), extrapolated x{S}/{rows} rows x 28 blocks x {T} steps x "
+                         f"recompute fraction {frac:.3f}; attention excluded"}
+    tops = g_ops / g_time / 1e12 if g_time > 0 else None
+    peak_tops = peak.get("tops") or NOMINAL_INT8_TOPS
+    line = {
+        "metric": "videos_per_s", "value": value, "unit": "videos/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic latents, random-init weights",
+        "config": {"workload": "C3: STDiT-XL/2 dims (28x1152, 16 heads, FFN 4608, cond 4096), "
+                               "16 frames 256x256 (S=4096), DDPM T=100, full QuantCache",
+                   "videos_per_gpu_per_step": B, "timesteps": T, "weight_bits": args.wbits,
+                   "parallelism": f"video-sharded x{world}", "attention": "bf16 SDPA (library)",
+                   "noise": "device Philox", "l2": "inputs > L2 (activation arena "
+                   f"{eng.arena.numel() * 4 / 2**30:.1f} GiB)",
+                   "thresholds": {"delta1": th.delta1, "delta2": th.delta2,
+                                  "v_low": th.v_low, "v_high": th.v_high}},
+        "s_per_video": elapsed / (args.steps * B),
+        "recompute_fraction": frac,
+        "executed_bit_macs_per_video": executed / (args.steps * B),
+        "roofline": {"bound": "tensor", "achieved": tops, "peak": peak_tops, "unit": "TOP/s",
+                     "frac": (tops / peak_tops) if tops else None, "traffic": None,
+                     "kernel": "gemm_u8_tcgen05", "peak_source": peak.get("source"),
+                     "nominal_int8_dense_tops": NOMINAL_INT8_TOPS,
+                     "gemm_share_of_step": g_time / elapsed if elapsed else None,
+                     "per_site": {s: {"tops": a[0] / a[1] / 1e12, "launches": a[2],
+                                      "ms_total": a[1] * 1e3} for s, a in per_site.items()}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_vps, "unit": "videos/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -151,16 +151,21 @@ static FeatP fp(QcbFeat f) { return FeatP{f.base, f.ld, f.row0}; }
 
 using namespace qc;
 
+// Workspace layout is independent of nseg so one zero-initialised buffer can
+// serve calls of any segment count: [kMaxSegs tickets][partials].  Tickets are
+// returned to zero by the last CTA of each segment.
+constexpr int kMaxSegs = 4096;
+
 extern "C" size_t qcb_reduce_workspace_bytes(int nseg) {
-  return (size_t)nseg * kMaxChunks * 3 * sizeof(double) + (size_t)nseg * sizeof(int) + 256;
+  return (size_t)kMaxSegs * sizeof(int) + (size_t)nseg * kMaxChunks * 3 * sizeof(double) + 256;
 }
 
 template <int KIND, int NV>
 static int launch_reduce(QcbFeat a, QcbFeat b, QcbFeat c, int rows, int cols, int nseg,
                          const int* seg_active, double* res, void* ws, void* stream) {
-  if (rows <= 0 || cols <= 0 || nseg <= 0) return QCB_ERR_DIM;
-  double* partials = reinterpret_cast<double*>(ws);
-  int* tickets = reinterpret_cast<int*>(partials + (size_t)nseg * kMaxChunks * 3);
+  if (rows <= 0 || cols <= 0 || nseg <= 0 || nseg > kMaxSegs) return QCB_ERR_DIM;
+  int* tickets = reinterpret_cast<int*>(ws);
+  double* partials = reinterpret_cast<double*>(tickets + kMaxSegs);
   const int ch = chunks_for(rows, cols, nseg);
   seg_reduce<KIND, NV><<<dim3(ch, nseg), kRThreads, 0, (cudaStream_t)stream>>>(
       fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch);

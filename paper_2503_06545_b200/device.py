@@ -20,6 +20,15 @@ from . import _native as N
 from .errors import DimensionError
 
 
+# Count of libqcb200 kernel launches issued (the bench reports the number issued
+# inside its timed region as `gpu_launches`).
+LAUNCHES = [0]
+
+
+def count(n: int = 1):
+    LAUNCHES[0] += n
+
+
 def round16(k: int) -> int:
     return (k + 15) // 16 * 16
 
@@ -70,6 +79,7 @@ def weight_prep(w: torch.Tensor, bits: int, chan_scale: Optional[torch.Tensor] =
                         ldk, N.ptr(scale), N.ptr(zero), N.ptr(colsum), N.ptr(w_eff),
                         N.ptr(w_deq))
     N.check(N.lib().qcb_weight_prep(C.byref(d), N.stream_ptr(stream)), "weight_prep")
+    count(1)
     return PackedWeight(codes, scale, zero, colsum, K, Nn, bits, chan_scale, signs, w_deq, w_eff)
 
 
@@ -161,6 +171,7 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
     q.ldc, q.ldxe = ldc, ldxe
     q.workspace = N.ptr(_WS.get(8 * 3 * nseg + 64))
     N.check(N.lib().qcb_act_quant(C.byref(q), N.stream_ptr(stream)), "act_quant")
+    count(3)
     return res
 
 
@@ -190,6 +201,7 @@ def gemm_u8(a: ActCodes, w: PackedWeight, M: Optional[int] = None, out=None,
     g.gate, g.gate_scalar = N.ptr(gate_vec), float(gate)
     g.epilogue, g.block_n, g.seg_active = epilogue, block_n, N.ptr(seg_active)
     N.check(N.lib().qcb_gemm_u8(C.byref(g), N.stream_ptr(stream)), "gemm_u8")
+    count(1)
     return out
 
 
@@ -215,6 +227,7 @@ def gemm_f64(a: torch.Tensor, w: torch.Tensor, out=None, epilogue: int = N.EPI_S
     g.resid_row0, g.bias = N.ptr(resid_row0), N.ptr(bias)
     g.gate_scalar, g.epilogue = float(gate), epilogue
     N.check(N.lib().qcb_gemm_f64(C.byref(g), N.stream_ptr(stream)), "gemm_f64")
+    count(1)
     return out
 
 
@@ -230,6 +243,7 @@ def ln_mod(x: torch.Tensor, gamma=None, beta=None, scale1: float = 1.0, shift: f
                    N.ptr(out_row0), K, seg_rows or rows // nseg, seg_valid or 0, nseg,
                    N.ptr(gamma), N.ptr(beta), float(scale1), float(shift))
     N.check(N.lib().qcb_ln_mod(C.byref(q), N.stream_ptr(stream)), "ln_mod")
+    count(1)
     return out
 
 
@@ -246,6 +260,7 @@ def attention_f64(q, k, v, heads: int, out=None, nseg: int = 1, S=None, Skv=None
                        N.ptr(out), out.stride(0), S, Skv, heads, d // heads, nseg, S, Skv, S,
                        seg_valid or 0)
     N.check(N.lib().qcb_attention_f64(C.byref(a), N.stream_ptr(stream)), "attention")
+    count(1)
     return out
 
 
@@ -254,6 +269,7 @@ def ddpm(x, eps, c1: float, c2: float, noise=None, c3: float = 0.0, out=None, st
         out = torch.empty_like(x)
     d = N.QcbDdpm(N.ptr(x), N.ptr(eps), N.ptr(noise), N.ptr(out), x.numel(), c1, c2, c3)
     N.check(N.lib().qcb_ddpm_step(C.byref(d), N.stream_ptr(stream)), "ddpm_step")
+    count(1)
     return out
 
 
@@ -271,6 +287,7 @@ def reduce_hlc(out: N.QcbFeat, ref: N.QcbFeat, prev: N.QcbFeat, rows: int, cols:
                nseg: int, res: torch.Tensor, seg_active=None, stream=None):
     N.check(N.lib().qcb_reduce_hlc(out, ref, prev, rows, cols, nseg, N.ptr(seg_active),
                                    N.ptr(res), _rws(nseg), N.stream_ptr(stream)), "reduce_hlc")
+    count(1)
     return res
 
 
@@ -278,6 +295,7 @@ def reduce_srap(a: N.QcbFeat, b: N.QcbFeat, rows: int, cols: int, nseg: int,
                 res: torch.Tensor, seg_active=None, stream=None):
     N.check(N.lib().qcb_reduce_srap(a, b, rows, cols, nseg, N.ptr(seg_active), N.ptr(res),
                                     _rws(nseg), N.stream_ptr(stream)), "reduce_srap")
+    count(1)
     return res
 
 
@@ -285,6 +303,7 @@ def reduce_l1(x: N.QcbFeat, h: N.QcbFeat, rows: int, cols: int, nseg: int,
               res: torch.Tensor, stream=None):
     N.check(N.lib().qcb_reduce_l1(x, h, rows, cols, nseg, N.ptr(res), _rws(nseg),
                                   N.stream_ptr(stream)), "reduce_l1")
+    count(1)
     return res
 
 

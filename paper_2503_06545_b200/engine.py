@@ -135,6 +135,7 @@ class QuantCacheEngine:
         self.sign_seed, self.prune_seed = sign_seed, prune_seed
         self.block_cost = block_mac_cost(self.cfg)
         self.head_macs = head_mac_cost(self.cfg)
+        self.gemm_profile: Optional[list] = None   # set to [] to time every u8 GEMM
         self._upload_weights(act_absmax or {})
         self._alloc()
 
@@ -216,21 +217,34 @@ class QuantCacheEngine:
         self.mask = torch.zeros((L, nv), dtype=torch.int32, device=dev)
         self.hist_l1 = torch.zeros((self.th.history_k + 1, nv), dtype=torch.float64, device=dev)
         self.hlc = torch.zeros((nv, 2), dtype=torch.float64, device=dev)
-        self.idx_host = torch.zeros(1 << 16, dtype=torch.int64).pin_memory()
-        self.idx_dev = torch.zeros(1 << 16, dtype=torch.int64, device=dev)
+        n_idx = 2 * max(1 << 15, 16 * L * (nv + 4) + 64)
+        self.idx_host = torch.zeros(n_idx, dtype=torch.int64).pin_memory()
+        self.idx_dev = torch.zeros(n_idx, dtype=torch.int64, device=dev)
+        self._begin_step(0)
 
     # ------------------------------------------------------------------ index tables
+    def _begin_step(self, t: int):
+        """Staging for index tables is double-buffered by step parity: every
+        upload of step t gets a fresh region of half (t & 1), and the plan sync
+        of step t-1 guarantees step t-2's copies (same half) have retired."""
+        half = self.idx_host.numel() // 2
+        self._idx_base = (t & 1) * half
+        self._idx_end = self._idx_base + half
+        self._idx_cur = self._idx_base
+
     def _upload_idx(self, arrays: Sequence[Sequence[int]]) -> List[torch.Tensor]:
-        """Pack small int64 row tables into one pinned buffer, one H2D copy."""
+        """Pack small int64 row tables into a pinned region, one H2D copy."""
         sizes = [len(a) for a in arrays]
         total = sum(sizes)
-        if total > self.idx_host.numel():
-            raise RuntimeError("index table overflow")
-        flat = np.concatenate([np.asarray(a, np.int64) for a in arrays]) if total else \
-            np.zeros(0, np.int64)
-        self.idx_host[:total].numpy()[:] = flat
-        self.idx_dev[:total].copy_(self.idx_host[:total], non_blocking=True)
-        out, off = [], 0
+        lo = self._idx_cur
+        if lo + total > self._idx_end:
+            raise RuntimeError("index table staging overflow")
+        if total:
+            flat = np.concatenate([np.asarray(a, np.int64) for a in arrays])
+            self.idx_host[lo:lo + total].numpy()[:] = flat
+            self.idx_dev[lo:lo + total].copy_(self.idx_host[lo:lo + total], non_blocking=True)
+        self._idx_cur = lo + total
+        out, off = [], lo
         for n in sizes:
             out.append(self.idx_dev[off:off + n])
             off += n
@@ -265,10 +279,19 @@ class QuantCacheEngine:
             Dv.act_quant(x, bits, trs, seg_rows=seg_rows, seg_valid=seg_valid, nseg=nseg,
                          x_row0=x_row0, ln=ln, mod=mod, out=acs)
             targets = outs or [out]
+            prof = self.gemm_profile
             for o, p in enumerate(pws):
+                if prof is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
                 Dv.gemm_u8(acs[o], p, M=M, out=targets[o], epilogue=epi, resid=resid,
                            gate=gate, seg_rows=seg_rows, seg_valid=seg_valid,
                            out_row0=out_row0, resid_row0=resid_row0)
+                if prof is not None:
+                    e1.record()
+                    # algorithmic work: 2*M_valid*N*K ops (padding rows excluded)
+                    prof.append((e0, e1, 2 * nseg * seg_valid * p.N * p.K, sites[o]))
             return
         # full-precision GEMMs (weight-only, act-only or plain)
         for o, s in enumerate(sites):
@@ -322,6 +345,7 @@ class QuantCacheEngine:
                            Sp, S)
         N.check(N.lib().qcb_attention_f64(C.byref(a), N.stream_ptr()), "attention")
 
+
     def _block(self, l, t, vids, bits, xin_row0, out_row0, cond_row0):
         """block_forward (model.py:159-199) for the videos `vids` at one bits."""
         n = len(vids)
@@ -351,10 +375,19 @@ class QuantCacheEngine:
                    out_row0=out_row0, resid=A, resid_row0=out_row0, gate=g3)
 
     # ------------------------------------------------------------------ run
-    def generate(self, seeds: Sequence[int], device_noise_seed: Optional[int] = None):
+    def generate(self, seeds: Sequence[int], device_noise_seed: Optional[int] = None,
+                 collect_features: Optional[list] = None, x0_dev: Optional[torch.Tensor] = None,
+                 cond_dev: Optional[torch.Tensor] = None, return_device: bool = False):
         """Run the full reverse trajectory for len(seeds) videos (one per seed).
 
-        Returns (latents f32 [nv][F][T][d] on host, traces per video)."""
+        The initial latent and cond are drawn from NumPy's stream per seed like
+        the reference (sampler.py:108-111), unless device-resident x0_dev
+        [nv,S,d] / cond_dev [nv,c] are given (benchmark: inputs already in HBM).
+        collect_features (list, optional): appended per step with
+        (t, x_t [nv,S,d], [block outputs [nv,S,d] per layer]) host copies, like
+        the reference's generate(collect_features=...) (sampler.py:113-126).
+        Returns (latents f32 [nv][F][T][d] on host, or a CUDA tensor with
+        return_device, and traces per video)."""
         nv = len(seeds)
         if nv > self.nv:
             raise ValueError(f"engine sized for {self.nv} videos")
@@ -366,11 +399,15 @@ class QuantCacheEngine:
         for v, seed in enumerate(seeds):
             vs = VideoState(SlotPool(v * self.P, self.P), np.random.default_rng(seed),
                             cache=[None] * L, prev=[None] * L)
-            x0 = vs.rng.standard_normal((F, Tk, d)).astype(np.float32)
-            cond = vs.rng.standard_normal(self.c).astype(np.float32)
             vs.x = vs.pool.alloc()
-            self.slot_view(vs.x).copy_(torch.from_numpy(x0.reshape(S, d)))
-            self.cond[v].copy_(torch.from_numpy(cond))
+            if x0_dev is not None:
+                self.slot_view(vs.x).copy_(x0_dev[v].reshape(S, d))
+                self.cond[v].copy_(cond_dev[v])
+            else:
+                x0 = vs.rng.standard_normal((F, Tk, d)).astype(np.float32)
+                cond = vs.rng.standard_normal(self.c).astype(np.float32)
+                self.slot_view(vs.x).copy_(torch.from_numpy(x0.reshape(S, d)))
+                self.cond[v].copy_(torch.from_numpy(cond))
             vids.append(vs)
         gen = None
         if self.opts.noise == "device":
@@ -380,6 +417,7 @@ class QuantCacheEngine:
         lib = N.lib()
         sp = N.stream_ptr()
         for t in range(T - 1, -1, -1):
+            self._begin_step(t)
             # ---------------- plan (device) ----------------
             nh = len(vids[0].hist)
             srap_layers = []
@@ -401,9 +439,11 @@ class QuantCacheEngine:
                 Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]), Dv.feat(self.arena, tabs[2 * j + 1]),
                              S, d, nv, self.hist_l1[j])
             N.check(lib.qcb_policy_plan_reuse(pol, nv, L, t, self.thc, sp), "plan_reuse")
+
             if srap_layers:
                 N.check(lib.qcb_policy_sim_mask(pol, nv, L, self.thc, N.ptr(self.mask), sp),
                         "sim_mask")
+
                 for i, l in enumerate(srap_layers):
                     a, b = tabs[2 * nh + 2 * i], tabs[2 * nh + 2 * i + 1]
                     Dv.reduce_srap(Dv.feat(self.arena, a), Dv.feat(self.arena, b), S, d, nv,
@@ -411,6 +451,7 @@ class QuantCacheEngine:
             N.check(lib.qcb_policy_plan_finish(pol, nv, L, t, self.thc, N.ptr(self.srap),
                                                N.ptr(self.hist_l1), nh,
                                                N.ptr(self.draws[t]), 0, sp), "plan_finish")
+
             self.pol_host.copy_(self.pol, non_blocking=True)
             st.synchronize()
             plans = [N.QcbPolicyVideo.from_buffer_copy(
@@ -420,6 +461,7 @@ class QuantCacheEngine:
                 vs.seen += 1
             # ---------------- execute blocks ----------------
             cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
+            feats = [] if collect_features is not None else None
             for l in range(L):
                 outs = list(cur)
                 rec = [v for v in range(nv) if plans[v].action[l] == N.ACT_RECOMPUTE]
@@ -458,6 +500,7 @@ class QuantCacheEngine:
                                   seg_active=act)
                 N.check(lib.qcb_policy_observe(pol, nv, l, t, self.thc, N.ptr(self.hlc), sp),
                         "observe")
+
                 # host mirror of the cache / prev references (schedule.py:349-351)
                 for v, vs in enumerate(vids):
                     if plans[v].action[l] == N.ACT_RECOMPUTE and t > 0:
@@ -467,6 +510,11 @@ class QuantCacheEngine:
                     vs.prev[l] = vs.pool.inc(outs[v])
                     vs.pool.dec(cur[v])
                 cur = outs
+                if feats is not None:
+                    feats.append(torch.stack([self.slot_view(s) for s in cur]).cpu().numpy())
+            if collect_features is not None:
+                x_now = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
+                collect_features.append((t, x_now, feats))
             # ---------------- head + sampler update ----------------
             tabh = self._upload_idx([[self.rows(c) for c in cur]])
             Dv.gemm_f64(self.arena, self.head_w, out=self.eps, epilogue=N.EPI_BIAS,
@@ -502,10 +550,13 @@ class QuantCacheEngine:
                 if len(vs.hist) > self.th.history_k:
                     vs.pool.dec(vs.hist.pop(0))
                 vs.x = new
-        out = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
-        traces = self._collect_traces(vids)
-        # release everything for the next call
-        return out.reshape(nv, F, Tk, d), traces
+        out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
+        if return_device:
+            return out, vids
+        return out.cpu().numpy(), self._collect_traces(vids)
+
+    def traces_of(self, vids) -> List[List[TraceRecord]]:
+        return self._collect_traces(vids)
 
     def _collect_traces(self, vids) -> List[List[TraceRecord]]:
         raw = self.pol_trace.cpu().numpy()

@@ -1,0 +1,111 @@
+"""End-to-end parity of the device engine with the REFERENCE on its own
+configs: every ablation toggle set of the small config (seed 3) and the
+default benchmark config (seed 7), with the reference's calibration.
+
+Bars: decisions (actions, activation bits, weight bits, billed MACs) identical
+at every (step, layer); D / S / V within 1e-9 relative (f64 sums in another
+order); final latents bit-identical (asserted) -- the stated tolerance if a
+future change breaks exactness would be rtol 1e-5 / atol 1e-5."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+CASES = [(c, t) for c in ("small", "default")
+         for t in ("none", "hlc", "hlc_aigq", "full", "aigq")]
+TOGGLES = {"none": {}, "hlc": dict(hlc=True),
+           "hlc_aigq": dict(hlc=True, aigq_weights=True, aigq_acts=True),
+           "full": dict(hlc=True, aigq_weights=True, aigq_acts=True, srap=True),
+           "aigq": dict(aigq_weights=True, aigq_acts=True)}
+SMALL = {"seed": 3, "model": {"num_blocks": 3, "model_dim": 16, "num_heads": 2,
+                              "tokens_per_frame": 4, "frames": 2, "cond_dim": 8},
+         "schedule": {"steps": 10}}
+
+
+def _cfg(golden_dir, cname, tname):
+    from paper_2503_06545_b200 import harness
+    base = dict(SMALL) if cname == "small" else {"seed": 7}
+    base = dict(base, calibration=os.path.join(golden_dir, f"calib_{cname}.json"),
+                toggles=TOGGLES[tname])
+    return harness.parse_config(base)
+
+
+@pytest.fixture(scope="module")
+def runs(golden_dir, cuda_dev):
+    return np.load(os.path.join(golden_dir, "runs.npz"))
+
+
+@pytest.mark.parametrize("cname,tname", CASES)
+def test_run_matches_reference(golden_dir, runs, cname, tname):
+    from paper_2503_06545_b200 import harness
+    cfg = _cfg(golden_dir, cname, tname)
+    calib = harness.load_calibration(cfg.calibration)
+    res = harness.run_single(cfg, cfg.toggles_obj(), calib)
+    ref_trace = [json.loads(l) for l in
+                 open(os.path.join(golden_dir, f"trace_{cname}_{tname}.jsonl"))]
+    got = [r.to_json_obj() for r in res.scheduler.trace]
+    assert len(got) == len(ref_trace)
+    for a, b in zip(ref_trace, got):
+        for k in ("t", "layer", "action", "bits", "wbits", "macs"):
+            assert a[k] == b[k], (k, a, b)
+        for k in ("D", "S", "V"):
+            if a[k] is None:
+                assert b[k] is None or (k == "V" and a["layer"] == "head"), (k, a, b)
+            else:
+                assert b[k] == pytest.approx(a[k], rel=1e-9, abs=1e-12), (k, a, b)
+    meta = json.load(open(os.path.join(golden_dir, "runs_meta.json")))[f"{cname}_{tname}"]
+    assert res.scheduler.executed_macs() == meta["executed"]
+    assert res.scheduler.baseline_macs() == meta["baseline"]
+    want = runs[f"{cname}_{tname}"]
+    assert res.output.shape == want.shape
+    assert np.array_equal(res.output, want), float(np.abs(res.output - want).max())
+
+
+def test_reference_metrics_reproduced(golden_dir, runs):
+    """reference_metrics.json: full-stack MSE / PSNR / bit-weighted MAC speedup."""
+    from paper_2503_06545_b200 import harness
+    cfg = _cfg(golden_dir, "default", "full")
+    calib = harness.load_calibration(cfg.calibration)
+    metrics, trace, base, conf = harness.run_benchmark(cfg, calib=calib)
+    assert metrics.speedup_mac == 47.54406614227479
+    assert metrics.mse_vs_baseline == pytest.approx(32.10987246021118, rel=1e-12)
+    assert metrics.psnr_vs_baseline == pytest.approx(12.832895012303487, rel=1e-12)
+    # golden_default (sha256 recorded in runs_meta.json) is the disabled path
+    import hashlib
+    meta = json.load(open(os.path.join(golden_dir, "runs_meta.json")))
+    assert hashlib.sha256(base.astype("<f4").tobytes()).hexdigest() == \
+        meta["golden_default_sha256"]
+
+
+def test_batched_videos_match_single(golden_dir):
+    """Per-video decisions in one batched engine call equal separate runs."""
+    from paper_2503_06545_b200 import harness
+    cfg = _cfg(golden_dir, "small", "full")
+    calib = harness.load_calibration(cfg.calibration)
+    eng, _ = harness.build_engine(cfg, cfg.toggles_obj(), calib, max_videos=3)
+    outs, traces = eng.generate([3, 11, 12])
+    for i, seed in enumerate([3, 11, 12]):
+        e1, _ = harness.build_engine(cfg, cfg.toggles_obj(), calib, max_videos=1)
+        o1, t1 = e1.generate([seed])
+        assert np.array_equal(outs[i], o1[0])
+        assert [r.to_json_obj() for r in traces[i]] == [r.to_json_obj() for r in t1[0]]
+
+
+def test_repeat_runs_byte_identical(golden_dir):
+    """Criterion 9 (test_acceptance.py:256-286) on the device path."""
+    from paper_2503_06545_b200 import harness
+    cfg = harness.parse_config(dict(SMALL, toggles={"hlc": True, "aigq_acts": True,
+                                                     "srap": True},
+                                    thresholds={"delta1": 100.0, "delta2": 300.0,
+                                                "v_low": 50.0, "v_high": 150.0}))
+    a = harness.run_single(cfg, cfg.toggles_obj())
+    b = harness.run_single(cfg, cfg.toggles_obj())
+    assert a.output.tobytes() == b.output.tobytes()
+    assert [r.to_json_obj() for r in a.scheduler.trace] == \
+        [r.to_json_obj() for r in b.scheduler.trace]
