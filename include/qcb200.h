@@ -87,6 +87,7 @@ typedef struct QcbGemm {
   int epilogue;
   int block_n;                 /* 0 = auto                                      */
   const int* seg_active;       /* nullable: per-segment flag, skip inactive     */
+  long long out_rows;          /* rows of the output buffer (TMA bounds); 0 = M */
 } QcbGemm;
 
 int qcb_gemm_u8(const QcbGemm* g, void* stream);

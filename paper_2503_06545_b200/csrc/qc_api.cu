@@ -84,6 +84,6 @@ extern "C" int qcb_device_sm_count(void) { return num_sms(); }
 
 extern "C" const char* qcb_version(void) { return "qcb200 0.1.0 sm_100a"; }
 
-extern "C" const char* qcb_last_error(void) {
-  return cudaGetErrorString(cudaPeekAtLastError());
-}
+cudaError_t qc::g_last_err = cudaSuccess;
+
+extern "C" const char* qcb_last_error(void) { return cudaGetErrorString(qc::g_last_err); }

@@ -5,6 +5,28 @@
 #include "../../include/qcb200.h"
 
 namespace qc {
+// Last CUDA error seen by a launcher (reported by qcb_last_error()).
+extern cudaError_t g_last_err;
+
+// Status of the launch just issued: QCB_OK or QCB_ERR_CUDA (error recorded).
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_last_err = e;
+    return QCB_ERR_CUDA;
+  }
+  return QCB_OK;
+}
+
+// Opt a kernel into the full dynamic shared-memory carve-out once.
+template <typename K>
+inline void allow_max_smem(K kernel, bool& done) {
+  if (!done) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    done = true;
+  }
+}
+
 int num_sms();
 int pick_block_n(int N);
 int gemm_u8_launch(const QcbGemm* g, cudaStream_t st);

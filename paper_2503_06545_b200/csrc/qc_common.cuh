@@ -67,6 +67,25 @@ QC_DEV void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0
       : "memory");
 }
 
+// 2-D tiled bulk tensor store from CTA shared memory (bulk-group completion).
+QC_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
+QC_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+QC_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+QC_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Generic-proxy shared-memory writes -> visible to the async (TMA) proxy.
+QC_DEV void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+QC_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 QC_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 QC_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -166,59 +185,66 @@ QC_DEV double scale_up16(double s) {
 // symmetry, 1 - erfc for |x| > 1), which the reference's GELU calls
 // (model.py:145-147).  Matching the formulation keeps 1 + erf(x) identical in
 // the cancellation region x << 0; only exp() may differ from glibc by an ulp.
-QC_DEV double polevl(double x, const double* c, int n) {
-  double a = c[0];
-  for (int i = 1; i <= n; ++i) a = __dadd_rn(__dmul_rn(a, x), c[i]);
-  return a;
-}
-QC_DEV double p1evl(double x, const double* c, int n) {
-  double a = __dadd_rn(x, c[0]);
-  for (int i = 1; i < n; ++i) a = __dadd_rn(__dmul_rn(a, x), c[i]);
-  return a;
-}
+// Horner steps as cephes polevl/p1evl evaluate them (separate mul and add, no
+// FMA); coefficients are literals so nothing spills to local memory.
+#define QC_H(a, x, c) __dadd_rn(__dmul_rn((a), (x)), (c))
 QC_DEV double erfc_pos(double x) {  // x >= 1
-  const double P[] = {2.46196981473530512524E-10, 5.64189564831068821977E-1,
-                      7.46321056442269912687E0,   4.86371970985681366614E1,
-                      1.96520832956077098242E2,   5.26445194995477358631E2,
-                      9.34528527171957607540E2,   1.02755188689515710272E3,
-                      5.57535335369399327526E2};
-  const double Q[] = {1.32281951154744992508E1, 8.67072140885989742329E1,
-                      3.54937778887819891062E2, 9.75708501743205489753E2,
-                      1.82390916687909736289E3, 2.24633760818710981792E3,
-                      1.65666309194161350182E3, 5.57535340817727675546E2};
-  const double R[] = {5.64189583547755073984E-1, 1.27536670759978104416E0,
-                      5.01905042251180477414E0,  6.16021097993053585195E0,
-                      7.40974269950448939160E0,  2.97886665372100240670E0};
-  const double S[] = {2.26052863220117276590E0, 9.39603524938001434673E0,
-                      1.20489539808096656605E1, 1.70814450747565897222E1,
-                      9.60896809063285878198E0, 3.36907645100081516050E0};
   const double z0 = -__dmul_rn(x, x);
   if (z0 < -7.09782712893383996843E2) return 0.0;
   const double z = exp(z0);
   double p, q;
   if (x < 8.0) {
-    p = polevl(x, P, 8);
-    q = p1evl(x, Q, 8);
+    p = 2.46196981473530512524E-10;
+    p = QC_H(p, x, 5.64189564831068821977E-1);
+    p = QC_H(p, x, 7.46321056442269912687E0);
+    p = QC_H(p, x, 4.86371970985681366614E1);
+    p = QC_H(p, x, 1.96520832956077098242E2);
+    p = QC_H(p, x, 5.26445194995477358631E2);
+    p = QC_H(p, x, 9.34528527171957607540E2);
+    p = QC_H(p, x, 1.02755188689515710272E3);
+    p = QC_H(p, x, 5.57535335369399327526E2);
+    q = __dadd_rn(x, 1.32281951154744992508E1);
+    q = QC_H(q, x, 8.67072140885989742329E1);
+    q = QC_H(q, x, 3.54937778887819891062E2);
+    q = QC_H(q, x, 9.75708501743205489753E2);
+    q = QC_H(q, x, 1.82390916687909736289E3);
+    q = QC_H(q, x, 2.24633760818710981792E3);
+    q = QC_H(q, x, 1.65666309194161350182E3);
+    q = QC_H(q, x, 5.57535340817727675546E2);
   } else {
-    p = polevl(x, R, 5);
-    q = p1evl(x, S, 6);
+    p = 5.64189583547755073984E-1;
+    p = QC_H(p, x, 1.27536670759978104416E0);
+    p = QC_H(p, x, 5.01905042251180477414E0);
+    p = QC_H(p, x, 6.16021097993053585195E0);
+    p = QC_H(p, x, 7.40974269950448939160E0);
+    p = QC_H(p, x, 2.97886665372100240670E0);
+    q = __dadd_rn(x, 2.26052863220117276590E0);
+    q = QC_H(q, x, 9.39603524938001434673E0);
+    q = QC_H(q, x, 1.20489539808096656605E1);
+    q = QC_H(q, x, 1.70814450747565897222E1);
+    q = QC_H(q, x, 9.60896809063285878198E0);
+    q = QC_H(q, x, 3.36907645100081516050E0);
   }
   return __ddiv_rn(__dmul_rn(z, p), q);
 }
 QC_DEV double erf_cephes(double x) {
-  const double T[] = {9.60497373987051638749E0, 9.00260197203842689217E1,
-                      2.23200534594684319226E3, 7.00332514112805075473E3,
-                      5.55923013010394962768E4};
-  const double U[] = {3.35617141647503099647E1, 5.21357949780152679795E2,
-                      4.59432382970980127987E3, 2.26290000613890934246E4,
-                      4.92673942608635921086E4};
   const double ax = fabs(x);
   double r;
   if (ax > 1.0) {
     r = __dsub_rn(1.0, erfc_pos(ax));
   } else {
     const double z = __dmul_rn(ax, ax);
-    r = __ddiv_rn(__dmul_rn(ax, polevl(z, T, 4)), p1evl(z, U, 5));
+    double t = 9.60497373987051638749E0;
+    t = QC_H(t, z, 9.00260197203842689217E1);
+    t = QC_H(t, z, 2.23200534594684319226E3);
+    t = QC_H(t, z, 7.00332514112805075473E3);
+    t = QC_H(t, z, 5.55923013010394962768E4);
+    double u = __dadd_rn(z, 3.35617141647503099647E1);
+    u = QC_H(u, z, 5.21357949780152679795E2);
+    u = QC_H(u, z, 4.59432382970980127987E3);
+    u = QC_H(u, z, 2.26290000613890934246E4);
+    u = QC_H(u, z, 4.92673942608635921086E4);
+    r = __ddiv_rn(__dmul_rn(ax, t), u);
   }
   return x < 0.0 ? -r : r;
 }

@@ -93,7 +93,7 @@ int gemm_f64_launch(const QcbGemmF64* g, cudaStream_t st) {
   GemmF64P P{*g};
   dim3 grid((g->N + kFT - 1) / kFT, (g->M + kFT - 1) / kFT);
   gemm_f64_k<<<grid, 256, 0, st>>>(P);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  return launch_status();
 }
 
 // ------------------------------------------------------------------ ln + mod
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) ln_mod_k(const QcbLnMod q) {
 int ln_mod_launch(const QcbLnMod* q, cudaStream_t st) {
   dim3 grid(q->seg_valid > 0 ? q->seg_valid : q->seg_rows, q->nseg);
   ln_mod_k<<<grid, 256, 0, st>>>(*q);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  return launch_status();
 }
 
 // ------------------------------------------------------------------ attention
@@ -215,18 +215,34 @@ __global__ void __launch_bounds__(128) attention_f64_k(const QcbAttention a) {
   }
 }
 
+// Cross-attention on the single cond token (model.py:190-193): the softmax over
+// one key is exactly 1 (exp(0)/exp(0)), and mm(p, v) = f32(0 + 1.0*v) = v, so
+// every query row's output is the value row -- identical bits, one copy.
+__global__ void attention_single_key_k(const QcbAttention a) {
+  const int seg = blockIdx.y;
+  const int d = a.heads * a.dh;
+  const float* vrow = a.v + (long long)seg * a.kv_seg_stride * a.ldv;
+  const int valid = a.seg_valid > 0 ? a.seg_valid : a.S;
+  for (int i = blockIdx.x; i < valid; i += gridDim.x) {
+    float* orow = a.out + ((long long)seg * a.o_seg_stride + i) * a.ldo;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) orow[j] = vrow[j];
+  }
+}
+
 int attention_f64_launch(const QcbAttention* a, cudaStream_t st) {
+  if (a->Skv == 1) {
+    dim3 grid((unsigned)min(a->S, 1024), a->nseg);
+    attention_single_key_k<<<grid, 128, 0, st>>>(*a);
+    return launch_status();
+  }
   if (a->dh > 256) return QCB_ERR_DIM;
   const size_t smem = (size_t)a->Skv * sizeof(double);
   if (smem > 200 * 1024) return QCB_ERR_DIM;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(attention_f64_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  static bool attr = false;
+  allow_max_smem(attention_f64_k, attr);
   dim3 grid(a->seg_valid > 0 ? a->seg_valid : a->S, a->heads, a->nseg);
   attention_f64_k<<<grid, 128, smem, st>>>(*a);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  return launch_status();
 }
 
 // ------------------------------------------------------------------ ddpm
@@ -241,7 +257,7 @@ __global__ void ddpm_k(const QcbDdpm d) {
 int ddpm_launch(const QcbDdpm* d, cudaStream_t st) {
   const int th = 256;
   ddpm_k<<<(unsigned)((d->n + th - 1) / th), th, 0, st>>>(*d);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  return launch_status();
 }
 
 }  // namespace qc

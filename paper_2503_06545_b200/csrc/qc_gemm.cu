@@ -42,7 +42,12 @@ struct GemmCfg {
                                         : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256
                                                           : 512;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  // epilogue: 4 warps x one 32x32 f32 staging tile (128B-swizzled, TMA store)
+  static constexpr int kStageOutBytes = 4 * 32 * 32 * 4;
+  // per-tile column parameters, double-buffered by accumulator stage
+  static constexpr int kColBytes = 2 * BN * (8 + 4 + 4);
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kStageOutBytes + kColBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct GemmParams {
@@ -66,20 +71,26 @@ struct GemmParams {
   float gate_scalar;
   int mode;
   const int* seg_active;  // nullable: skip tiles of inactive segments
+  int tma_store;          // 1: each 32-row warp slab maps to contiguous output rows
 };
 
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_u8_tcgen05(const __grid_constant__ CUtensorMap map_a,
-                    const __grid_constant__ CUtensorMap map_b, const GemmParams p) {
+                    const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_out, const GemmParams p) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + Cfg::kStages * Cfg::kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint8_t* smem_out = smem + Cfg::kStages * Cfg::kStageBytes;           // 1024-aligned
+  double* col_sw = reinterpret_cast<double*>(smem_out + Cfg::kStageOutBytes);  // [2][BN]
+  int* col_zw = reinterpret_cast<int*>(col_sw + 2 * BN);                      // [2][BN]
+  int* col_cs = col_zw + 2 * BN;                                               // [2][BN]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(col_cs + 2 * BN);
   uint64_t* empty_bar = full_bar + Cfg::kStages;
   uint64_t* tfull_bar = empty_bar + Cfg::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -175,12 +186,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (TMEM -> regs -> global)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int et = threadIdx.x - 128;  // 0..127 epilogue thread id
+    uint8_t* stage_out = smem_out + q * 4096;
+    const bool resid_mode = (p.mode == QCB_EPI_GATE_RESID || p.mode == QCB_EPI_RESID);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       if (!tile_active(tile)) continue;
       const int m0 = (tile / p.num_n_tiles) * kBlockM;
       const int n0 = (tile % p.num_n_tiles) * BN;
+      // per-tile column parameters -> smem (buffer `acc`; see the barrier note)
+      double* t_sw = col_sw + acc * BN;
+      int* t_zw = col_zw + acc * BN;
+      int* t_cs = col_cs + acc * BN;
+      for (int i = et; i < BN; i += 128) {
+        const int n = n0 + i;
+        const bool ok = n < p.N;
+        t_sw[i] = ok ? __ldg(p.sw + n) : 0.0;
+        t_zw[i] = ok ? __ldg(p.zw + n) : 0;
+        t_cs[i] = ok ? __ldg(p.colsum + n) : 0;
+      }
+      // One barrier per tile: a warp can only refill this buffer two tiles
+      // later, after every epilogue warp has passed the next tile's barrier.
+      named_bar_sync(1, 128);
+
       const int m = m0 + q * 32 + lane;
       const int seg = m / p.seg_rows;
       const int mrow = m - seg * p.seg_rows;
@@ -197,65 +226,76 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.out_row0) orow = p.out_row0[seg] + mrow;
         if (p.resid_row0) rrow = p.resid_row0[seg] + mrow;
       }
-      const int kzz = p.K * za;
+      // acc = raw - zw*rowsum - za*colsum + K*za*zw = raw - zw*(rowsum - K*za) - za*colsum
+      const int tr = rs - p.K * za;
+      // first output row of this warp's 32-row slab (TMA store path)
+      const long long orow_slab = __shfl_sync(0xffffffffu, orow, 0);
 
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        const int nb = n0 + c * 32;
+        if (nb >= p.N) break;
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
-        const int nb = n0 + c * 32;
-        if (row_ok && nb < p.N) {
-          float* orow_ptr = p.out + orow * p.ldo;
-          const float* rrow_ptr = p.resid ? p.resid + rrow * p.ldr : nullptr;
+        float v[32];
+        float rv[32];
+        if (resid_mode && row_ok) {
+          const float* rp = p.resid + rrow * p.ldr + nb;
+          if (nb + 32 <= p.N && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
 #pragma unroll
-          for (int j4 = 0; j4 < 32; j4 += 4) {
-            float v[4];
-            float rv[4] = {0.f, 0.f, 0.f, 0.f};
-            const int n4 = nb + j4;
-            const bool full4 = (n4 + 3 < p.N);
-            if (rrow_ptr && (p.mode == QCB_EPI_GATE_RESID || p.mode == QCB_EPI_RESID)) {
-              if (full4 && ((reinterpret_cast<uintptr_t>(rrow_ptr + n4) & 15) == 0)) {
-                float4 t = *reinterpret_cast<const float4*>(rrow_ptr + n4);
-                rv[0] = t.x; rv[1] = t.y; rv[2] = t.z; rv[3] = t.w;
-              } else {
-                for (int e = 0; e < 4; ++e)
-                  if (n4 + e < p.N) rv[e] = rrow_ptr[n4 + e];
-              }
+            for (int j = 0; j < 32; j += 4) {
+              const float4 t4 = *reinterpret_cast<const float4*>(rp + j);
+              rv[j] = t4.x; rv[j + 1] = t4.y; rv[j + 2] = t4.z; rv[j + 3] = t4.w;
             }
+          } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int n = n4 + e;
-              float y = 0.f;
-              if (n < p.N) {
-                const int zw = __ldg(p.zw + n);
-                const int raw = (int)r[j4 + e];
-                const int accv = raw - zw * rs - za * __ldg(p.colsum + n) + kzz * zw;
-                if (p.mode == QCB_EPI_ACC) {
-                  y = __int_as_float(accv);
-                } else {
-                  const double joint = __dmul_rn(sa, __ldg(p.sw + n));
-                  y = __double2float_rn(__dmul_rn(joint, (double)accv));
-                  if (p.mode == QCB_EPI_GELU) {
-                    y = __double2float_rn(gelu_ref((double)y));
-                  } else if (p.mode == QCB_EPI_GATE_RESID) {
-                    y = __fadd_rn(rv[e], __fmul_rn(gate, y));
-                  } else if (p.mode == QCB_EPI_RESID) {
-                    y = __fadd_rn(rv[e], y);
-                  }
-                }
-              }
-              v[e] = y;
-            }
-            if (full4 && ((reinterpret_cast<uintptr_t>(orow_ptr + n4) & 15) == 0)) {
-              *reinterpret_cast<float4*>(orow_ptr + n4) = make_float4(v[0], v[1], v[2], v[3]);
-            } else {
-              for (int e = 0; e < 4; ++e)
-                if (n4 + e < p.N) orow_ptr[n4 + e] = v[e];
+            for (int j = 0; j < 32; ++j) rv[j] = (nb + j < p.N) ? rp[j] : 0.f;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int ci = c * 32 + j;
+          const int accv = (int)r[j] - t_zw[ci] * tr - za * t_cs[ci];
+          float y;
+          if (p.mode == QCB_EPI_ACC) {
+            y = __int_as_float(accv);
+          } else {
+            const double joint = __dmul_rn(sa, t_sw[ci]);
+            y = __double2float_rn(__dmul_rn(joint, (double)accv));
+            if (p.mode == QCB_EPI_GELU) {
+              y = __double2float_rn(gelu_ref((double)y));
+            } else if (p.mode == QCB_EPI_GATE_RESID) {
+              y = __fadd_rn(rv[j], __fmul_rn(gate, y));
+            } else if (p.mode == QCB_EPI_RESID) {
+              y = __fadd_rn(rv[j], y);
             }
           }
+          v[j] = y;
+        }
+        if (p.tma_store) {
+          // 32x32 f32 slab -> 128B-swizzled smem -> one TMA bulk tensor store.
+          if (lane == 0) bulk_wait_read0();  // previous store finished reading
+          __syncwarp();
+          uint8_t* rowp = stage_out + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_out, stage_out, nb, (int)orow_slab);
+            bulk_commit();
+          }
+        } else if (row_ok) {
+          float* op = p.out + orow * p.ldo + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < p.N) op[j] = v[j];
         }
       }
       tc_fence_before();
@@ -266,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait0();
   }
 
   __syncthreads();
@@ -303,6 +344,20 @@ static int make_map_u8(CUtensorMap* map, const void* base, int rows, int K, long
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? QCB_OK : QCB_ERR_CUDA;
+}
+
+// 2-D f32 output [rows][ld] (N valid columns), box 32 x 32, 128-byte swizzle.
+static int make_map_out(CUtensorMap* map, const void* base, long long rows, int N, long long ld) {
+  auto enc = get_encode_fn();
+  if (!enc) return QCB_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? QCB_OK : QCB_ERR_CUDA;
 }
 
@@ -348,6 +403,15 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st) {
   p.gate_scalar = g->gate_scalar;
   p.mode = g->epilogue;
   p.seg_active = g->seg_active;
+  // TMA-store epilogue when every 32-row slab is contiguous in the output.
+  const int nseg = (g->M + p.seg_rows - 1) / p.seg_rows;
+  const bool slab_contig = (p.seg_rows % 32 == 0) || (nseg == 1 && g->out_row0 == nullptr);
+  const long long out_rows = g->out_rows > 0 ? g->out_rows : (long long)g->M;
+  CUtensorMap mo = ma;
+  p.tma_store = 0;
+  if (slab_contig && (g->ldo * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->out) & 15) == 0 &&
+      make_map_out(&mo, g->out, out_rows, g->N, g->ldo) == QCB_OK)
+    p.tma_store = 1;
   static_assert(Cfg::kSmemBytes <= 227 * 1024, "GEMM smem budget exceeds 227 KB");
   static bool attr_set = false;
   if (!attr_set) {
@@ -358,8 +422,8 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st) {
   }
   int tiles = p.num_m_tiles * p.num_n_tiles;
   int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_u8_tcgen05<BN><<<grid, kThreads, Cfg::kSmemBytes, st>>>(ma, mb, p);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  gemm_u8_tcgen05<BN><<<grid, kThreads, Cfg::kSmemBytes, st>>>(ma, mb, mo, p);
+  return launch_status();
 }
 
 int pick_block_n(int N) {

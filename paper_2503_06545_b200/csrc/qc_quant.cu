@@ -257,18 +257,13 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
   init_keys<<<(nkeys + 255) / 256, 256, 0, st>>>(p.keys, nkeys);
   const size_t smem = (size_t)q->K * (sizeof(double) + sizeof(float));
   if (smem > 200 * 1024) return QCB_ERR_DIM;
-  static size_t attr1 = 0, attr2 = 0;
-  if (smem > 48 * 1024 && smem > attr1) {
-    cudaFuncSetAttribute(act_quant_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(act_quant_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr1 = attr2 = smem;
-  }
+  static bool attr1 = false, attr2 = false;
+  allow_max_smem(act_quant_rows<1>, attr1);
+  allow_max_smem(act_quant_rows<2>, attr2);
   dim3 grid(p.seg_valid, p.nseg);
   act_quant_rows<1><<<grid, kQThreads, smem, st>>>(p);
   act_quant_rows<2><<<grid, kQThreads, smem, st>>>(p);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  return launch_status();
 }
 
 // ------------------------------------------------------------------ weights
@@ -370,13 +365,10 @@ int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st) {
   p.w_deq = q->w_deq;
   const size_t smem = (size_t)q->K * sizeof(double);
   if (smem > 200 * 1024) return QCB_ERR_DIM;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(weight_prep_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  static bool attr = false;
+  allow_max_smem(weight_prep_cols, attr);
   weight_prep_cols<<<q->N, kQThreads, smem, st>>>(p);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  return launch_status();
 }
 
 }  // namespace qc

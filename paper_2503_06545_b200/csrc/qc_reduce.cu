@@ -169,7 +169,7 @@ static int launch_reduce(QcbFeat a, QcbFeat b, QcbFeat c, int rows, int cols, in
   const int ch = chunks_for(rows, cols, nseg);
   seg_reduce<KIND, NV><<<dim3(ch, nseg), kRThreads, 0, (cudaStream_t)stream>>>(
       fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch);
-  return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA;
+  return launch_status();
 }
 
 extern "C" int qcb_reduce_hlc(QcbFeat out, QcbFeat ref, QcbFeat prev, int rows, int cols,
@@ -334,7 +334,7 @@ __global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresho
 
 }  // namespace qc
 
-static int launch_ok() { return cudaGetLastError() == cudaSuccess ? QCB_OK : QCB_ERR_CUDA; }
+static int launch_ok() { return launch_status(); }
 
 extern "C" int qcb_policy_plan_reuse(QcbPolicyVideo* st, int nvid, int L, int t,
                                      QcbThresholds th, void* stream) {
