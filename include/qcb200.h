@@ -29,6 +29,7 @@
 #ifndef QCB200_H_
 #define QCB200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -56,7 +57,7 @@ enum {
 };
 
 /* Activation prologues. */
-enum { QCB_PRO_NONE = 0, QCB_PRO_LN_MOD = 1 };
+enum { QCB_PRO_NONE = 0, QCB_PRO_LN_MOD = 1, QCB_PRO_GELU = 2 /* f32(gelu_f64(x)), model.py:197 */ };
 
 #define QCB_MAX_LAYERS 64
 #define QCB_MAX_HIST 8
@@ -142,6 +143,8 @@ typedef struct QcbActQuant {
 } QcbActQuant;
 
 int qcb_act_quant(const QcbActQuant* q, void* stream);
+/* Workspace bytes qcb_act_quant needs (keys, reciprocals, f32 stash of xe). */
+size_t qcb_act_quant_workspace_bytes(int K, int seg_rows, int nseg, int n_out);
 
 typedef struct QcbWeightPrep {
   const float* w;            /* [K][N] f32, reference layout                     */
@@ -268,6 +271,9 @@ int qcb_policy_plan_finish(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresh
  * (schedule.py:330-351). */
 int qcb_policy_observe(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
                        const double* hlc_sums, void* stream);
+/* observe_block for every layer of step t in order, hlc sums [L][nvid][2]. */
+int qcb_policy_observe_all(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
+                           const double* hlc_sums, void* stream);
 
 /* ---------------------------------------------------------------- misc */
 int qcb_device_sm_count(void);

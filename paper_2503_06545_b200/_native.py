@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqcb200.so")
 QCB_OK, QCB_ERR_DIM, QCB_ERR_CONFIG, QCB_ERR_OVERFLOW, QCB_ERR_VALUE, QCB_ERR_TYPE, \
     QCB_ERR_CUDA = range(7)
 EPI_STORE, EPI_GELU, EPI_GATE_RESID, EPI_RESID, EPI_ACC, EPI_BIAS = range(6)
-PRO_NONE, PRO_LN_MOD = 0, 1
+PRO_NONE, PRO_LN_MOD, PRO_GELU = 0, 1, 2
 ACT_RECOMPUTE, ACT_REUSE, ACT_PRUNE = 0, 1, 2
 MAX_LAYERS = 64
 
@@ -130,11 +130,14 @@ def lib():
         "qcb_policy_sim_mask": [vp, i32, i32, QcbThresholds, vp, vp],
         "qcb_policy_plan_finish": [vp, i32, i32, i32, QcbThresholds, vp, vp, i32, vp, i64, vp],
         "qcb_policy_observe": [vp, i32, i32, i32, QcbThresholds, vp, vp],
+        "qcb_policy_observe_all": [vp, i32, i32, i32, QcbThresholds, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(h, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    h.qcb_act_quant_workspace_bytes.argtypes = [i32, i32, i32, i32]
+    h.qcb_act_quant_workspace_bytes.restype = C.c_size_t
     h.qcb_reduce_workspace_bytes.argtypes = [i32]
     h.qcb_reduce_workspace_bytes.restype = C.c_size_t
     h.qcb_device_sm_count.restype = C.c_int
@@ -144,10 +147,11 @@ def lib():
     return h
 
 
-EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_act_quant", "qcb_weight_prep", "qcb_ln_mod",
+EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_act_quant", "qcb_act_quant_workspace_bytes", "qcb_weight_prep", "qcb_ln_mod",
             "qcb_attention_f64", "qcb_ddpm_step", "qcb_reduce_hlc", "qcb_reduce_srap",
             "qcb_reduce_l1", "qcb_reduce_workspace_bytes", "qcb_policy_plan_reuse",
             "qcb_policy_sim_mask", "qcb_policy_plan_finish", "qcb_policy_observe",
+            "qcb_policy_observe_all",
             "qcb_device_sm_count", "qcb_version", "qcb_last_error")
 
 

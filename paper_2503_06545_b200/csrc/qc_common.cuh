@@ -253,6 +253,12 @@ QC_DEV double gelu_ref(double x) {
   const double e = erf_cephes(__ddiv_rn(x, 1.4142135623730951));
   return __dmul_rn(__dmul_rn(0.5, x), __dadd_rn(1.0, e));
 }
+// f32(GELU(x)) for an f32 input.  For x >= 6, erfc(x/sqrt2) < 2^-28 so the f64
+// value is within x*2^-29 of x and rounds back to x: return it directly.
+QC_DEV float gelu_f32_ref(float x) {
+  if (x >= 6.0f) return x;
+  return __double2float_rn(gelu_ref((double)x));
+}
 
 // Float total order as an unsigned key (for atomic min/max on floats).
 QC_DEV uint32_t f2key(float f) {

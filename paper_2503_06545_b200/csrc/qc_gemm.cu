@@ -29,11 +29,12 @@ namespace qc {
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 128;  // bytes == u8 elements
 constexpr int kUmmaK = 32;    // K per tcgen05.mma kind::i8
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;                    // 2 per TMEM lane quarter
+constexpr int kThreads = 128 + 32 * kEpiWarps;  // TMA, MMA, TMEM-alloc, spare + epilogue
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 192 ? 5 : (BN >= 128 ? 6 : 8));
+  static constexpr int kStages = BN >= 256 ? 3 : (BN >= 192 ? 4 : (BN >= 128 ? 5 : (BN >= 64 ? 7 : 8)));
   static constexpr int kABytes = kBlockM * kBlockK;
   static constexpr int kBBytes = BN * kBlockK;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -43,7 +44,7 @@ struct GemmCfg {
                                         : (2 * BN <= 256) ? 256
                                                           : 512;
   // epilogue: 4 warps x one 32x32 f32 staging tile (128B-swizzled, TMA store)
-  static constexpr int kStageOutBytes = 4 * 32 * 32 * 4;
+  static constexpr int kStageOutBytes = kEpiWarps * 32 * 32 * 4;
   // per-tile column parameters, double-buffered by accumulator stage
   static constexpr int kColBytes = 2 * BN * (8 + 4 + 4);
   static constexpr int kSmemBytes =
@@ -75,15 +76,17 @@ struct GemmParams {
 };
 
 
-template <int BN>
+template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_u8_tcgen05(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_out, const GemmParams p) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // Pointers are derived from the __shared__ symbol directly (no integer
+  // round-trip) so the compiler keeps them in the shared window (LDS/STS).
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();  // SW128 operands need 1024B alignment
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + Cfg::kStages * Cfg::kABytes;
   uint8_t* smem_out = smem + Cfg::kStages * Cfg::kStageBytes;           // 1024-aligned
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -186,9 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (TMEM -> regs -> global)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int et = threadIdx.x - 128;  // 0..127 epilogue thread id
-    uint8_t* stage_out = smem_out + q * 4096;
-    const bool resid_mode = (p.mode == QCB_EPI_GATE_RESID || p.mode == QCB_EPI_RESID);
+    const int et = threadIdx.x - 128;        // epilogue thread id
+    const int half = (warp - 4) >> 2;       // which column half of each tile this warp owns
+    uint8_t* stage_out = smem_out + (warp - 4) * 4096;
+    constexpr bool resid_mode = (MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       double* t_sw = col_sw + acc * BN;
       int* t_zw = col_zw + acc * BN;
       int* t_cs = col_cs + acc * BN;
-      for (int i = et; i < BN; i += 128) {
+      for (int i = et; i < BN; i += 32 * kEpiWarps) {
         const int n = n0 + i;
         const bool ok = n < p.N;
         t_sw[i] = ok ? __ldg(p.sw + n) : 0.0;
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // One barrier per tile: a warp can only refill this buffer two tiles
       // later, after every epilogue warp has passed the next tile's barrier.
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 32 * kEpiWarps);
 
       const int m = m0 + q * 32 + lane;
       const int seg = m / p.seg_rows;
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         const int nb = n0 + c * 32;
         if (nb >= p.N) break;
         uint32_t r[32];
@@ -260,16 +264,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ci = c * 32 + j;
           const int accv = (int)r[j] - t_zw[ci] * tr - za * t_cs[ci];
           float y;
-          if (p.mode == QCB_EPI_ACC) {
+          if (MODE == QCB_EPI_ACC) {
             y = __int_as_float(accv);
           } else {
             const double joint = __dmul_rn(sa, t_sw[ci]);
             y = __double2float_rn(__dmul_rn(joint, (double)accv));
-            if (p.mode == QCB_EPI_GELU) {
-              y = __double2float_rn(gelu_ref((double)y));
-            } else if (p.mode == QCB_EPI_GATE_RESID) {
+            if (MODE == QCB_EPI_GELU) {
+              y = gelu_f32_ref(y);
+            } else if (MODE == QCB_EPI_GATE_RESID) {
               y = __fadd_rn(rv[j], __fmul_rn(gate, y));
-            } else if (p.mode == QCB_EPI_RESID) {
+            } else if (MODE == QCB_EPI_RESID) {
               y = __fadd_rn(rv[j], y);
             }
           }
@@ -371,7 +375,7 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int BN>
+template <int BN, int MODE>
 static int launch_bn(const QcbGemm* g, cudaStream_t st) {
   using Cfg = GemmCfg<BN>;
   CUtensorMap ma, mb;
@@ -401,7 +405,6 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st) {
   p.resid_row0 = g->resid_row0;
   p.gate = g->gate;
   p.gate_scalar = g->gate_scalar;
-  p.mode = g->epilogue;
   p.seg_active = g->seg_active;
   // TMA-store epilogue when every 32-row slab is contiguous in the output.
   const int nseg = (g->M + p.seg_rows - 1) / p.seg_rows;
@@ -415,20 +418,21 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st) {
   static_assert(Cfg::kSmemBytes <= 227 * 1024, "GEMM smem budget exceeds 227 KB");
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_u8_tcgen05<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_u8_tcgen05<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmemBytes) != cudaSuccess)
       return QCB_ERR_CUDA;
     attr_set = true;
   }
   int tiles = p.num_m_tiles * p.num_n_tiles;
   int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_u8_tcgen05<BN><<<grid, kThreads, Cfg::kSmemBytes, st>>>(ma, mb, mo, p);
+  gemm_u8_tcgen05<BN, MODE><<<grid, kThreads, Cfg::kSmemBytes, st>>>(ma, mb, mo, p);
   return launch_status();
 }
 
 int pick_block_n(int N) {
   // Largest legal UMMA N (multiple of 16, <= 256) minimising padded columns.
-  static const int cands[] = {256, 192, 128, 64, 32};
+  // preference order on equal waste: deeper pipelines first (smem budget)
+  static const int cands[] = {192, 128, 256, 64, 32};
   int best = 32;
   long best_waste = 1L << 40;
   for (int bn : cands) {
@@ -442,14 +446,26 @@ int pick_block_n(int N) {
   return best;
 }
 
+template <int BN>
+static int launch_mode(const QcbGemm* g, cudaStream_t st) {
+  switch (g->epilogue) {
+    case QCB_EPI_STORE: return launch_bn<BN, QCB_EPI_STORE>(g, st);
+    case QCB_EPI_GELU: return launch_bn<BN, QCB_EPI_GELU>(g, st);
+    case QCB_EPI_GATE_RESID: return launch_bn<BN, QCB_EPI_GATE_RESID>(g, st);
+    case QCB_EPI_RESID: return launch_bn<BN, QCB_EPI_RESID>(g, st);
+    case QCB_EPI_ACC: return launch_bn<BN, QCB_EPI_ACC>(g, st);
+    default: return QCB_ERR_CONFIG;
+  }
+}
+
 int gemm_u8_launch(const QcbGemm* g, cudaStream_t st) {
   int bn = g->block_n > 0 ? g->block_n : pick_block_n(g->N);
   switch (bn) {
-    case 256: return launch_bn<256>(g, st);
-    case 192: return launch_bn<192>(g, st);
-    case 128: return launch_bn<128>(g, st);
-    case 64: return launch_bn<64>(g, st);
-    case 32: return launch_bn<32>(g, st);
+    case 256: return launch_mode<256>(g, st);
+    case 192: return launch_mode<192>(g, st);
+    case 128: return launch_mode<128>(g, st);
+    case 64: return launch_mode<64>(g, st);
+    case 32: return launch_mode<32>(g, st);
     default: return QCB_ERR_CONFIG;
   }
 }

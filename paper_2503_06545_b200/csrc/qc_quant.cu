@@ -107,6 +107,11 @@ QC_DEV void prologue_row(const ActQuantParams& p, const float* xrow, float* hrow
     __syncthreads();
     return;
   }
+  if (p.prologue == QCB_PRO_GELU) {
+    for (int j = threadIdx.x; j < K; j += blockDim.x) hrow[j] = gelu_f32_ref(xrow[j]);
+    __syncthreads();
+    return;
+  }
   double s = 0.0;
   for (int j = threadIdx.x; j < K; j += blockDim.x) s += (double)xrow[j];
   const double mean = block_reduce(s, red, [](double a, double b) { return a + b; }) / K;
@@ -219,6 +224,402 @@ __global__ void init_keys(uint32_t* keys, int n) {
   if (i < n) keys[i] = (i & 1) ? 0u : 0xFFFFFFFFu;
 }
 
+// ------------------------------------------------------------------ v2 path
+// Register FWHT for rotation blocks b = 1024 * WPR (STDiT: K = 1152 -> b = 1024,
+// K = 4608 -> b = 4096).  One warp owns 1024 elements of a row:
+//   load layout  e = lane + 32 r      (coalesced; r = register 0..31)
+//   stages on e bits 5..9 in registers, padded-smem transpose to
+//   e = 32 lane + r', stages on bits 0..4 in registers, then WPR-1 cross-warp
+//   stages through shared memory for bits 10, 11.
+// Pass 1 (LN / GELU prologue, balance, rotation, min/max) stashes xe as f32 so
+// pass 2 (codes) does no FP64 transform work.  Divisions take an exact
+// reciprocal fast path and fall back to IEEE division within a few ulps of a
+// rounding boundary, so results equal the reference's f64 division.
+
+constexpr int kV2Threads = 128;
+
+// true when the f64 value q is close enough to an f32 rounding boundary that a
+// multiply-by-reciprocal estimate may round differently from exact division.
+// True when rounding the f64 value q to f32 could differ from rounding a value
+// a few f64 ulps away: the 29 dropped fraction bits are within 64 units of the
+// round-to-nearest midpoint pattern, or q is outside the f32 normal range.
+QC_DEV bool f64_near_f32_tie(double q) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(q);
+  const int ex = (int)((u >> 52) & 0x7FF) - 1023;
+  if (ex < -125 || ex > 126) return true;
+  const int d = (int)((unsigned)u & 0x1FFFFFFFu) - (1 << 28);
+  return d > -64 && d < 64;
+}
+
+// f32(f64(h) / c) (quant.py:164): h * (1/c) is within 2 ulp64 of the exact
+// division, so its f32 rounding agrees unless it sits near a tie.
+QC_DEV float div_to_f32(float h, double c, double rc) {
+  const double q = __dmul_rn((double)h, rc);
+  if (f64_near_f32_tie(q)) return __double2float_rn(__ddiv_rn((double)h, c));
+  return __double2float_rn(q);
+}
+
+// clip(rha(f64(xe)/s) + z, 0, top) (quant.py:113-123).  f32 estimate: |q| <
+// 512, so the estimate of |q| + 0.5 is within 2^-14 of the exact value; when
+// it is further than 2^-12 from an integer the floor is certain, otherwise the
+// reference's f64 sequence is evaluated exactly.
+QC_DEV int code_of(float xe, float inv_sf, double s, float z, float top) {
+  const float qf = __fmul_rn(xe, inv_sf);
+  const float t = __fadd_rn(fabsf(qf), 0.5f);
+  float n = floorf(t);
+  const float fr = t - n;
+  float sgn = qf;
+  if (fr < 0x1p-12f || fr > 1.0f - 0x1p-12f) {
+    const double q = __ddiv_rn((double)xe, s);
+    n = (float)floor(__dadd_rn(fabs(q), 0.5));
+    sgn = (float)q;
+  }
+  float v = __fadd_rn(sgn < 0.0f ? -n : n, z);
+  v = fminf(fmaxf(v, 0.0f), top);
+  return (int)v;
+}
+
+struct AQ2 {
+  const double* rc[3];  // 1 / chan_scale
+  float* stash[3];      // xe [nseg*seg_rows][K]
+  long long ld_stash;
+  int total_rows;       // nseg * seg_valid
+};
+
+template <int WPR>
+struct V2Smem {
+  double xbuf[4][32 * 33];  // per-warp transpose / exchange buffer
+  float hbuf[4][1024 + 8 * 32];  // per-warp prologue output (block part + tail)
+  double red[4][2];         // cross-warp LN partial sums
+};
+
+QC_DEV void v2_row_index(const ActQuantParams& p, int gr, int& seg, int& mrow,
+                         long long& in_row, long long& out_row) {
+  seg = gr / p.seg_valid;
+  mrow = gr - seg * p.seg_valid;
+  in_row = (p.x_row0 ? p.x_row0[seg] : (long long)seg * p.seg_rows) + mrow;
+  out_row = (long long)seg * p.seg_rows + mrow;
+}
+
+template <int WPR>
+QC_DEV double v2_row_sum(double v, double* red_slot, int rowslot, int part) {
+  v = warp_sum(v);
+  if (WPR == 1) return v;
+  if ((threadIdx.x & 31) == 0) red_slot[part] = v;
+  named_bar_sync(1 + rowslot, 32 * WPR);
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < WPR; ++i) t += red_slot[i];
+  named_bar_sync(1 + rowslot, 32 * WPR);
+  return t;
+}
+
+// f32(f32(((x - mean) / sd) * g + b) * scale1 + shift), the LN prologue of
+// model.py:137-142 + modulation, via x * (1/sd) with an exact fallback.
+QC_DEV float ln_elem(float x, double mean, double sd, double rsd, double g, double b,
+                     float scale1, float shift) {
+  const double xm = (double)x - mean;
+  const double u = __dmul_rn(__dmul_rn(xm, rsd), g);
+  const double v = __dadd_rn(u, b);
+  double vv;
+  if (fabs(u) <= 4.0 * fabs(v) && !f64_near_f32_tie(v)) {
+    vv = v;
+  } else {
+    vv = __dadd_rn(__dmul_rn(__ddiv_rn(xm, sd), g), b);
+  }
+  return __fadd_rn(__fmul_rn(__double2float_rn(vv), scale1), shift);
+}
+
+template <int WPR, bool kPow2Scale>
+__global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, const AQ2 a) {
+  constexpr int RPC = 4 / WPR;     // rows per CTA iteration
+  constexpr int TPL = 8;           // max tail elements per lane
+  extern __shared__ __align__(16) uint8_t v2_smem[];
+  V2Smem<WPR>& sm = *reinterpret_cast<V2Smem<WPR>*>(v2_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rowslot = warp / WPR, part = warp % WPR;
+  const int K = p.K, b = p.b;
+  const int T = K - b;
+  double* xb = sm.xbuf[warp];
+  float* hb = sm.hbuf[warp];
+  float mn[3], mx[3];
+  int cur_seg = -1;
+#pragma unroll
+  for (int o = 0; o < 3; ++o) { mn[o] = INFINITY; mx[o] = -INFINITY; }
+
+  auto flush = [&](int seg) {
+    for (int o = 0; o < p.n_out; ++o) {
+      float lo = mn[o], hi = mx[o];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+      }
+      if (lane == 0 && hi >= lo) {
+        uint32_t* k = p.keys + ((size_t)o * p.nseg + seg) * 2;
+        atomicMin(&k[0], f2key(lo));
+        atomicMax(&k[1], f2key(hi));
+      }
+      mn[o] = INFINITY;
+      mx[o] = -INFINITY;
+    }
+  };
+
+  for (int base = blockIdx.x * RPC; base < a.total_rows; base += gridDim.x * RPC) {
+    const int gr = base + rowslot;
+    const bool active = gr < a.total_rows;   // uniform across the row's warps
+    int seg = 0, mrow = 0;
+    long long in_row = 0, out_row = 0;
+    if (active) v2_row_index(p, gr, seg, mrow, in_row, out_row);
+    if (active && seg != cur_seg) {
+      if (cur_seg >= 0) flush(cur_seg);
+      cur_seg = seg;
+    }
+    // ---- load this warp's share of the row: e = lane + 32 r, tail t = (i*WPR+part)*32+lane
+    {
+      const float* xr = p.x + in_row * p.ldx;
+      float xv[32], xt[TPL];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) xv[r] = active ? __ldg(xr + part * 1024 + lane + 32 * r) : 0.f;
+#pragma unroll
+      for (int i = 0; i < TPL; ++i) {
+        const int t = (i * WPR + part) * 32 + lane;
+        xt[i] = (active && t < T) ? __ldg(xr + b + t) : 0.f;
+      }
+      // ---- prologue (model.py:182,189,196 LN+mod; model.py:197 GELU) -> smem
+      if (p.prologue == QCB_PRO_LN_MOD) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) s += (double)xv[r];
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) s += (double)xt[i];
+        const double mean = v2_row_sum<WPR>(s, sm.red[rowslot], rowslot, part) / K;
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) { const double d = (double)xv[r] - mean; v += d * d; }
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) {
+          const int t = (i * WPR + part) * 32 + lane;
+          if (t < T) { const double d = (double)xt[i] - mean; v += d * d; }
+        }
+        const double var = v2_row_sum<WPR>(v, sm.red[rowslot], rowslot, part) / K;
+        const double sd = sqrt(var + 1e-5);
+        const double rsd = 1.0 / sd;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const int col = part * 1024 + lane + 32 * r;
+          const double g = p.ln_g ? (double)__ldg(p.ln_g + col) : 1.0;
+          const double bb = p.ln_b ? (double)__ldg(p.ln_b + col) : 0.0;
+          hb[lane + 32 * r] = ln_elem(xv[r], mean, sd, rsd, g, bb, p.scale1, p.shift);
+        }
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) {
+          const int t = (i * WPR + part) * 32 + lane;
+          if (t < T) {
+            const double g = p.ln_g ? (double)__ldg(p.ln_g + b + t) : 1.0;
+            const double bb = p.ln_b ? (double)__ldg(p.ln_b + b + t) : 0.0;
+            hb[1024 + 32 * i + lane] = ln_elem(xt[i], mean, sd, rsd, g, bb, p.scale1, p.shift);
+          }
+        }
+      } else if (p.prologue == QCB_PRO_GELU) {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) hb[lane + 32 * r] = gelu_f32_ref(xv[r]);
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) hb[1024 + 32 * i + lane] = gelu_f32_ref(xt[i]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) hb[lane + 32 * r] = xv[r];
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) hb[1024 + 32 * i + lane] = xt[i];
+      }
+    }
+    __syncwarp();
+    // ---- per output: balance, rotation, min/max, stash
+    for (int o = 0; o < p.n_out; ++o) {
+      const double* c = p.c[o];
+      const double* rc = a.rc[o];
+      const uint32_t* sgb = reinterpret_cast<const uint32_t*>(p.signs[o]);
+      double w[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int col = part * 1024 + lane + 32 * r;
+        const float h = hb[lane + 32 * r];
+        float y = c ? div_to_f32(h, __ldg(c + col), __ldg(rc + col)) : h;
+        if (c) y = __uint_as_float(__float_as_uint(y) ^ (__ldg(sgb + col) & 0x80000000u));
+        w[r] = (double)y;
+      }
+      float xe[32];
+      if (c) {
+        // stages on e bits 5..9 (register index bits 0..4)
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            if ((r & h) == 0) {
+              const double u = w[r], v = w[r + h];
+              w[r] = u + v;
+              w[r + h] = u - v;
+            }
+        // transpose e = lane + 32 r  ->  e = 32 lane + r
+#pragma unroll
+        for (int r = 0; r < 32; ++r) xb[lane + 33 * r] = w[r];
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 32; ++r) w[r] = xb[33 * lane + r];
+        __syncwarp();
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            if ((r & h) == 0) {
+              const double u = w[r], v = w[r + h];
+              w[r] = u + v;
+              w[r + h] = u - v;
+            }
+        // cross-warp stages (bits 10, 11)
+#pragma unroll
+        for (int hbit = 1; hbit < WPR; hbit <<= 1) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) xb[33 * lane + r] = w[r];
+          named_bar_sync(1 + rowslot, 32 * WPR);
+          const double* pb = sm.xbuf[rowslot * WPR + (part ^ hbit)];
+          const bool lower = (part & hbit) == 0;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            const double v = pb[33 * lane + r];
+            w[r] = lower ? w[r] + v : v - w[r];
+          }
+          named_bar_sync(1 + rowslot, 32 * WPR);
+        }
+        if (kPow2Scale) {   // r = 2^-k exactly: f32(w * r) = f32(w) * r
+#pragma unroll
+          for (int r = 0; r < 32; ++r) xe[r] = __fmul_rn(__double2float_rn(w[r]), p.rscale);
+        } else {
+          const double rsc = (double)p.rscale;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) xe[r] = __double2float_rn(__dmul_rn(w[r], rsc));
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) xe[r] = (float)w[r];
+      }
+      float tl[TPL];
+#pragma unroll
+      for (int i = 0; i < TPL; ++i) {
+        const int t = (i * WPR + part) * 32 + lane;
+        const float h = hb[1024 + 32 * i + lane];
+        tl[i] = (c && t < T) ? div_to_f32(h, __ldg(c + b + t), __ldg(rc + b + t)) : h;
+      }
+      if (active) {
+        float lo = mn[o], hi = mx[o];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) { lo = fminf(lo, xe[r]); hi = fmaxf(hi, xe[r]); }
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) {
+          const int t = (i * WPR + part) * 32 + lane;
+          if (t < T) { lo = fminf(lo, tl[i]); hi = fmaxf(hi, tl[i]); }
+        }
+        mn[o] = lo;
+        mx[o] = hi;
+        float* so = a.stash[o] + out_row * a.ld_stash;
+        if (c) {   // rotated layout: this lane owns e = 32 lane + r (contiguous)
+          float4* dst = reinterpret_cast<float4*>(so + part * 1024 + 32 * lane);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(xe[4 * j], xe[4 * j + 1], xe[4 * j + 2], xe[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) so[part * 1024 + lane + 32 * r] = xe[r];
+        }
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) {
+          const int t = (i * WPR + part) * 32 + lane;
+          if (t < T) so[b + t] = tl[i];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (cur_seg >= 0) flush(cur_seg);
+}
+
+// Pass 2: codes (+ optional dequantized copy) from the f32 stash; warp per row.
+__global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, const AQ2 a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.K;
+  const double top = (double)((1 << p.bits) - 1);
+  for (int gr = blockIdx.x * 4 + warp; gr < a.total_rows; gr += gridDim.x * 4) {
+    int seg, mrow;
+    long long in_row, out_row;
+    v2_row_index(p, gr, seg, mrow, in_row, out_row);
+    for (int o = 0; o < p.n_out; ++o) {
+      const uint32_t* k = p.keys + ((size_t)o * p.nseg + seg) * 2;
+      const double lo = (double)key2f(k[0]), hi = (double)key2f(k[1]);
+      const double span = hi - lo;
+      double s, z;
+      if (span <= 0.0) {
+        s = 1.0;
+        z = 0.0;
+      } else {
+        s = scale_up16(__ddiv_rn(span, top));
+        z = fmin(fmax(rha(__ddiv_rn(-lo, s)), 0.0), top);
+      }
+      if (mrow == 0 && lane == 0) {
+        p.scale[o][seg] = s;
+        p.zero[o][seg] = (int)z;
+      }
+      const float inv_sf = (float)(1.0 / s);
+      const float zf = (float)z, topf = (float)top;
+      const float* xr = a.stash[o] + out_row * a.ld_stash;
+      uint8_t* cr = p.codes[o] ? p.codes[o] + out_row * p.ldc : nullptr;
+      float* dr = p.deq_out[o] ? p.deq_out[o] + out_row * p.ldxe : nullptr;
+      int rs = 0;
+      for (int j = lane * 4; j < K; j += 128) {
+        float v4[4];
+        if (j + 3 < K) {
+          const float4 t4 = *reinterpret_cast<const float4*>(xr + j);
+          v4[0] = t4.x; v4[1] = t4.y; v4[2] = t4.z; v4[3] = t4.w;
+        } else {
+          for (int e = 0; e < 4; ++e) v4[e] = (j + e < K) ? xr[j + e] : 0.f;
+        }
+        uint32_t packed = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (j + e < K) {
+            const int code = code_of(v4[e], inv_sf, s, zf, topf);
+            rs += code;
+            packed |= (uint32_t)code << (8 * e);
+            if (dr) dr[j + e] = __double2float_rn(__dmul_rn(s, (double)(code - (int)z)));
+          }
+        }
+        if (cr) {
+          if (j + 3 < K) *reinterpret_cast<uint32_t*>(cr + j) = packed;
+          else
+            for (int e = 0; e < 4 && j + e < K; ++e) cr[j + e] = (uint8_t)(packed >> (8 * e));
+        }
+      }
+      rs = warp_sum(rs);
+      if (lane == 0 && cr) p.rowsum[o][out_row] = rs;
+    }
+  }
+}
+
+__global__ void recip_k(const double* c, double* rc, int K) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < K) rc[i] = 1.0 / c[i];
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace qc
+
+extern "C" size_t qcb_act_quant_workspace_bytes(int K, int seg_rows, int nseg, int n_out) {
+  return qc::align256((size_t)8 * 3 * nseg) + qc::align256((size_t)8 * 3 * K) +
+         (size_t)3 * qc::align256((size_t)4 * K * seg_rows * nseg) + 256;
+}
+
+namespace qc {
+
 int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
   ActQuantParams p{};
   p.x = q->x;
@@ -255,6 +656,57 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
   p.keys = reinterpret_cast<uint32_t*>(q->workspace);
   const int nkeys = 2 * q->n_out * q->nseg;
   init_keys<<<(nkeys + 255) / 256, 256, 0, st>>>(p.keys, nkeys);
+  // v2: register FWHT for b in {1024, 2048, 4096} with a short tail
+  const int wpr = b / 1024;
+  const bool v2 = (b == 1024 || b == 2048 || b == 4096) && (q->K - b) <= 8 * 32 * wpr &&
+                  (q->K % 4 == 0) && (q->ldx % 4 == 0) && (q->ldc % 4 == 0 || !q->codes[0]);
+  if (v2) {
+    uint8_t* ws = reinterpret_cast<uint8_t*>(q->workspace);
+    size_t off = align256((size_t)8 * 3 * q->nseg);
+    AQ2 a{};
+    a.total_rows = p.seg_valid * p.nseg;
+    double* rcbuf = reinterpret_cast<double*>(ws + off);
+    off += align256((size_t)8 * 3 * q->K);
+    const size_t stash_bytes = align256((size_t)4 * q->K * q->seg_rows * q->nseg);
+    a.ld_stash = q->K;
+    for (int o = 0; o < q->n_out; ++o) {
+      a.rc[o] = rcbuf + (size_t)o * q->K;
+      if (q->chan_scale[o])
+        recip_k<<<(q->K + 255) / 256, 256, 0, st>>>(q->chan_scale[o], rcbuf + (size_t)o * q->K, q->K);
+      if (q->xe_out[o] && q->ldxe == q->K) {
+        a.stash[o] = q->xe_out[o];
+      } else {
+        a.stash[o] = reinterpret_cast<float*>(ws + off);
+        off += stash_bytes;
+      }
+    }
+    const int rpc = 4 / wpr;
+    int blocks = (a.total_rows + rpc - 1) / rpc;
+    const int cap = num_sms() * 4;
+    if (blocks > cap) blocks = cap;
+    // 1/sqrt(b) is a power of two for b = 1024, 4096
+    const size_t sm1 = sizeof(V2Smem<1>);
+    static bool at1 = false, at2 = false, at4 = false;
+    switch (wpr) {
+      case 1:
+        allow_max_smem(aq2_pass1<1, true>, at1);
+        aq2_pass1<1, true><<<blocks, kV2Threads, sm1, st>>>(p, a);
+        break;
+      case 2:
+        allow_max_smem(aq2_pass1<2, false>, at2);
+        aq2_pass1<2, false><<<blocks, kV2Threads, sm1, st>>>(p, a);
+        break;
+      default:
+        allow_max_smem(aq2_pass1<4, true>, at4);
+        aq2_pass1<4, true><<<blocks, kV2Threads, sm1, st>>>(p, a);
+        break;
+    }
+    int b2 = (a.total_rows + 3) / 4;
+    if (b2 > cap) b2 = cap;
+    aq2_pass2<<<b2, kV2Threads, 0, st>>>(p, a);
+    if (q->xe_out[0] && q->ldxe != q->K) return QCB_ERR_DIM;  // debug copy layout unsupported
+    return launch_status();
+  }
   const size_t smem = (size_t)q->K * (sizeof(double) + sizeof(float));
   if (smem > 200 * 1024) return QCB_ERR_DIM;
   static bool attr1 = false, attr2 = false;

@@ -62,10 +62,26 @@ __global__ void __launch_bounds__(kRThreads)
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
   const bool vec = (cols % 4 == 0) && (f0.ld % 4 == 0) && (f1.ld % 4 == 0) &&
                    (KIND != 0 || f2.ld % 4 == 0);
+  // SRAP on a pruned chain compares a slot with itself: read it once.
+  const bool alias = (KIND == 1) && (f0.base == f1.base) && (f0.ld == f1.ld) &&
+                     (f0.row0 ? (f1.row0 && f0.row0[seg] == f1.row0[seg]) : !f1.row0);
   for (int r = r0; r < r1; ++r) {
     const float* a = feat_row(f0, seg, rows, r);
     const float* b = feat_row(f1, seg, rows, r);
     const float* c = KIND == 0 ? feat_row(f2, seg, rows, r) : nullptr;
+    if (alias) {
+      if (vec) {
+        for (int j = threadIdx.x; j < cols / 4; j += kRThreads) {
+          const float4 x = reinterpret_cast<const float4*>(a)[j];
+          const double s2 = (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z +
+                            (double)x.w * x.w;
+          acc[0] += s2;
+        }
+      } else {
+        for (int j = threadIdx.x; j < cols; j += kRThreads) acc[0] += (double)a[j] * a[j];
+      }
+      continue;
+    }
     if (vec) {
       for (int j = threadIdx.x; j < cols / 4; j += kRThreads) {
         const float4 x = reinterpret_cast<const float4*>(a)[j];
@@ -108,6 +124,10 @@ __global__ void __launch_bounds__(kRThreads)
         }
       }
     }
+  }
+  if (alias) {
+#pragma unroll
+    for (int i = 1; i < NV; ++i) acc[i] = acc[0];
   }
   block_sum_vec<NV>(acc, scratch);
   if (threadIdx.x == 0) {
@@ -291,11 +311,8 @@ __global__ void plan_finish_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThr
   s.seen += 1;
 }
 
-__global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
-                          const double* hlc) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nvid) return;
-  QcbPolicyVideo& s = st[v];
+QC_DEV void observe_one(QcbPolicyVideo& s, int l, int t, const QcbThresholds& th,
+                        const double* hlc2) {
   if (s.action[l] == QCB_ACT_RECOMPUTE) {
     int k = 1;
     int ref = 0;
@@ -308,8 +325,8 @@ __global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresho
     }
     int tau;
     if (ref != 0 && s.prev_valid[l]) {
-      const double l1 = hlc[(size_t)v * 2 + 0];
-      const double l2 = sqrt(hlc[(size_t)v * 2 + 1]);
+      const double l1 = hlc2[0];
+      const double l2 = sqrt(hlc2[1]);
       const double d = (l1 / (double)k) * l2;
       if (!s.has_d[l]) {
         s.has_d[l] = 1;
@@ -330,6 +347,22 @@ __global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresho
     }
   }
   s.prev_valid[l] = 1;
+}
+
+__global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
+                          const double* hlc) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvid) return;
+  observe_one(st[v], l, t, th, hlc + (size_t)v * 2);
+}
+
+// All layers of a step in order (nothing inside a step reads what observe_block
+// writes, so the per-layer updates can be applied together at the step's end).
+__global__ void observe_all_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
+                              const double* hlc /*[L][nvid][2]*/) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvid) return;
+  for (int l = 0; l < L; ++l) observe_one(st[v], l, t, th, hlc + ((size_t)l * nvid + v) * 2);
 }
 
 }  // namespace qc
@@ -357,6 +390,13 @@ extern "C" int qcb_policy_plan_finish(QcbPolicyVideo* st, int nvid, int L, int t
   if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0 || n_hist < 0) return QCB_ERR_DIM;
   plan_finish_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(
       st, nvid, L, t, th, srap, hist_l1, n_hist, draws, dstride);
+  return launch_ok();
+}
+
+extern "C" int qcb_policy_observe_all(QcbPolicyVideo* st, int nvid, int L, int t,
+                                     QcbThresholds th, const double* hlc, void* stream) {
+  if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
+  observe_all_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, t, th, hlc);
   return launch_ok();
 }
 

@@ -115,7 +115,8 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
               nseg: int = 1, x_row0: Optional[torch.Tensor] = None,
               ln: Optional[tuple] = None, mod: tuple = (1.0, 0.0), want_codes: bool = True,
               want_xe: bool = False, want_deq: bool = False,
-              out: Optional[List[ActCodes]] = None, stream=None) -> List[ActCodes]:
+              out: Optional[List[ActCodes]] = None, gelu: bool = False,
+              stream=None) -> List[ActCodes]:
     """Fused [LN+mod] -> balance/rotate -> per-segment min/max -> codes.
 
     transforms[o] = (chan_scale f64 [K], signs f32 [b]) or None (no transform).
@@ -149,6 +150,8 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
     if ln is not None:
         q.prologue = N.PRO_LN_MOD
         q.ln_g, q.ln_b = N.ptr(ln[0]), N.ptr(ln[1])
+    elif gelu:
+        q.prologue = N.PRO_GELU   # f32(gelu_f64(x)) applied to the input rows
     else:
         q.prologue = N.PRO_NONE
     q.mod_scale1, q.mod_shift = float(mod[0]), float(mod[1])
@@ -169,7 +172,8 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
             if buf is not None:
                 ldxe = buf.stride(0)
     q.ldc, q.ldxe = ldc, ldxe
-    q.workspace = N.ptr(_WS.get(8 * 3 * nseg + 64))
+    q.workspace = N.ptr(_WS.get(int(N.lib().qcb_act_quant_workspace_bytes(K, seg_rows, nseg,
+                                                                         n_out))))
     N.check(N.lib().qcb_act_quant(C.byref(q), N.stream_ptr(stream)), "act_quant")
     count(3)
     return res

@@ -216,7 +216,7 @@ class QuantCacheEngine:
         self.srap = torch.zeros((L, nv, 3), dtype=torch.float64, device=dev)
         self.mask = torch.zeros((L, nv), dtype=torch.int32, device=dev)
         self.hist_l1 = torch.zeros((self.th.history_k + 1, nv), dtype=torch.float64, device=dev)
-        self.hlc = torch.zeros((nv, 2), dtype=torch.float64, device=dev)
+        self.hlc = torch.zeros((L, nv, 2), dtype=torch.float64, device=dev)
         n_idx = 2 * max(1 << 15, 16 * L * (nv + 4) + 64)
         self.idx_host = torch.zeros(n_idx, dtype=torch.int64).pin_memory()
         self.idx_dev = torch.zeros(n_idx, dtype=torch.int64, device=dev)
@@ -259,7 +259,8 @@ class QuantCacheEngine:
     # ------------------------------------------------------------------ sites
     def _site(self, l, site, bits, x, nseg, *, x_row0=None, seg_rows=None, seg_valid=None,
               ln=None, mod=(1.0, 0.0), epi=N.EPI_STORE, out=None, out_row0=None,
-              resid=None, resid_row0=None, gate=1.0, outs=None, sites=None):
+              resid=None, resid_row0=None, gate=1.0, outs=None, sites=None,
+              gelu_in=False):
         """One GEMM site (or a fused group sharing the same input) through the
         mode the reference's QuantRuntime.gemm_fn would pick (runtime.py:69-79)."""
         tog = self.tog
@@ -277,7 +278,7 @@ class QuantCacheEngine:
                 acs.append(Dv.ActCodes(self.codes[o][:M, :Dv.round16(p.K)],
                                        a.rowsum[:M], a.scale[:nseg], a.zero[:nseg], p.K))
             Dv.act_quant(x, bits, trs, seg_rows=seg_rows, seg_valid=seg_valid, nseg=nseg,
-                         x_row0=x_row0, ln=ln, mod=mod, out=acs)
+                         x_row0=x_row0, ln=ln, mod=mod, out=acs, gelu=gelu_in)
             targets = outs or [out]
             prof = self.gemm_profile
             for o, p in enumerate(pws):
@@ -368,11 +369,14 @@ class QuantCacheEngine:
         self._attention(self.q2, self.k2, self.v2, self.att, n, 1, 1)
         self._site(l, "ca_o", bits, self.att, n, epi=N.EPI_RESID, out=A, out_row0=out_row0,
                    resid=A, resid_row0=out_row0)
-        # FFN
+        # FFN.  On the integer path GELU (model.py:197) moves from the ffn1
+        # epilogue into the ffn2 quantizer's prologue: same f32(gelu_f64(y)) per
+        # element, computed once, on the quantizer's wider grid.
+        int_path = self.tog.aigq_weights and self.tog.aigq_acts and bits < FP_BITS
         self._site(l, "ffn1", bits, A, n, x_row0=out_row0, ln=(ln3g, ln3b), mod=(sc3, sh3),
-                   epi=N.EPI_GELU, out=self.hid)
+                   epi=N.EPI_STORE if int_path else N.EPI_GELU, out=self.hid)
         self._site(l, "ffn2", bits, self.hid, n, epi=N.EPI_GATE_RESID, out=A,
-                   out_row0=out_row0, resid=A, resid_row0=out_row0, gate=g3)
+                   out_row0=out_row0, resid=A, resid_row0=out_row0, gate=g3, gelu_in=int_path)
 
     # ------------------------------------------------------------------ run
     def generate(self, seeds: Sequence[int], device_noise_seed: Optional[int] = None,
@@ -420,86 +424,85 @@ class QuantCacheEngine:
             self._begin_step(t)
             # ---------------- plan (device) ----------------
             nh = len(vids[0].hist)
-            srap_layers = []
             pre = []
             for j in range(nh):
                 pre.append([self.rows(vs.x) for vs in vids])
                 pre.append([self.rows(vs.hist[j]) for vs in vids])
             boundary = vids[0].seen == 0 or t == 0
-            if self.tog.srap and not boundary:
-                for l in range(1, L):
-                    if any(vs.prev[l - 1] is not None and vs.prev[l] is not None for vs in vids):
-                        srap_layers.append(l)
-                        pre.append([self.rows(vs.prev[l - 1]) if vs.prev[l - 1] is not None
-                                    else 0 for vs in vids])
-                        pre.append([self.rows(vs.prev[l]) if vs.prev[l] is not None else 0
-                                    for vs in vids])
+            do_srap = self.tog.srap and not boundary
+            if do_srap:
+                # one launch for every (layer, video) pair: prev[l-1] vs prev[l]
+                pre.append([self.rows(vs.prev[l - 1]) if l > 0 and vs.prev[l - 1] is not None
+                            else 0 for l in range(L) for vs in vids])
+                pre.append([self.rows(vs.prev[l]) if vs.prev[l] is not None else 0
+                            for l in range(L) for vs in vids])
             tabs = self._upload_idx(pre)
             for j in range(nh):
                 Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]), Dv.feat(self.arena, tabs[2 * j + 1]),
                              S, d, nv, self.hist_l1[j])
             N.check(lib.qcb_policy_plan_reuse(pol, nv, L, t, self.thc, sp), "plan_reuse")
-
-            if srap_layers:
+            Dv.count(1)
+            if do_srap:
                 N.check(lib.qcb_policy_sim_mask(pol, nv, L, self.thc, N.ptr(self.mask), sp),
                         "sim_mask")
-
-                for i, l in enumerate(srap_layers):
-                    a, b = tabs[2 * nh + 2 * i], tabs[2 * nh + 2 * i + 1]
-                    Dv.reduce_srap(Dv.feat(self.arena, a), Dv.feat(self.arena, b), S, d, nv,
-                                   self.srap[l], seg_active=self.mask[l])
+                Dv.count(1)
+                Dv.reduce_srap(Dv.feat(self.arena, tabs[2 * nh]),
+                               Dv.feat(self.arena, tabs[2 * nh + 1]), S, d, L * nv,
+                               self.srap.view(L * nv, 3), seg_active=self.mask.view(L * nv))
             N.check(lib.qcb_policy_plan_finish(pol, nv, L, t, self.thc, N.ptr(self.srap),
                                                N.ptr(self.hist_l1), nh,
                                                N.ptr(self.draws[t]), 0, sp), "plan_finish")
-
+            Dv.count(1)
             self.pol_host.copy_(self.pol, non_blocking=True)
             st.synchronize()
+            raw = self.pol_host.numpy()
             plans = [N.QcbPolicyVideo.from_buffer_copy(
-                self.pol_host.numpy()[v * self.pol_size:(v + 1) * self.pol_size].tobytes())
-                for v in range(nv)]
+                raw[v * self.pol_size:(v + 1) * self.pol_size].tobytes()) for v in range(nv)]
             for vs in vids:
                 vs.seen += 1
             # ---------------- execute blocks ----------------
             cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
             feats = [] if collect_features is not None else None
             for l in range(L):
+                acts = [p.action[l] for p in plans]
                 outs = list(cur)
-                rec = [v for v in range(nv) if plans[v].action[l] == N.ACT_RECOMPUTE]
+                rec = []
                 for v in range(nv):
-                    a = plans[v].action[l]
+                    a = acts[v]
                     if a == N.ACT_REUSE:
                         outs[v] = vids[v].pool.inc(vids[v].cache[l])
                     elif a == N.ACT_PRUNE:
                         outs[v] = vids[v].pool.inc(cur[v])
                     else:
                         outs[v] = vids[v].pool.alloc()
-                # group recomputing videos by activation bits
-                groups: Dict[int, List[int]] = {}
-                for v in rec:
-                    groups.setdefault(plans[v].abits, []).append(v)
-                need_d = [v in rec and (vids[v].cache[l] is not None or vids[v].prev[l] is not None)
-                          and vids[v].prev[l] is not None for v in range(nv)]
-                tabl = []
-                for bits, g in groups.items():
-                    tabl += [[self.rows(cur[v]) for v in g], [self.rows(outs[v]) for v in g],
-                             g]
-                if any(need_d):
-                    tabl += [[self.rows(outs[v]) for v in range(nv)],
-                             [self.rows(vids[v].cache[l] if vids[v].cache[l] is not None
-                                        else (vids[v].prev[l] or 0)) for v in range(nv)],
-                             [self.rows(vids[v].prev[l] or 0) for v in range(nv)],
-                             [int(x) for x in need_d]]
-                tl = self._upload_idx(tabl)
-                for gi, (bits, g) in enumerate(groups.items()):
-                    self._block(l, t, g, bits, tl[3 * gi], tl[3 * gi + 1], tl[3 * gi + 2])
-                if any(need_d):
-                    base = 3 * len(groups)
-                    act = tl[base + 3].to(torch.int32)
-                    Dv.reduce_hlc(Dv.feat(self.arena, tl[base]), Dv.feat(self.arena, tl[base + 1]),
-                                  Dv.feat(self.arena, tl[base + 2]), S, d, nv, self.hlc,
-                                  seg_active=act)
-                N.check(lib.qcb_policy_observe(pol, nv, l, t, self.thc, N.ptr(self.hlc), sp),
-                        "observe")
+                        rec.append(v)
+                if rec:
+                    # group recomputing videos by activation bits
+                    groups: Dict[int, List[int]] = {}
+                    for v in rec:
+                        groups.setdefault(plans[v].abits, []).append(v)
+                    need_d = [acts[v] == N.ACT_RECOMPUTE and vids[v].prev[l] is not None
+                              for v in range(nv)]
+                    tabl = []
+                    for bits, g in groups.items():
+                        tabl += [[self.rows(cur[v]) for v in g], [self.rows(outs[v]) for v in g],
+                                 g]
+                    if any(need_d):
+                        tabl += [[self.rows(outs[v]) for v in range(nv)],
+                                 [self.rows(vids[v].cache[l] if vids[v].cache[l] is not None
+                                            else (vids[v].prev[l] or 0)) for v in range(nv)],
+                                 [self.rows(vids[v].prev[l] or 0) for v in range(nv)],
+                                 [int(x) for x in need_d]]
+                    tl = self._upload_idx(tabl)
+                    for gi, (bits, g) in enumerate(groups.items()):
+                        self._block(l, t, g, bits, tl[3 * gi], tl[3 * gi + 1], tl[3 * gi + 2])
+                    if any(need_d):
+                        base = 3 * len(groups)
+                        act = tl[base + 3].to(torch.int32)
+                        Dv.reduce_hlc(Dv.feat(self.arena, tl[base]),
+                                      Dv.feat(self.arena, tl[base + 1]),
+                                      Dv.feat(self.arena, tl[base + 2]), S, d, nv,
+                                      self.hlc[l], seg_active=act)
 
                 # host mirror of the cache / prev references (schedule.py:349-351)
                 for v, vs in enumerate(vids):
@@ -512,6 +515,10 @@ class QuantCacheEngine:
                 cur = outs
                 if feats is not None:
                     feats.append(torch.stack([self.slot_view(s) for s in cur]).cpu().numpy())
+            # observe_block for every layer of the step (schedule.py:330-351)
+            N.check(lib.qcb_policy_observe_all(pol, nv, L, t, self.thc, N.ptr(self.hlc), sp),
+                    "observe_all")
+            Dv.count(1)
             if collect_features is not None:
                 x_now = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
                 collect_features.append((t, x_now, feats))

@@ -197,6 +197,43 @@ class TestActQuant:
                 assert np.array_equal(codes, O.codes_of(xe_want, s, z, 6))
 
 
+    @pytest.mark.parametrize("K,bits", [(1152, 8), (4608, 6), (2304, 4), (1024, 8)])
+    def test_v2_gelu_prologue_rows_segments(self, D, K, bits):
+        """Register-FWHT path (b = 1024/2048/4096): GELU prologue, rows gathered
+        through a per-segment row table, per-segment params, vs the oracle."""
+        rng = np.random.default_rng(K + bits)
+        S, Spad, nseg = 40, 64, 3
+        src = (rng.standard_normal((5 * Spad, K)) * 1.7).astype(np.float32)
+        row0 = np.array([3 * Spad, 0, Spad], np.int64)      # segment -> first source row
+        c = rng.uniform(0.2, 3.0, K)
+        b = D.pow2_floor(K)
+        sg = D.sign_vector(11, b)
+        (r,) = D.act_quant(t(src), bits, [(t(c), t(sg))], seg_rows=Spad, seg_valid=S,
+                           nseg=nseg, x_row0=t(row0), gelu=True)
+        codes = r.codes.cpu().numpy()
+        for v in range(nseg):
+            xin = src[row0[v]:row0[v] + S]
+            h = O.gelu64(xin)
+            xe = O.rotate_act_fwht(h, c, 11)
+            s, z = O.act_params(xe, bits)
+            assert float(r.scale[v]) == s and int(r.zero[v]) == z, v
+            want = O.codes_of(xe, s, z, bits)
+            got = codes[v * Spad:v * Spad + S, :K]
+            assert np.array_equal(got, want), (v, int((got != want).sum()))
+            assert np.array_equal(r.rowsum.cpu().numpy()[v * Spad:v * Spad + S],
+                                  want.sum(1))
+
+    def test_v2_identity_transform_and_deq(self, D):
+        rng = np.random.default_rng(3)
+        x = rng.standard_normal((70, 1152)).astype(np.float32)
+        (r,) = D.act_quant(t(x), 8, [None], want_deq=True)
+        s, z = O.act_params(x, 8)
+        codes = O.codes_of(x, s, z, 8)
+        assert float(r.scale.item()) == s and int(r.zero.item()) == z
+        assert np.array_equal(r.codes.cpu().numpy()[:, :1152], codes)
+        assert np.array_equal(r.deq.cpu().numpy(), O.dequant(codes, s, z))
+
+
 class TestWeightPrep:
     def test_rotation_and_channel_quant(self, D, golden_dir):
         f = np.load(os.path.join(golden_dir, "rotation.npz"))
