@@ -241,6 +241,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2503_06545_b200 import device as Dv
+    from paper_2503_06545_b200 import dist as qdist
     from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
     from paper_2503_06545_b200.model import DiTConfig
     from paper_2503_06545_b200.sampler import linear_beta_schedule
@@ -286,7 +287,9 @@ def run_ours(args):
     gen.manual_seed(7 + rank)
     x0 = torch.randn((B, S, d), device="cuda", generator=gen)
     cond = torch.randn((B, cfg.cond_dim), device="cuda", generator=gen)
-    seeds = lambda k: [10_000 * rank + 100 * k + v for v in range(B)]
+    # video sharding: global video ids of this rank for bench step k (weak scaling:
+    # B videos per GPU per step), seeds follow the video id
+    seeds = lambda k: qdist.video_seeds(qdist.shard_videos(B * world, world, rank), 1_000 * k)
     for k in range(args.warmup):
         eng.generate(seeds(k), device_noise_seed=k, x0_dev=x0, cond_dev=cond,
                      return_device=True)
@@ -315,9 +318,7 @@ def run_ours(args):
     eng.gemm_profile = None
     if world > 1:
         dist.barrier()
-        t = torch.tensor([elapsed], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+    elapsed = qdist.max_over_ranks(elapsed, device="cuda")
     # recompute fraction / decisions of the timed runs
     traces = [eng.traces_of(v) for v in vids_all]
     recs = [r for trs in traces for tv in trs for r in tv if r.layer != "head"]

@@ -21,6 +21,7 @@
  *   qcb_attention_f64  model.py:150-156, tensor.py:115-132  _mha / attention
  *   qcb_ln_mod         model.py:137-142 (+182,196)  _ln and modulation
  *   qcb_ddpm_step      sampler.py:59-88   reverse_step / final_step
+ *   qcb_gelu_inplace   model.py:145-147   _gelu
  *   qcb_reduce_hlc     schedule.py:67-82  divergence_score partial sums
  *   qcb_reduce_srap    schedule.py:108-116 layer_similarity partial sums
  *   qcb_reduce_var     schedule.py:128-133 cumulative_variation
@@ -139,7 +140,8 @@ typedef struct QcbActQuant {
   float* xe_out[3];          /* nullable: rotated activations (debug / FP modes) */
   long long ldxe;
   float* deq_out[3];         /* nullable: f32(s*(code-z)) fake-quant outputs     */
-  void* workspace;           /* >= 8*n_out*nseg bytes                            */
+  void* workspace;           /* qcb_act_quant_workspace_bytes(...) bytes         */
+  const double* chan_recip[3]; /* nullable: 1/chan_scale (else computed per call) */
 } QcbActQuant;
 
 int qcb_act_quant(const QcbActQuant* q, void* stream);
@@ -158,6 +160,7 @@ typedef struct QcbWeightPrep {
   int* colsum;               /* [N]                                              */
   float* w_eff;              /* nullable [K][N]: rotated weights                 */
   float* w_deq;              /* nullable [K][N]: dequantized weights             */
+  double* chan_recip_out;    /* nullable [K]: 1/chan_scale for qcb_act_quant     */
 } QcbWeightPrep;
 
 int qcb_weight_prep(const QcbWeightPrep* q, void* stream);
@@ -194,6 +197,10 @@ typedef struct QcbDdpm {
 } QcbDdpm;
 
 int qcb_ddpm_step(const QcbDdpm* d, void* stream);
+
+/* In-place x = f32(gelu_f64(x)) with SciPy's erf (model.py:145-147) over a
+ * [rows][ld] f32 buffer (cols valid columns); ld % 4 == 0, x 16-byte aligned. */
+int qcb_gelu_inplace(float* x, long long ld, int rows, int cols, void* stream);
 
 /* ---------------------------------------------------------------- reductions */
 /* Segmented f64 reductions over f32 feature maps, one result per segment.

@@ -47,13 +47,14 @@ class QcbActQuant(C.Structure):
                 ("ln_b", vp), ("mod_scale1", f32), ("mod_shift", f32), ("n_out", i32),
                 ("bits", i32), ("chan_scale", vp * 3), ("signs", vp * 3), ("codes", vp * 3),
                 ("ldc", i64), ("rowsum", vp * 3), ("scale", vp * 3), ("zero", vp * 3),
-                ("xe_out", vp * 3), ("ldxe", i64), ("deq_out", vp * 3), ("workspace", vp)]
+                ("xe_out", vp * 3), ("ldxe", i64), ("deq_out", vp * 3), ("workspace", vp),
+                ("chan_recip", vp * 3)]
 
 
 class QcbWeightPrep(C.Structure):
     _fields_ = [("w", vp), ("K", i32), ("N", i32), ("bits", i32), ("chan_scale", vp),
                 ("signs", vp), ("codes", vp), ("ldk", i64), ("scale", vp), ("zero", vp),
-                ("colsum", vp), ("w_eff", vp), ("w_deq", vp)]
+                ("colsum", vp), ("w_eff", vp), ("w_deq", vp), ("chan_recip_out", vp)]
 
 
 class QcbLnMod(C.Structure):
@@ -123,6 +124,7 @@ def lib():
         "qcb_ln_mod": [P(QcbLnMod), vp],
         "qcb_attention_f64": [P(QcbAttention), vp],
         "qcb_ddpm_step": [P(QcbDdpm), vp],
+        "qcb_gelu_inplace": [vp, i64, i32, i32, vp],
         "qcb_reduce_hlc": [QcbFeat, QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp, vp],
         "qcb_reduce_srap": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp, vp],
         "qcb_reduce_l1": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp],
@@ -148,7 +150,7 @@ def lib():
 
 
 EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_act_quant", "qcb_act_quant_workspace_bytes", "qcb_weight_prep", "qcb_ln_mod",
-            "qcb_attention_f64", "qcb_ddpm_step", "qcb_reduce_hlc", "qcb_reduce_srap",
+            "qcb_attention_f64", "qcb_ddpm_step", "qcb_gelu_inplace", "qcb_reduce_hlc", "qcb_reduce_srap",
             "qcb_reduce_l1", "qcb_reduce_workspace_bytes", "qcb_policy_plan_reuse",
             "qcb_policy_sim_mask", "qcb_policy_plan_finish", "qcb_policy_observe",
             "qcb_policy_observe_all",

@@ -80,6 +80,13 @@ extern "C" int qcb_ddpm_step(const QcbDdpm* d, void* stream) {
   return ddpm_launch(d, (cudaStream_t)stream);
 }
 
+extern "C" int qcb_gelu_inplace(float* x, long long ld, int rows, int cols, void* stream) {
+  if (!x) return QCB_ERR_VALUE;
+  if (rows <= 0 || cols <= 0 || ld < cols) return QCB_ERR_DIM;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (ld % 4)) return QCB_ERR_DIM;
+  return gelu_launch(x, ld, rows, cols, (cudaStream_t)stream);
+}
+
 extern "C" int qcb_device_sm_count(void) { return num_sms(); }
 
 extern "C" const char* qcb_version(void) { return "qcb200 0.1.0 sm_100a"; }

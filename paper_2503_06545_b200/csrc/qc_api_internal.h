@@ -36,4 +36,5 @@ int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st);
 int ln_mod_launch(const QcbLnMod* q, cudaStream_t st);
 int attention_f64_launch(const QcbAttention* a, cudaStream_t st);
 int ddpm_launch(const QcbDdpm* d, cudaStream_t st);
+int gelu_launch(float* x, long long ld, int rows, int cols, cudaStream_t st);
 }  // namespace qc

@@ -260,6 +260,63 @@ QC_DEV float gelu_f32_ref(float x) {
   return __double2float_rn(gelu_ref((double)x));
 }
 
+// ---- conversions without the XU pipe ----------------------------------------
+// On this B200 an f32<->f64 convert issues at ~8/clk/SM (measured), an f64 add
+// at ~61/clk/SM.  These exact bit-level equivalents run on the ALU / FP64 pipes
+// and fall back to the hardware conversion only for rare special values.
+
+// exact (double)f
+QC_DEV double f2d_alu(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t e = (u >> 23) & 0xFFu, m = u & 0x7FFFFFu;
+  if (e == 0xFFu || (e == 0u && m != 0u)) return (double)f;   // inf/nan/subnormal
+  const unsigned long long s = (unsigned long long)(u & 0x80000000u) << 32;
+  const unsigned long long body =
+      e == 0u ? 0ull : ((unsigned long long)(e + 896u) << 52) | ((unsigned long long)m << 29);
+  return __longlong_as_double((long long)(s | body));
+}
+
+// exact (double)i for any int32 (magic-number add on the FP64 pipe)
+QC_DEV double i2d_alu(int i) {
+  return __longlong_as_double(0x4338000000000000LL + (long long)i) - 6755399441055744.0;
+}
+
+// round-to-nearest-even of d to f32; integer path when the result is a normal
+// f32 (or zero), hardware conversion otherwise.
+QC_DEV float d2f_alu(double d) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  const unsigned long long s = u & 0x8000000000000000ull;
+  u &= 0x7FFFFFFFFFFFFFFFull;
+  if (u == 0ull) return __uint_as_float((uint32_t)(s >> 32));
+  const int ex = (int)(u >> 52);
+  if (ex < 1023 - 126 || ex > 1023 + 126) return __double2float_rn(d);   // f32 range edge
+  u += 0x0FFFFFFFull + ((u >> 29) & 1ull);   // RNE at bit 29; carries bump the exponent
+  const uint32_t bits = (uint32_t)(s >> 32) |
+                        ((uint32_t)((int)(u >> 52) - 1023 + 127) << 23) |
+                        (uint32_t)((u >> 29) & 0x7FFFFFull);
+  return __uint_as_float(bits);
+}
+
+// d rounded to a 24-bit significand (RNE), kept as f64 == (double)f32(d) for
+// values in the f32 normal range (callers guarantee the range).
+QC_DEV double d_round24(double d) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  u += 0x0FFFFFFFull + ((u >> 29) & 1ull);
+  u &= ~0x1FFFFFFFull;
+  return __longlong_as_double((long long)u);
+}
+
+// True when rounding the f64 value q to f32 could differ from rounding a value
+// a few f64 ulps away: the 29 dropped fraction bits are within 64 units of the
+// round-to-nearest midpoint pattern, or q is outside the f32 normal range.
+QC_DEV bool f64_near_f32_tie_dev(double q) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(q);
+  const int ex = (int)((u >> 52) & 0x7FF) - 1023;
+  if (ex < -125 || ex > 126) return true;
+  const int d = (int)((unsigned)u & 0x1FFFFFFFu) - (1 << 28);
+  return d > -64 && d < 64;
+}
+
 // Float total order as an unsigned key (for atomic min/max on floats).
 QC_DEV uint32_t f2key(float f) {
   uint32_t u = __float_as_uint(f);

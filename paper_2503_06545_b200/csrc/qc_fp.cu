@@ -22,8 +22,9 @@ struct GemmF64P {
 
 __global__ void __launch_bounds__(256) gemm_f64_k(const GemmF64P P) {
   const QcbGemmF64& g = P.g;
-  __shared__ float As[kFK][kFT + 1];
-  __shared__ float Ws[kFK][kFT + 1];
+  // tiles held as f64 so each element is converted once, not once per use
+  __shared__ double As[kFK][kFT + 2];
+  __shared__ double Ws[kFK][kFT + 2];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int m0 = blockIdx.y * kFT, n0 = blockIdx.x * kFT;
   const int seg_rows = g.seg_rows > 0 ? g.seg_rows : g.M;
@@ -89,10 +90,94 @@ __global__ void __launch_bounds__(256) gemm_f64_k(const GemmF64P P) {
   }
 }
 
+// Large-tile variant: 128x128 outputs per CTA, 8x8 per thread (strided so the
+// shared-memory reads are broadcast / conflict-free), k tile 8; each output is
+// still one ascending-k f64 FMA chain, so results equal `mm` bit for bit.
+constexpr int kBT = 128, kBK = 8;
+
+QC_DEV float f64_epilogue(const QcbGemmF64& g, double acc, long long rrow, int n) {
+  float y = __double2float_rn(acc);
+  switch (g.epilogue) {
+    case QCB_EPI_GELU: y = gelu_f32_ref(y); break;
+    case QCB_EPI_GATE_RESID: y = __fadd_rn(g.resid[rrow * g.ldr + n], __fmul_rn(g.gate_scalar, y)); break;
+    case QCB_EPI_RESID: y = __fadd_rn(g.resid[rrow * g.ldr + n], y); break;
+    case QCB_EPI_BIAS: y = __fadd_rn(y, g.bias[n]); break;
+    default: break;
+  }
+  return y;
+}
+
+__global__ void __launch_bounds__(256) gemm_f64_big_k(const GemmF64P P) {
+  const QcbGemmF64& g = P.g;
+  __shared__ double As[kBK][kBT];
+  __shared__ double Ws[kBK][kBT];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * kBT, n0 = blockIdx.x * kBT;
+  const int seg_rows = g.seg_rows > 0 ? g.seg_rows : g.M;
+  const int seg_valid = g.seg_valid > 0 ? g.seg_valid : seg_rows;
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  // per-thread A rows for the tile loads: 4 loads of (row, k) per k tile
+  for (int k0 = 0; k0 < g.K; k0 += kBK) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int idx = threadIdx.x + 256 * l;   // 0..1023
+      const int mm = idx >> 3, kk = idx & 7;   // A: 128 rows x 8 k
+      const int m = m0 + mm, k = k0 + kk;
+      double av = 0.0;
+      if (m < g.M && k < g.K) {
+        const int seg = m / seg_rows, r = m - seg * seg_rows;
+        const long long row = g.a_row0 ? g.a_row0[seg] + r : (long long)m;
+        if (r < seg_valid) av = (double)g.a[row * g.lda + k];
+      }
+      As[kk][mm] = av;
+      const int kw = idx >> 7, nn = idx & 127;  // W: 8 k x 128 cols
+      const int n = n0 + nn, k2 = k0 + kw;
+      Ws[kw][nn] = (n < g.N && k2 < g.K) ? (double)g.w[(long long)k2 * g.ldw + n] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      double a[8], w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = Ws[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], w[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + ty + 16 * i;
+    if (m >= g.M) continue;
+    const int seg = m / seg_rows, r = m - seg * seg_rows;
+    if (r >= seg_valid) continue;
+    const long long orow = g.out_row0 ? g.out_row0[seg] + r : (long long)m;
+    const long long rrow = g.resid_row0 ? g.resid_row0[seg] + r : (long long)m;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + tx + 16 * j;
+      if (n < g.N) g.out[orow * g.ldo + n] = f64_epilogue(g, acc[i][j], rrow, n);
+    }
+  }
+}
+
 int gemm_f64_launch(const QcbGemmF64* g, cudaStream_t st) {
   GemmF64P P{*g};
-  dim3 grid((g->N + kFT - 1) / kFT, (g->M + kFT - 1) / kFT);
-  gemm_f64_k<<<grid, 256, 0, st>>>(P);
+  if ((long long)g->M * g->N >= 256LL * 1024) {   // enough tiles for the big variant
+    dim3 grid((g->N + kBT - 1) / kBT, (g->M + kBT - 1) / kBT);
+    gemm_f64_big_k<<<grid, 256, 0, st>>>(P);
+  } else {
+    dim3 grid((g->N + kFT - 1) / kFT, (g->M + kFT - 1) / kFT);
+    gemm_f64_k<<<grid, 256, 0, st>>>(P);
+  }
   return launch_status();
 }
 
@@ -242,6 +327,120 @@ int attention_f64_launch(const QcbAttention* a, cudaStream_t st) {
   allow_max_smem(attention_f64_k, attr);
   dim3 grid(a->seg_valid > 0 ? a->seg_valid : a->S, a->heads, a->nseg);
   attention_f64_k<<<grid, 128, smem, st>>>(*a);
+  return launch_status();
+}
+
+// ------------------------------------------------------------------ GELU
+// In-place f32(gelu_f64(x)) with SciPy/cephes erf (model.py:145-147).
+// Phase A (branch-free, every element): x >= 6 -> x; |x/sqrt2| < 1 - 2^-40 ->
+// the cephes T/U rational on a reciprocal-based argument, accepted unless the
+// f64 result is near an f32 tie; everything else is "hard".  Phase B: the
+// warp's hard elements are compacted through shared memory and evaluated with
+// the exact cephes replica by all 32 lanes.
+QC_DEV bool gelu_fast(float xf, float& y) {
+  if (xf >= 6.0f) {
+    y = xf;
+    return true;
+  }
+  const double x = (double)xf;
+  const double xs = __dmul_rn(x, 0.70710678118654752440);   // ~ x / sqrt(2)
+  const double ax = fabs(xs);
+  if (!(ax < 1.0 - 0x1p-40)) return false;                   // erfc branch or boundary
+  const double z = __dmul_rn(ax, ax);
+  double t = 9.60497373987051638749E0;
+  t = QC_H(t, z, 9.00260197203842689217E1);
+  t = QC_H(t, z, 2.23200534594684319226E3);
+  t = QC_H(t, z, 7.00332514112805075473E3);
+  t = QC_H(t, z, 5.55923013010394962768E4);
+  double u = __dadd_rn(z, 3.35617141647503099647E1);
+  u = QC_H(u, z, 5.21357949780152679795E2);
+  u = QC_H(u, z, 4.59432382970980127987E3);
+  u = QC_H(u, z, 2.26290000613890934246E4);
+  u = QC_H(u, z, 4.92673942608635921086E4);
+  double r = __dmul_rn(ax, t) / u;
+  if (xs < 0.0) r = -r;
+  const double g = __dmul_rn(__dmul_rn(0.5, x), __dadd_rn(1.0, r));
+  // 1 + erf >= 0.15 here (no cancellation): the estimate is within a few ulps
+  if (f64_near_f32_tie_dev(g)) return false;
+  y = __double2float_rn(g);
+  return true;
+}
+
+__global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, int rows, int cols) {
+  __shared__ float q_val[8][256];
+  __shared__ int q_row[8][256];
+  __shared__ int q_col[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cpr = (cols + 255) / 256;   // 256-column chunks per row (8 per lane)
+  const long long nchunks = (long long)rows * cpr;
+  for (long long ch = (long long)blockIdx.x * 8 + warp; ch < nchunks;
+       ch += (long long)gridDim.x * 8) {
+    const int row = (int)(ch / cpr);
+    const int c0 = (int)(ch - (long long)row * cpr) * 256;
+    float* xr = x + row * ld;
+    float v[8];
+    uint32_t hard = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = c0 + h * 128 + lane * 4;
+      if (c + 3 < cols) {
+        const float4 t4 = *reinterpret_cast<const float4*>(xr + c);
+        v[4 * h] = t4.x; v[4 * h + 1] = t4.y; v[4 * h + 2] = t4.z; v[4 * h + 3] = t4.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[4 * h + e] = (c + e < cols) ? xr[c + e] : 0.f;
+      }
+    }
+    float y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int c = c0 + (i >> 2) * 128 + lane * 4 + (i & 3);
+      if (c < cols && !gelu_fast(v[i], y[i])) hard |= 1u << i;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = c0 + h * 128 + lane * 4;
+      if (c + 3 < cols) {
+        *reinterpret_cast<float4*>(xr + c) =
+            make_float4(y[4 * h], y[4 * h + 1], y[4 * h + 2], y[4 * h + 3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c + e < cols) xr[c + e] = y[4 * h + e];
+      }
+    }
+    // phase B: compact hard elements of the warp, evaluate exactly on all lanes
+    const int cnt = __popc(hard);
+    int off = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += n;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
+    if (total == 0) continue;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((hard >> i) & 1u) {
+        q_val[warp][off] = v[i];
+        q_row[warp][off] = row;
+        q_col[warp][off] = c0 + (i >> 2) * 128 + lane * 4 + (i & 3);
+        ++off;
+      }
+    __syncwarp();
+    for (int i = lane; i < total; i += 32)
+      x[q_row[warp][i] * ld + q_col[warp][i]] = gelu_f32_ref(q_val[warp][i]);
+    __syncwarp();
+  }
+}
+
+int gelu_launch(float* x, long long ld, int rows, int cols, cudaStream_t st) {
+  const long long chunks = (long long)rows * ((cols + 255) / 256);
+  long long blocks = (chunks + 7) / 8;
+  const long long cap = (long long)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  gelu_inplace_k<<<(unsigned)blocks, 256, 0, st>>>(x, ld, rows, cols);
   return launch_status();
 }
 

@@ -240,16 +240,7 @@ constexpr int kV2Threads = 128;
 
 // true when the f64 value q is close enough to an f32 rounding boundary that a
 // multiply-by-reciprocal estimate may round differently from exact division.
-// True when rounding the f64 value q to f32 could differ from rounding a value
-// a few f64 ulps away: the 29 dropped fraction bits are within 64 units of the
-// round-to-nearest midpoint pattern, or q is outside the f32 normal range.
-QC_DEV bool f64_near_f32_tie(double q) {
-  const unsigned long long u = (unsigned long long)__double_as_longlong(q);
-  const int ex = (int)((u >> 52) & 0x7FF) - 1023;
-  if (ex < -125 || ex > 126) return true;
-  const int d = (int)((unsigned)u & 0x1FFFFFFFu) - (1 << 28);
-  return d > -64 && d < 64;
-}
+QC_DEV bool f64_near_f32_tie(double q) { return f64_near_f32_tie_dev(q); }
 
 // f32(f64(h) / c) (quant.py:164): h * (1/c) is within 2 ulp64 of the exact
 // division, so its f32 rounding agrees unless it sits near a tie.
@@ -291,6 +282,8 @@ struct V2Smem {
   double xbuf[4][32 * 33];  // per-warp transpose / exchange buffer
   float hbuf[4][1024 + 8 * 32];  // per-warp prologue output (block part + tail)
   double red[4][2];         // cross-warp LN partial sums
+  float run_mn[4][3][32];   // per-lane running min / max per output (smem: dynamic o)
+  float run_mx[4][3][32];
 };
 
 QC_DEV void v2_row_index(const ActQuantParams& p, int gr, int& seg, int& mrow,
@@ -342,14 +335,17 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
   const int T = K - b;
   double* xb = sm.xbuf[warp];
   float* hb = sm.hbuf[warp];
-  float mn[3], mx[3];
+  float* mn_s = &sm.run_mn[warp][0][0];   // [o*32 + lane]
+  float* mx_s = &sm.run_mx[warp][0][0];
   int cur_seg = -1;
 #pragma unroll
-  for (int o = 0; o < 3; ++o) { mn[o] = INFINITY; mx[o] = -INFINITY; }
+  for (int o = 0; o < 3; ++o) { mn_s[o * 32 + lane] = INFINITY; mx_s[o * 32 + lane] = -INFINITY; }
 
   auto flush = [&](int seg) {
-    for (int o = 0; o < p.n_out; ++o) {
-      float lo = mn[o], hi = mx[o];
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (o >= p.n_out) break;
+      float lo = mn_s[o * 32 + lane], hi = mx_s[o * 32 + lane];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
@@ -360,8 +356,8 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
         atomicMin(&k[0], f2key(lo));
         atomicMax(&k[1], f2key(hi));
       }
-      mn[o] = INFINITY;
-      mx[o] = -INFINITY;
+      mn_s[o * 32 + lane] = INFINITY;
+      mx_s[o * 32 + lane] = -INFINITY;
     }
   };
 
@@ -405,12 +401,27 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
         const double var = v2_row_sum<WPR>(v, sm.red[rowslot], rowslot, part) / K;
         const double sd = sqrt(var + 1e-5);
         const double rsd = 1.0 / sd;
+        // branch-free fast path for the whole slab, exact fix-up after a vote
+        uint32_t slow = 0;
 #pragma unroll
         for (int r = 0; r < 32; ++r) {
           const int col = part * 1024 + lane + 32 * r;
           const double g = p.ln_g ? (double)__ldg(p.ln_g + col) : 1.0;
           const double bb = p.ln_b ? (double)__ldg(p.ln_b + col) : 0.0;
-          hb[lane + 32 * r] = ln_elem(xv[r], mean, sd, rsd, g, bb, p.scale1, p.shift);
+          const double u = __dmul_rn(__dmul_rn((double)xv[r] - mean, rsd), g);
+          const double v = __dadd_rn(u, bb);
+          slow |= (uint32_t)(!(fabs(u) <= 4.0 * fabs(v)) || f64_near_f32_tie(v)) << r;
+          hb[lane + 32 * r] = __fadd_rn(__fmul_rn(__double2float_rn(v), p.scale1), p.shift);
+        }
+        if (__any_sync(0xffffffffu, slow != 0)) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            if ((slow >> r) & 1u) {
+              const int col = part * 1024 + lane + 32 * r;
+              const double g = p.ln_g ? (double)p.ln_g[col] : 1.0;
+              const double bb = p.ln_b ? (double)p.ln_b[col] : 0.0;
+              hb[lane + 32 * r] = ln_elem(xv[r], mean, sd, rsd, g, bb, p.scale1, p.shift);
+            }
         }
 #pragma unroll
         for (int i = 0; i < TPL; ++i) {
@@ -440,13 +451,28 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
       const double* rc = a.rc[o];
       const uint32_t* sgb = reinterpret_cast<const uint32_t*>(p.signs[o]);
       double w[32];
+      if (c) {
+        uint32_t slow = 0;
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const int col = part * 1024 + lane + 32 * r;
-        const float h = hb[lane + 32 * r];
-        float y = c ? div_to_f32(h, __ldg(c + col), __ldg(rc + col)) : h;
-        if (c) y = __uint_as_float(__float_as_uint(y) ^ (__ldg(sgb + col) & 0x80000000u));
-        w[r] = (double)y;
+        for (int r = 0; r < 32; ++r) {
+          const int col = part * 1024 + lane + 32 * r;
+          const double q = __dmul_rn((double)hb[lane + 32 * r], __ldg(rc + col));
+          slow |= (uint32_t)f64_near_f32_tie(q) << r;
+          const float y = __double2float_rn(q);
+          w[r] = (double)__uint_as_float(__float_as_uint(y) ^ (__ldg(sgb + col) & 0x80000000u));
+        }
+        if (__any_sync(0xffffffffu, slow != 0)) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            if ((slow >> r) & 1u) {
+              const int col = part * 1024 + lane + 32 * r;
+              const float y = __double2float_rn(__ddiv_rn((double)hb[lane + 32 * r], c[col]));
+              w[r] = (double)__uint_as_float(__float_as_uint(y) ^ (sgb[col] & 0x80000000u));
+            }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) w[r] = (double)hb[lane + 32 * r];
       }
       float xe[32];
       if (c) {
@@ -511,7 +537,7 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
         tl[i] = (c && t < T) ? div_to_f32(h, __ldg(c + b + t), __ldg(rc + b + t)) : h;
       }
       if (active) {
-        float lo = mn[o], hi = mx[o];
+        float lo = mn_s[o * 32 + lane], hi = mx_s[o * 32 + lane];
 #pragma unroll
         for (int r = 0; r < 32; ++r) { lo = fminf(lo, xe[r]); hi = fmaxf(hi, xe[r]); }
 #pragma unroll
@@ -519,8 +545,8 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
           const int t = (i * WPR + part) * 32 + lane;
           if (t < T) { lo = fminf(lo, tl[i]); hi = fmaxf(hi, tl[i]); }
         }
-        mn[o] = lo;
-        mx[o] = hi;
+        mn_s[o * 32 + lane] = lo;
+        mx_s[o * 32 + lane] = hi;
         float* so = a.stash[o] + out_row * a.ld_stash;
         if (c) {   // rotated layout: this lane owns e = 32 lane + r (contiguous)
           float4* dst = reinterpret_cast<float4*>(so + part * 1024 + 32 * lane);
@@ -539,6 +565,206 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
       }
     }
     __syncwarp();
+  }
+  if (cur_seg >= 0) flush(cur_seg);
+}
+
+// ------------------------------------------------------------------ v3 pass 1
+// CTA-level shared-memory FWHT with radix-16 register passes.  256 threads
+// handle R = 4096 / b rows at a time; each thread owns 16 f64 values per pass
+// (low register use -> several CTAs per SM).  Element e of a row lives at
+// smem index e + (e >> 4) (one pad per 16 keeps f64 accesses ~conflict-free).
+constexpr int kV3Threads = 256;
+
+QC_DEV int v3_pad(int e) { return e + (e >> 4); }
+
+// Element index of the j-th value (j < 16) of group gi in a pass over bits
+// [sh, sh+q): j's low q bits -> bits [sh, sh+q), j's high 4-q bits -> the
+// lowest free bits, gi fills the remaining positions in ascending order.
+QC_DEV int v3_elem(int gi, int j, int sh, int q, int nbits) {
+  const int lo_bits = 4 - q;   // extra "batch" bits taken from the bottom
+  int e = ((j & ((1 << q) - 1)) << sh) | (j >> q);
+  int g = gi, pos = 0;
+  for (int bit = 0; bit < nbits; ++bit) {
+    const bool used = (bit >= sh && bit < sh + q) || (bit < lo_bits && !(sh == 0));
+    if (used) continue;
+    e |= ((g >> pos) & 1) << bit;
+    ++pos;
+  }
+  return e;
+}
+
+template <int B>
+struct V3Smem {
+  static constexpr int R = 4096 / B;
+  double f[R][B + B / 16];
+  float h[R][2 * B];      // prologue output (K < 2b)
+  double red[8];          // LN partial sums, one per warp
+  float run_mn[3][kV3Threads / 32];
+  float run_mx[3][kV3Threads / 32];
+};
+
+template <int B, bool kPow2Scale>
+__global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, const AQ2 a) {
+  constexpr int R = 4096 / B;           // rows per CTA iteration
+  constexpr int TPR = kV3Threads / R;   // threads per row (b / 16)
+  constexpr int NB = (B == 1024) ? 10 : (B == 2048 ? 11 : 12);
+  extern __shared__ __align__(16) uint8_t v3_smem[];
+  V3Smem<B>& sm = *reinterpret_cast<V3Smem<B>*>(v3_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rl = tid / TPR, lt = tid % TPR;   // row slot, thread within the row
+  const int K = p.K, T = K - B;
+  double* f = sm.f[rl];
+  float* h = sm.h[rl];
+  int cur_seg = -1;
+  for (int o = 0; o < 3; ++o) {
+    if (lane == 0) { sm.run_mn[o][warp] = INFINITY; sm.run_mx[o][warp] = -INFINITY; }
+  }
+  auto flush = [&](int seg) {
+    if (lane != 0) return;
+    for (int o = 0; o < p.n_out; ++o) {
+      const float lo = sm.run_mn[o][warp], hi = sm.run_mx[o][warp];
+      if (hi >= lo) {
+        uint32_t* k = p.keys + ((size_t)o * p.nseg + seg) * 2;
+        atomicMin(&k[0], f2key(lo));
+        atomicMax(&k[1], f2key(hi));
+      }
+      sm.run_mn[o][warp] = INFINITY;
+      sm.run_mx[o][warp] = -INFINITY;
+    }
+  };
+
+  for (int base = blockIdx.x * R; base < a.total_rows; base += gridDim.x * R) {
+    const int gr = base + rl;
+    const bool active = gr < a.total_rows;
+    int seg = 0, mrow = 0;
+    long long in_row = 0, out_row = 0;
+    if (active) v2_row_index(p, gr, seg, mrow, in_row, out_row);
+    if (active && seg != cur_seg) {
+      if (cur_seg >= 0) flush(cur_seg);
+      cur_seg = seg;
+    }
+    // ---- load the row (coalesced) + prologue -> h (f32 smem)
+    const float* xr = p.x + in_row * p.ldx;
+    if (p.prologue == QCB_PRO_LN_MOD) {
+      double s = 0.0;
+      for (int j = lt; j < K; j += TPR) {
+        const float xv = active ? __ldg(xr + j) : 0.f;
+        h[j] = xv;
+        s += (double)xv;
+      }
+      s = warp_sum(s);
+      if (lane == 0) sm.red[warp] = s;
+      __syncthreads();
+      double tot = 0.0;
+      for (int w = rl * (TPR / 32); w < (rl + 1) * (TPR / 32); ++w) tot += sm.red[w];
+      const double mean = tot / K;
+      double v = 0.0;
+      for (int j = lt; j < K; j += TPR) {
+        const double d = (double)h[j] - mean;
+        v += d * d;
+      }
+      v = warp_sum(v);
+      __syncthreads();
+      if (lane == 0) sm.red[warp] = v;
+      __syncthreads();
+      double vt = 0.0;
+      for (int w = rl * (TPR / 32); w < (rl + 1) * (TPR / 32); ++w) vt += sm.red[w];
+      const double sd = sqrt(vt / K + 1e-5);
+      const double rsd = 1.0 / sd;
+      for (int j = lt; j < K; j += TPR) {
+        const double g = p.ln_g ? (double)__ldg(p.ln_g + j) : 1.0;
+        const double bb = p.ln_b ? (double)__ldg(p.ln_b + j) : 0.0;
+        h[j] = ln_elem(h[j], mean, sd, rsd, g, bb, p.scale1, p.shift);
+      }
+    } else if (p.prologue == QCB_PRO_GELU) {
+      for (int j = lt; j < K; j += TPR) h[j] = gelu_f32_ref(active ? __ldg(xr + j) : 0.f);
+    } else {
+      for (int j = lt; j < K; j += TPR) h[j] = active ? __ldg(xr + j) : 0.f;
+    }
+    __syncthreads();
+    for (int o = 0; o < p.n_out; ++o) {
+      const double* c = p.c[o];
+      const double* rc = a.rc[o];
+      const uint32_t* sgb = reinterpret_cast<const uint32_t*>(p.signs[o]);
+      float* so = a.stash[o] + out_row * a.ld_stash;
+      float lo = INFINITY, hi = -INFINITY;
+      if (c) {
+        // balance + sign into f (f64), tail straight to the stash
+        for (int e = lt; e < B; e += TPR) {
+          const float hv = h[e];
+          const double q = __dmul_rn((double)hv, __ldg(rc + e));
+          float y = f64_near_f32_tie(q) ? __double2float_rn(__ddiv_rn((double)hv, c[e]))
+                                        : __double2float_rn(q);
+          y = __uint_as_float(__float_as_uint(y) ^ (__ldg(sgb + e) & 0x80000000u));
+          f[v3_pad(e)] = (double)y;
+        }
+        for (int t = lt; t < T; t += TPR) {
+          const float hv = h[B + t];
+          const double q = __dmul_rn((double)hv, __ldg(rc + B + t));
+          const float y = f64_near_f32_tie(q) ? __double2float_rn(__ddiv_rn((double)hv, c[B + t]))
+                                              : __double2float_rn(q);
+          lo = fminf(lo, y);
+          hi = fmaxf(hi, y);
+          if (active) so[B + t] = y;
+        }
+        __syncthreads();
+        // radix-16 passes over bits [0,4), [4,8), [8, NB)
+#pragma unroll
+        for (int pass = 0; pass < 3; ++pass) {
+          const int sh = 4 * pass;
+          const int q = (NB - sh) < 4 ? (NB - sh) : 4;
+          double v[16];
+          int idx[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            idx[j] = v3_pad(v3_elem(lt, j, sh, q, NB));
+            v[j] = f[idx[j]];
+          }
+#pragma unroll
+          for (int hs = 1; hs < 16; hs <<= 1) {
+            if (hs >= (1 << q)) break;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if ((j & hs) == 0) {
+                const double u = v[j], w = v[j + hs];
+                v[j] = u + w;
+                v[j + hs] = u - w;
+              }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[idx[j]] = v[j];
+          __syncthreads();
+        }
+        // scale, min/max, coalesced stash write
+        for (int e = lt; e < B; e += TPR) {
+          const double v = f[v3_pad(e)];
+          const float xe = kPow2Scale ? __fmul_rn(__double2float_rn(v), p.rscale)
+                                      : __double2float_rn(__dmul_rn(v, (double)p.rscale));
+          lo = fminf(lo, xe);
+          hi = fmaxf(hi, xe);
+          if (active) so[e] = xe;
+        }
+      } else {
+        for (int e = lt; e < K; e += TPR) {
+          const float y = h[e];
+          lo = fminf(lo, y);
+          hi = fmaxf(hi, y);
+          if (active) so[e] = y;
+        }
+      }
+      // per-warp running min/max (all lanes of a warp serve the same row)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+      }
+      if (lane == 0 && active) {
+        sm.run_mn[o][warp] = fminf(sm.run_mn[o][warp], lo);
+        sm.run_mx[o][warp] = fmaxf(sm.run_mx[o][warp], hi);
+      }
+      __syncthreads();   // f reused by the next output
+    }
   }
   if (cur_seg >= 0) flush(cur_seg);
 }
@@ -583,13 +809,28 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, 
           for (int e = 0; e < 4; ++e) v4[e] = (j + e < K) ? xr[j + e] : 0.f;
         }
         uint32_t packed = 0;
+        int code[4];
+        bool slow = false;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {   // f32 estimate of rha(xe/s), branch-free
+          const float qf = __fmul_rn(v4[e], inv_sf);
+          const float t = __fadd_rn(fabsf(qf), 0.5f);
+          const float n = floorf(t);
+          const float fr = t - n;
+          slow |= (fr < 0x1p-12f) || (fr > 1.0f - 0x1p-12f);
+          const float v = fminf(fmaxf(__fadd_rn(qf < 0.0f ? -n : n, zf), 0.0f), topf);
+          code[e] = (int)v;
+        }
+        if (slow) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) code[e] = code_of(v4[e], inv_sf, s, zf, topf);
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (j + e < K) {
-            const int code = code_of(v4[e], inv_sf, s, zf, topf);
-            rs += code;
-            packed |= (uint32_t)code << (8 * e);
-            if (dr) dr[j + e] = __double2float_rn(__dmul_rn(s, (double)(code - (int)z)));
+            rs += code[e];
+            packed |= (uint32_t)code[e] << (8 * e);
+            if (dr) dr[j + e] = __double2float_rn(__dmul_rn(s, (double)(code[e] - (int)z)));
           }
         }
         if (cr) {
@@ -671,8 +912,11 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     a.ld_stash = q->K;
     for (int o = 0; o < q->n_out; ++o) {
       a.rc[o] = rcbuf + (size_t)o * q->K;
-      if (q->chan_scale[o])
+      if (q->chan_scale[o] && q->chan_recip[o]) {
+        a.rc[o] = q->chan_recip[o];
+      } else if (q->chan_scale[o]) {
         recip_k<<<(q->K + 255) / 256, 256, 0, st>>>(q->chan_scale[o], rcbuf + (size_t)o * q->K, q->K);
+      }
       if (q->xe_out[o] && q->ldxe == q->K) {
         a.stash[o] = q->xe_out[o];
       } else {
@@ -684,21 +928,24 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     int blocks = (a.total_rows + rpc - 1) / rpc;
     const int cap = num_sms() * 4;
     if (blocks > cap) blocks = cap;
-    // 1/sqrt(b) is a power of two for b = 1024, 4096
-    const size_t sm1 = sizeof(V2Smem<1>);
+    // pass 1: CTA shared-memory FWHT (v3); 1/sqrt(b) is a power of two for b = 1024, 4096
+    (void)blocks;
     static bool at1 = false, at2 = false, at4 = false;
-    switch (wpr) {
-      case 1:
-        allow_max_smem(aq2_pass1<1, true>, at1);
-        aq2_pass1<1, true><<<blocks, kV2Threads, sm1, st>>>(p, a);
+    const int rows_per_cta = 4096 / b;
+    int b1 = (a.total_rows + rows_per_cta - 1) / rows_per_cta;
+    if (b1 > num_sms() * 3) b1 = num_sms() * 3;
+    switch (b) {
+      case 1024:
+        allow_max_smem(aq3_pass1<1024, true>, at1);
+        aq3_pass1<1024, true><<<b1, kV3Threads, sizeof(V3Smem<1024>), st>>>(p, a);
         break;
-      case 2:
-        allow_max_smem(aq2_pass1<2, false>, at2);
-        aq2_pass1<2, false><<<blocks, kV2Threads, sm1, st>>>(p, a);
+      case 2048:
+        allow_max_smem(aq3_pass1<2048, false>, at2);
+        aq3_pass1<2048, false><<<b1, kV3Threads, sizeof(V3Smem<2048>), st>>>(p, a);
         break;
       default:
-        allow_max_smem(aq2_pass1<4, true>, at4);
-        aq2_pass1<4, true><<<blocks, kV2Threads, sm1, st>>>(p, a);
+        allow_max_smem(aq3_pass1<4096, true>, at4);
+        aq3_pass1<4096, true><<<b1, kV3Threads, sizeof(V3Smem<4096>), st>>>(p, a);
         break;
     }
     int b2 = (a.total_rows + 3) / 4;
@@ -733,6 +980,7 @@ struct WeightPrepParams {
   int* colsum;    // [N]
   float* w_eff;   // nullable [K][N] (debug / weight-only FP mode)
   float* w_deq;   // nullable [K][N]: f32(s*(code-z)) (runtime.py:61)
+  double* rc_out;  // nullable [K]: 1/c
 };
 
 // One CTA per output channel n.
@@ -794,6 +1042,8 @@ __global__ void __launch_bounds__(kQThreads) weight_prep_cols(const WeightPrepPa
     p.zero[n] = (int)z;
     p.colsum[n] = cs;
   }
+  if (n == 0 && p.rc_out && p.c)
+    for (int k = threadIdx.x; k < K; k += blockDim.x) p.rc_out[k] = 1.0 / p.c[k];
 }
 
 int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st) {
@@ -815,6 +1065,7 @@ int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st) {
   p.colsum = q->colsum;
   p.w_eff = q->w_eff;
   p.w_deq = q->w_deq;
+  p.rc_out = q->chan_recip_out;
   const size_t smem = (size_t)q->K * sizeof(double);
   if (smem > 200 * 1024) return QCB_ERR_DIM;
   static bool attr = false;

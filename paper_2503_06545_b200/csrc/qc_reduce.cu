@@ -13,7 +13,7 @@
 namespace qc {
 
 constexpr int kRThreads = 256;
-constexpr int kMaxChunks = 64;
+constexpr int kMaxChunks = 1024;
 
 struct FeatP {
   const float* base;
@@ -139,26 +139,31 @@ __global__ void __launch_bounds__(kRThreads)
     last = (done == chunks - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
+    // fixed-order final sum: thread i folds chunks i, i+256, ..., then a fixed tree
     __threadfence();
     double tot[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) tot[i] = 0.0;
-    for (int ch = 0; ch < chunks; ++ch) {
-      const volatile double* pp = partials + ((size_t)seg * kMaxChunks + ch) * NV;
+    for (int ch = threadIdx.x; ch < chunks; ch += kRThreads) {
+      const double* pp = partials + ((size_t)seg * kMaxChunks + ch) * NV;
 #pragma unroll
-      for (int i = 0; i < NV; ++i) tot[i] += pp[i];
+      for (int i = 0; i < NV; ++i) tot[i] += __ldcg(pp + i);
     }
+    __syncthreads();
+    block_sum_vec<NV>(tot, scratch);
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) res[(size_t)seg * NV + i] = tot[i];
-    tickets[seg] = 0;
+      for (int i = 0; i < NV; ++i) res[(size_t)seg * NV + i] = tot[i];
+      tickets[seg] = 0;
+    }
   }
 }
 
 static int chunks_for(int rows, int cols, int nseg) {
   long long elems = (long long)rows * cols;
-  int ch = (int)((elems + 32767) / 32768);  // ~32K elements per CTA
-  int per_seg_target = (4 * num_sms() + nseg - 1) / nseg;
+  int ch = (int)((elems + 8191) / 8192);  // ~8K elements (32 KB per operand) per CTA
+  int per_seg_target = (8 * num_sms() + nseg - 1) / nseg;  // ~8 CTAs per SM in flight
   if (ch > per_seg_target) ch = per_seg_target;
   if (ch > kMaxChunks) ch = kMaxChunks;
   if (ch > rows) ch = rows;

@@ -57,6 +57,7 @@ class PackedWeight:
     signs: Optional[torch.Tensor] = None        # f32 [b]
     w_deq: Optional[torch.Tensor] = None        # f32 [K][N] dequantized (weight-only mode)
     w_eff: Optional[torch.Tensor] = None
+    chan_recip: Optional[torch.Tensor] = None   # f64 [K] 1/c (quantizer fast path)
 
 
 def weight_prep(w: torch.Tensor, bits: int, chan_scale: Optional[torch.Tensor] = None,
@@ -72,15 +73,18 @@ def weight_prep(w: torch.Tensor, bits: int, chan_scale: Optional[torch.Tensor] =
     colsum = torch.empty(Nn, dtype=torch.int32, device=dev)
     w_deq = torch.empty((K, Nn), dtype=torch.float32, device=dev) if keep_deq else None
     w_eff = torch.empty((K, Nn), dtype=torch.float32, device=dev) if keep_eff else None
+    rc = None
     if chan_scale is not None:
         chan_scale = chan_scale.to(dev, torch.float64).contiguous()
         signs = signs.to(dev, torch.float32).contiguous()
+        rc = torch.empty(K, dtype=torch.float64, device=dev)
     d = N.QcbWeightPrep(N.ptr(w), K, Nn, bits, N.ptr(chan_scale), N.ptr(signs), N.ptr(codes),
                         ldk, N.ptr(scale), N.ptr(zero), N.ptr(colsum), N.ptr(w_eff),
-                        N.ptr(w_deq))
+                        N.ptr(w_deq), N.ptr(rc))
     N.check(N.lib().qcb_weight_prep(C.byref(d), N.stream_ptr(stream)), "weight_prep")
     count(1)
-    return PackedWeight(codes, scale, zero, colsum, K, Nn, bits, chan_scale, signs, w_deq, w_eff)
+    return PackedWeight(codes, scale, zero, colsum, K, Nn, bits, chan_scale, signs, w_deq, w_eff,
+                        rc)
 
 
 @dataclass
@@ -159,6 +163,8 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
     for o, tr in enumerate(transforms):
         if tr is not None:
             q.chan_scale[o], q.signs[o] = N.ptr(tr[0]), N.ptr(tr[1])
+            if len(tr) > 2:
+                q.chan_recip[o] = N.ptr(tr[2])
         r = res[o]
         q.codes[o], q.rowsum[o] = N.ptr(r.codes), N.ptr(r.rowsum)
         q.scale[o], q.zero[o] = N.ptr(r.scale), N.ptr(r.zero)
@@ -276,6 +282,17 @@ def ddpm(x, eps, c1: float, c2: float, noise=None, c3: float = 0.0, out=None, st
     N.check(N.lib().qcb_ddpm_step(C.byref(d), N.stream_ptr(stream)), "ddpm_step")
     count(1)
     return out
+
+
+def gelu_inplace(x: torch.Tensor, rows: Optional[int] = None, cols: Optional[int] = None,
+                 stream=None) -> torch.Tensor:
+    """x[:rows, :cols] = f32(gelu_f64(x)) in place (reference _gelu)."""
+    rows = rows if rows is not None else x.shape[0]
+    cols = cols if cols is not None else x.shape[1]
+    N.check(N.lib().qcb_gelu_inplace(N.ptr(x), x.stride(0), rows, cols, N.stream_ptr(stream)),
+            "gelu")
+    count(1)
+    return x
 
 
 def feat(t: Optional[torch.Tensor], row0=None, ld=None) -> N.QcbFeat:

@@ -271,7 +271,8 @@ class QuantCacheEngine:
         quant_acts = tog.aigq_acts and bits < FP_BITS
         if tog.aigq_weights and quant_acts:
             pws = [self.packed[l][s] for s in sites]
-            trs = [(p.chan_scale, p.signs) if p.chan_scale is not None else None for p in pws]
+            trs = [(p.chan_scale, p.signs, p.chan_recip) if p.chan_scale is not None else None
+                   for p in pws]
             acs = []
             for o, p in enumerate(pws):
                 a = self.ac[o]
@@ -369,14 +370,16 @@ class QuantCacheEngine:
         self._attention(self.q2, self.k2, self.v2, self.att, n, 1, 1)
         self._site(l, "ca_o", bits, self.att, n, epi=N.EPI_RESID, out=A, out_row0=out_row0,
                    resid=A, resid_row0=out_row0)
-        # FFN.  On the integer path GELU (model.py:197) moves from the ffn1
-        # epilogue into the ffn2 quantizer's prologue: same f32(gelu_f64(y)) per
-        # element, computed once, on the quantizer's wider grid.
+        # FFN.  On the integer path GELU (model.py:197) runs as its own in-place
+        # kernel between ffn1 and the ffn2 quantizer: same f32(gelu_f64(y)) per
+        # element, with divergent exact evaluations compacted per warp.
         int_path = self.tog.aigq_weights and self.tog.aigq_acts and bits < FP_BITS
         self._site(l, "ffn1", bits, A, n, x_row0=out_row0, ln=(ln3g, ln3b), mod=(sc3, sh3),
                    epi=N.EPI_STORE if int_path else N.EPI_GELU, out=self.hid)
+        if int_path:
+            Dv.gelu_inplace(self.hid, rows=n * self.Sp)
         self._site(l, "ffn2", bits, self.hid, n, epi=N.EPI_GATE_RESID, out=A,
-                   out_row0=out_row0, resid=A, resid_row0=out_row0, gate=g3, gelu_in=int_path)
+                   out_row0=out_row0, resid=A, resid_row0=out_row0, gate=g3)
 
     # ------------------------------------------------------------------ run
     def generate(self, seeds: Sequence[int], device_noise_seed: Optional[int] = None,

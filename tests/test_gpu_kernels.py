@@ -287,7 +287,7 @@ class TestSiteFixtures:
 class TestFp:
     def test_gemm_f64_matches_seq_mm(self, D):
         rng = np.random.default_rng(5)
-        for (m, k, n) in [(3, 4, 5), (64, 64, 256), (70, 256, 64), (1, 8, 16)]:
+        for (m, k, n) in [(3, 4, 5), (64, 64, 256), (70, 256, 64), (1, 8, 16), (300, 1152, 900)]:
             a = rng.standard_normal((m, k)).astype(np.float32)
             w = rng.standard_normal((k, n)).astype(np.float32)
             assert np.array_equal(D.gemm_f64(t(a), t(w)).cpu().numpy(), O.seq_mm(a, w))
@@ -299,6 +299,25 @@ class TestFp:
             got = D.attention_f64(t(q), t(k), t(v), h).cpu().numpy()
             want = O.attention_heads(q, k, v, h)
             np.testing.assert_allclose(got, want, rtol=0, atol=2e-7 * np.abs(want).max())
+
+    def test_gelu_inplace_exact(self, D):
+        """f32(gelu_f64(x)) with SciPy's erf (model.py:145-147), all regions."""
+        rng = np.random.default_rng(12)
+        x = np.concatenate([
+            rng.standard_normal(300_000) * 2.0, rng.uniform(-40, 40, 50_000),
+            np.linspace(-1.4143, -1.4141, 2001), np.linspace(1.4141, 1.4143, 2001),
+            np.linspace(5.99, 6.01, 2001), [0.0, -0.0, 1e-30, -1e-30, 37.0, -37.0, -39.0]])
+        x = x.astype(np.float32)
+        cols = 1000
+        pad = (-len(x)) % cols
+        buf = np.concatenate([x, np.zeros(pad, np.float32)]).reshape(-1, cols)
+        dev = torch.zeros((buf.shape[0], 1024), dtype=torch.float32, device="cuda")
+        dev[:, :cols] = t(buf)
+        D.gelu_inplace(dev, cols=cols)
+        got = dev[:, :cols].cpu().numpy().reshape(-1)[:len(x)]
+        want = O.gelu64(x)
+        bad = np.flatnonzero(got.view(np.int32) != want.view(np.int32))
+        assert bad.size == 0, (bad.size, x[bad[:5]], got[bad[:5]], want[bad[:5]])
 
     def test_ln_mod(self, D):
         rng = np.random.default_rng(7)
