@@ -75,6 +75,16 @@ QC_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1
       "r"(c0), "r"(c1), "r"(smem_u32(src))
       : "memory");
 }
+// 1-D bulk async copy global -> shared (16-byte aligned, size % 16 == 0),
+// completion signalled on `bar` as transaction bytes.
+QC_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 QC_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 QC_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 QC_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -297,6 +307,20 @@ QC_DEV float d2f_alu(double d) {
   return __uint_as_float(bits);
 }
 
+// Branch-free d2f_alu for batches: sets `bad` when d needs the hardware path
+// (f32 range edge); the caller redoes the batch with __double2float_rn then.
+QC_DEV float d2f_alu_flag(double d, bool& bad) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  const uint32_t s = (uint32_t)(u >> 32) & 0x80000000u;
+  u &= 0x7FFFFFFFFFFFFFFFull;
+  const int ex = (int)(u >> 52);
+  bad |= (u != 0ull) & ((ex < 1023 - 126) | (ex > 1023 + 126));
+  u += 0x0FFFFFFFull + ((u >> 29) & 1ull);
+  const uint32_t bits = ((uint32_t)((int)(u >> 52) - 1023 + 127) << 23) |
+                        (uint32_t)((u >> 29) & 0x7FFFFFull);
+  return __uint_as_float(s | (ex == 0 ? 0u : bits));
+}
+
 // d rounded to a 24-bit significand (RNE), kept as f64 == (double)f32(d) for
 // values in the f32 normal range (callers guarantee the range).
 QC_DEV double d_round24(double d) {
@@ -311,6 +335,7 @@ QC_DEV double d_round24(double d) {
 // round-to-nearest midpoint pattern, or q is outside the f32 normal range.
 QC_DEV bool f64_near_f32_tie_dev(double q) {
   const unsigned long long u = (unsigned long long)__double_as_longlong(q);
+  if ((u << 1) == 0ull) return false;   // +-0 rounds exactly
   const int ex = (int)((u >> 52) & 0x7FF) - 1023;
   if (ex < -125 || ex > 126) return true;
   const int d = (int)((unsigned)u & 0x1FFFFFFFu) - (1 << 28);

@@ -51,6 +51,13 @@ struct GemmCfg {
       kStages * kStageBytes + kStageOutBytes + kColBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// one output column's epilogue parameters: a single 16-byte broadcast load
+struct __align__(16) ColParam {
+  double sw;
+  int zw;
+  int cs;
+};
+
 struct GemmParams {
   int M, N, K;
   int seg_rows;    // rows per activation segment (video); params are per segment
@@ -90,10 +97,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + Cfg::kStages * Cfg::kABytes;
   uint8_t* smem_out = smem + Cfg::kStages * Cfg::kStageBytes;           // 1024-aligned
-  double* col_sw = reinterpret_cast<double*>(smem_out + Cfg::kStageOutBytes);  // [2][BN]
-  int* col_zw = reinterpret_cast<int*>(col_sw + 2 * BN);                      // [2][BN]
-  int* col_cs = col_zw + 2 * BN;                                               // [2][BN]
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(col_cs + 2 * BN);
+  ColParam* col = reinterpret_cast<ColParam*>(smem_out + Cfg::kStageOutBytes);  // [2][BN]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(col + 2 * BN);
   uint64_t* empty_bar = full_bar + Cfg::kStages;
   uint64_t* tfull_bar = empty_bar + Cfg::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -200,15 +205,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = (tile / p.num_n_tiles) * kBlockM;
       const int n0 = (tile % p.num_n_tiles) * BN;
       // per-tile column parameters -> smem (buffer `acc`; see the barrier note)
-      double* t_sw = col_sw + acc * BN;
-      int* t_zw = col_zw + acc * BN;
-      int* t_cs = col_cs + acc * BN;
+      ColParam* t_col = col + acc * BN;
       for (int i = et; i < BN; i += 32 * kEpiWarps) {
         const int n = n0 + i;
         const bool ok = n < p.N;
-        t_sw[i] = ok ? __ldg(p.sw + n) : 0.0;
-        t_zw[i] = ok ? __ldg(p.zw + n) : 0;
-        t_cs[i] = ok ? __ldg(p.colsum + n) : 0;
+        ColParam cp;
+        cp.sw = ok ? __ldg(p.sw + n) : 0.0;
+        cp.zw = ok ? __ldg(p.zw + n) : 0;
+        cp.cs = ok ? __ldg(p.colsum + n) : 0;
+        t_col[i] = cp;
       }
       // One barrier per tile: a warp can only refill this buffer two tiles
       // later, after every epilogue warp has passed the next tile's barrier.
@@ -259,25 +264,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) rv[j] = (nb + j < p.N) ? rp[j] : 0.f;
           }
         }
+        // y = f32(f64(sa*sw) * acc); int->f64 by a magic add on the FP64 pipe
+        // so only the final rounding uses the conversion (XU) pipe.
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int ci = c * 32 + j;
-          const int accv = (int)r[j] - t_zw[ci] * tr - za * t_cs[ci];
-          float y;
+          const ColParam cp = t_col[c * 32 + j];
+          const int accv = (int)r[j] - cp.zw * tr - za * cp.cs;
           if (MODE == QCB_EPI_ACC) {
-            y = __int_as_float(accv);
+            v[j] = __int_as_float(accv);
           } else {
-            const double joint = __dmul_rn(sa, t_sw[ci]);
-            y = __double2float_rn(__dmul_rn(joint, (double)accv));
+            v[j] = __double2float_rn(__dmul_rn(__dmul_rn(sa, cp.sw), i2d_alu(accv)));
+          }
+        }
+        if (MODE == QCB_EPI_GELU || MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
             if (MODE == QCB_EPI_GELU) {
-              y = gelu_f32_ref(y);
+              v[j] = gelu_f32_ref(v[j]);
             } else if (MODE == QCB_EPI_GATE_RESID) {
-              y = __fadd_rn(rv[j], __fmul_rn(gate, y));
-            } else if (MODE == QCB_EPI_RESID) {
-              y = __fadd_rn(rv[j], y);
+              v[j] = __fadd_rn(rv[j], __fmul_rn(gate, v[j]));
+            } else {
+              v[j] = __fadd_rn(rv[j], v[j]);
             }
           }
-          v[j] = y;
         }
         if (p.tma_store) {
           // 32x32 f32 slab -> 128B-swizzled smem -> one TMA bulk tensor store.

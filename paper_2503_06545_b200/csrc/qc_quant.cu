@@ -311,7 +311,7 @@ QC_DEV double v2_row_sum(double v, double* red_slot, int rowslot, int part) {
 // model.py:137-142 + modulation, via x * (1/sd) with an exact fallback.
 QC_DEV float ln_elem(float x, double mean, double sd, double rsd, double g, double b,
                      float scale1, float shift) {
-  const double xm = (double)x - mean;
+  const double xm = (double)(x) - mean;
   const double u = __dmul_rn(__dmul_rn(xm, rsd), g);
   const double v = __dadd_rn(u, b);
   double vv;
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, 
       for (int j = lt; j < K; j += TPR) {
         const float xv = active ? __ldg(xr + j) : 0.f;
         h[j] = xv;
-        s += (double)xv;
+        s += (double)(xv);
       }
       s = warp_sum(s);
       if (lane == 0) sm.red[warp] = s;
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, 
       const double mean = tot / K;
       double v = 0.0;
       for (int j = lt; j < K; j += TPR) {
-        const double d = (double)h[j] - mean;
+        const double d = (double)(h[j]) - mean;
         v += d * d;
       }
       v = warp_sum(v);
@@ -673,8 +673,8 @@ __global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, 
       const double sd = sqrt(vt / K + 1e-5);
       const double rsd = 1.0 / sd;
       for (int j = lt; j < K; j += TPR) {
-        const double g = p.ln_g ? (double)__ldg(p.ln_g + j) : 1.0;
-        const double bb = p.ln_b ? (double)__ldg(p.ln_b + j) : 0.0;
+        const double g = p.ln_g ? (double)(__ldg(p.ln_g + j)) : 1.0;
+        const double bb = p.ln_b ? (double)(__ldg(p.ln_b + j)) : 0.0;
         h[j] = ln_elem(h[j], mean, sd, rsd, g, bb, p.scale1, p.shift);
       }
     } else if (p.prologue == QCB_PRO_GELU) {
@@ -692,17 +692,18 @@ __global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, 
       if (c) {
         // balance + sign into f (f64), tail straight to the stash
         for (int e = lt; e < B; e += TPR) {
-          const float hv = h[e];
-          const double q = __dmul_rn((double)hv, __ldg(rc + e));
-          float y = f64_near_f32_tie(q) ? __double2float_rn(__ddiv_rn((double)hv, c[e]))
-                                        : __double2float_rn(q);
-          y = __uint_as_float(__float_as_uint(y) ^ (__ldg(sgb + e) & 0x80000000u));
-          f[v3_pad(e)] = (double)y;
+          const double hd = (double)(h[e]);
+          const double q = __dmul_rn(hd, __ldg(rc + e));
+          // y = f32(h / c) held exactly in f64 (24-bit rounding on the ALU)
+          const double y = f64_near_f32_tie(q) ? (double)__double2float_rn(__ddiv_rn(hd, c[e]))
+                                               : d_round24(q);
+          f[v3_pad(e)] = __longlong_as_double(
+              __double_as_longlong(y) ^ ((long long)(__ldg(sgb + e) & 0x80000000u) << 32));
         }
         for (int t = lt; t < T; t += TPR) {
-          const float hv = h[B + t];
-          const double q = __dmul_rn((double)hv, __ldg(rc + B + t));
-          const float y = f64_near_f32_tie(q) ? __double2float_rn(__ddiv_rn((double)hv, c[B + t]))
+          const double hd = (double)(h[B + t]);
+          const double q = __dmul_rn(hd, __ldg(rc + B + t));
+          const float y = f64_near_f32_tie(q) ? __double2float_rn(__ddiv_rn(hd, c[B + t]))
                                               : __double2float_rn(q);
           lo = fminf(lo, y);
           hi = fmaxf(hi, y);
@@ -769,57 +770,362 @@ __global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, 
   if (cur_seg >= 0) flush(cur_seg);
 }
 
+// ------------------------------------------------------------------ v4 pass 1
+// Streaming register-first FWHT.  Each of the R = 4096 / b row slots of a CTA
+// is served by TPR = b / 16 threads and walks its own sequence of rows; the
+// slot's next two rows are in flight as 1-D bulk async copies (TMA engine)
+// into a double-buffered shared-memory row, so HBM reads overlap the FP64
+// work.  Row slots synchronise only among themselves (named barriers).
+// Thread lt of a slot owns, per radix-16 stage:
+//   stage A (bits NB-4..NB-1): e = lt + TPR j           (from the smem row)
+//   stage B (bits 0..3):       e = 16 lt + j
+//   stage C (bits 4..NB-5):    e = (lt & 15) + 16 jj + 16 GS top,
+//                              top = (lt >> 4) + (TPR / 16) g
+// so every shared access is lane-consecutive (conflict-free) and the final
+// registers store coalesced runs of xe.  Element e lives at f[e + (e >> 4)].
+constexpr int kV4Threads = 256;
+constexpr int kV4Tail = 4;   // max tail elements (K - b) per thread
+
+template <int B>
+struct V4Smem {
+  static constexpr int R = 4096 / B;
+  static constexpr int kRowMax = B + kV4Tail * (B / 16);
+  float xrow[R][2][kRowMax];      // double-buffered input rows (bulk copies)
+  double f[R][B + B / 16];        // FWHT work row
+  uint64_t full[R][2];            // bulk-copy completion barriers
+  double red[2][kV4Threads / 32]; // LN partial sums (mean, variance)
+  uint32_t smask[3][kV4Threads];  // sign bits of the thread's 16 stage-A elements
+  float run_mn[3][kV4Threads];    // per-thread running min / max per output
+  float run_mx[3][kV4Threads];
+};
+
+// Radix-2^Q butterflies over groups of 2^Q consecutive registers.
+template <int Q>
+QC_DEV void fwht_regs(double (&v)[16]) {
+#pragma unroll
+  for (int hs = 1; hs < (1 << Q); hs <<= 1)
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if ((j & hs) == 0) {
+        const double u = v[j], w = v[j + hs];
+        v[j] = u + w;
+        v[j + hs] = u - w;
+      }
+}
+
+QC_DEV double flip_sign(double x, uint32_t bit) {
+  return __longlong_as_double(__double_as_longlong(x) ^ ((long long)bit << 63));
+}
+
+template <int B, bool kPow2Scale>
+__global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams p, const AQ2 a) {
+  constexpr int R = 4096 / B;               // row slots per CTA
+  constexpr int TPR = B / 16;               // threads per row slot
+  constexpr int WPR = TPR / 32;             // warps per row slot (>= 2)
+  constexpr int NB = (B == 1024) ? 10 : (B == 2048 ? 11 : 12);
+  constexpr int Q = NB - 8;                 // bits of stage C
+  constexpr int GS = 1 << Q;                // stage-C group size
+  constexpr int G = 16 / GS;                // stage-C groups per thread
+  constexpr int SA = 17 * TPR / 16;         // stage-A smem stride
+  extern __shared__ __align__(128) uint8_t v4_smem[];
+  V4Smem<B>& sm = *reinterpret_cast<V4Smem<B>*>(v4_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rl = tid / TPR, lt = tid % TPR;
+  const int K = p.K, T = K - B;
+  const uint32_t row_bytes = (uint32_t)K * 4u;
+  double* const fa = sm.f[rl] + lt + (lt >> 4);
+  double* const fb = sm.f[rl] + 17 * lt;
+  double* const fc = sm.f[rl] + (lt & 15) + 17 * GS * (lt >> 4);
+  auto row_sync = [&]() { named_bar_sync(1 + rl, TPR); };
+
+  for (int o = 0; o < 3; ++o) {
+    uint32_t m = 0;
+    if (o < p.n_out && p.c[o]) {
+      const uint32_t* sg = reinterpret_cast<const uint32_t*>(p.signs[o]) + lt;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) m |= (__ldg(sg + TPR * j) >> 31) << j;
+    }
+    sm.smask[o][tid] = m;
+    sm.run_mn[o][tid] = INFINITY;
+    sm.run_mx[o][tid] = -INFINITY;
+  }
+  // the slot's k-th row
+  const int stride_rows = gridDim.x * R;
+  auto row_of = [&](int k) { return blockIdx.x * R + k * stride_rows + rl; };
+  auto issue = [&](int k) {   // lt == 0 only
+    const int gr = row_of(k);
+    if (gr >= a.total_rows) return;
+    int seg, mrow;
+    long long in_row, out_row;
+    v2_row_index(p, gr, seg, mrow, in_row, out_row);
+    mbar_arrive_expect_tx(&sm.full[rl][k & 1], row_bytes);
+    bulk_load(sm.xrow[rl][k & 1], p.x + in_row * p.ldx, row_bytes, &sm.full[rl][k & 1]);
+  };
+  if (lt == 0) {
+    mbar_init(&sm.full[rl][0], 1);
+    mbar_init(&sm.full[rl][1], 1);
+    fence_barrier_init();
+    issue(0);
+    issue(1);
+  }
+  __syncthreads();
+
+  auto flush = [&](int seg) {   // warp-level: running min/max -> the segment's keys
+    for (int o = 0; o < p.n_out; ++o) {
+      float lo = sm.run_mn[o][tid], hi = sm.run_mx[o][tid];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+      }
+      if (lane == 0 && hi >= lo) {
+        uint32_t* k = p.keys + ((size_t)o * p.nseg + seg) * 2;
+        atomicMin(&k[0], f2key(lo));
+        atomicMax(&k[1], f2key(hi));
+      }
+      sm.run_mn[o][tid] = INFINITY;
+      sm.run_mx[o][tid] = -INFINITY;
+    }
+  };
+  auto slot_sum = [&](double v, double* red) {   // sum over the slot's warps
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    row_sync();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) t += red[rl * WPR + w];
+    return t;
+  };
+
+  int cur_seg = -1;
+  for (int k = 0;; ++k) {
+    const int gr = row_of(k);
+    if (gr >= a.total_rows) break;   // uniform per slot
+    int seg, mrow;
+    long long in_row, out_row;
+    v2_row_index(p, gr, seg, mrow, in_row, out_row);
+    if (seg != cur_seg) {
+      if (cur_seg >= 0) flush(cur_seg);
+      cur_seg = seg;
+    }
+    // ---- row from shared memory + prologue, in registers
+    mbar_wait(&sm.full[rl][k & 1], (k >> 1) & 1);
+    const float* xs = sm.xrow[rl][k & 1];
+    float h[16], ht[kV4Tail];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) h[j] = xs[lt + TPR * j];
+#pragma unroll
+    for (int i = 0; i < kV4Tail; ++i) {
+      const int t = lt + TPR * i;
+      ht[i] = (t < T) ? xs[B + t] : 0.f;
+    }
+    if (p.prologue == QCB_PRO_LN_MOD) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) s += (double)h[j];
+#pragma unroll
+      for (int i = 0; i < kV4Tail; ++i) s += (double)ht[i];
+      const double mean = slot_sum(s, sm.red[0]) / K;
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double d = (double)h[j] - mean;
+        v += d * d;
+      }
+#pragma unroll
+      for (int i = 0; i < kV4Tail; ++i) {
+        if (lt + TPR * i < T) {
+          const double d = (double)ht[i] - mean;
+          v += d * d;
+        }
+      }
+      const double vt = slot_sum(v, sm.red[1]);
+      const double sd = sqrt(vt / K + 1e-5);
+      const double rsd = 1.0 / sd;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = lt + TPR * j;
+        const double g = p.ln_g ? (double)__ldg(p.ln_g + col) : 1.0;
+        const double bb = p.ln_b ? (double)__ldg(p.ln_b + col) : 0.0;
+        h[j] = ln_elem(h[j], mean, sd, rsd, g, bb, p.scale1, p.shift);
+      }
+#pragma unroll
+      for (int i = 0; i < kV4Tail; ++i) {
+        const int t = lt + TPR * i;
+        if (t < T) {
+          const double g = p.ln_g ? (double)__ldg(p.ln_g + B + t) : 1.0;
+          const double bb = p.ln_b ? (double)__ldg(p.ln_b + B + t) : 0.0;
+          ht[i] = ln_elem(ht[i], mean, sd, rsd, g, bb, p.scale1, p.shift);
+        }
+      }
+    } else if (p.prologue == QCB_PRO_GELU) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) h[j] = gelu_f32_ref(h[j]);
+#pragma unroll
+      for (int i = 0; i < kV4Tail; ++i) ht[i] = gelu_f32_ref(ht[i]);
+    }
+    // every thread of the slot has read the smem row: refill it with row k+2
+    row_sync();
+    if (lt == 0) issue(k + 2);
+
+    for (int o = 0; o < p.n_out; ++o) {
+      const double* c = p.c[o];
+      float* so = a.stash[o] + out_row * a.ld_stash;
+      float lo = INFINITY, hi = -INFINITY;
+      if (c) {
+        const double* rc = a.rc[o];
+        const uint32_t sgm = sm.smask[o][tid];
+        // ---- balance (exact f32(h / c), held in f64) + sign, stage A
+        double v[16];
+        bool slow = false;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const double q = __dmul_rn((double)h[j], __ldg(rc + lt + TPR * j));
+          slow |= f64_near_f32_tie(q);
+          v[j] = flip_sign(d_round24(q), (sgm >> j) & 1u);
+        }
+        if (slow) {   // exact IEEE division next to an f32 rounding boundary (rare)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const double hd = (double)h[j];
+            const int col = lt + TPR * j;
+            if (f64_near_f32_tie(__dmul_rn(hd, __ldg(rc + col))))
+              v[j] = flip_sign((double)__double2float_rn(__ddiv_rn(hd, c[col])), (sgm >> j) & 1u);
+          }
+        }
+        fwht_regs<4>(v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) fa[SA * j] = v[j];
+        // tail (unrotated): y = f32(h / c) straight to the stash
+#pragma unroll
+        for (int i = 0; i < kV4Tail; ++i) {
+          const int t = lt + TPR * i;
+          if (t < T) {
+            const double hd = (double)ht[i];
+            const double q = __dmul_rn(hd, __ldg(rc + B + t));
+            const float y = f64_near_f32_tie(q) ? __double2float_rn(__ddiv_rn(hd, c[B + t]))
+                                                : __double2float_rn(q);
+            lo = fminf(lo, y);
+            hi = fmaxf(hi, y);
+            so[B + t] = y;
+          }
+        }
+        row_sync();
+        // ---- stage B (bits 0..3), in place
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = fb[j];
+        fwht_regs<4>(v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) fb[j] = v[j];
+        row_sync();
+        // ---- stage C (bits 4..NB-5) -> scale, min/max, stash
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int jj = 0; jj < GS; ++jj) v[g * GS + jj] = fc[g * (TPR / 16) * 17 * GS + 17 * jj];
+        fwht_regs<Q>(v);
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int jj = 0; jj < GS; ++jj) {
+            const double vv = v[g * GS + jj];
+            const float xe = kPow2Scale ? __fmul_rn(__double2float_rn(vv), p.rscale)
+                                        : __double2float_rn(__dmul_rn(vv, (double)p.rscale));
+            lo = fminf(lo, xe);
+            hi = fmaxf(hi, xe);
+            const int e = (lt & 15) + 16 * jj + 16 * GS * ((lt >> 4) + (TPR / 16) * g);
+            so[e] = xe;
+          }
+        row_sync();   // f is rewritten by the next output / row
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          lo = fminf(lo, h[j]);
+          hi = fmaxf(hi, h[j]);
+          so[lt + TPR * j] = h[j];
+        }
+#pragma unroll
+        for (int i = 0; i < kV4Tail; ++i) {
+          const int t = lt + TPR * i;
+          if (t < T) {
+            lo = fminf(lo, ht[i]);
+            hi = fmaxf(hi, ht[i]);
+            so[B + t] = ht[i];
+          }
+        }
+      }
+      sm.run_mn[o][tid] = fminf(sm.run_mn[o][tid], lo);
+      sm.run_mx[o][tid] = fmaxf(sm.run_mx[o][tid], hi);
+    }
+  }
+  if (cur_seg >= 0) flush(cur_seg);
+}
+
 // Pass 2: codes (+ optional dequantized copy) from the f32 stash; warp per row.
+// Each lane keeps kP2Batch 16-byte loads in flight; the per-segment (s, z)
+// derivation (two f64 divisions) is cached per warp in shared memory.
+constexpr int kP2Batch = 4;
+
 __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, const AQ2 a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.K;
   const double top = (double)((1 << p.bits) - 1);
+  __shared__ int c_seg[kV2Threads / 32][3];
+  __shared__ double c_s[kV2Threads / 32][3];
+  __shared__ double c_z[kV2Threads / 32][3];
+  if (lane < 3) c_seg[warp][lane] = -1;
+  __syncwarp();
   for (int gr = blockIdx.x * 4 + warp; gr < a.total_rows; gr += gridDim.x * 4) {
     int seg, mrow;
     long long in_row, out_row;
     v2_row_index(p, gr, seg, mrow, in_row, out_row);
     for (int o = 0; o < p.n_out; ++o) {
-      const uint32_t* k = p.keys + ((size_t)o * p.nseg + seg) * 2;
-      const double lo = (double)key2f(k[0]), hi = (double)key2f(k[1]);
-      const double span = hi - lo;
       double s, z;
-      if (span <= 0.0) {
-        s = 1.0;
-        z = 0.0;
+      if (c_seg[warp][o] == seg) {
+        s = c_s[warp][o];
+        z = c_z[warp][o];
       } else {
-        s = scale_up16(__ddiv_rn(span, top));
-        z = fmin(fmax(rha(__ddiv_rn(-lo, s)), 0.0), top);
-      }
-      if (mrow == 0 && lane == 0) {
-        p.scale[o][seg] = s;
-        p.zero[o][seg] = (int)z;
+        const uint32_t* k = p.keys + ((size_t)o * p.nseg + seg) * 2;
+        const double lo = (double)key2f(k[0]), hi = (double)key2f(k[1]);
+        const double span = hi - lo;
+        if (span <= 0.0) {
+          s = 1.0;
+          z = 0.0;
+        } else {
+          s = scale_up16(__ddiv_rn(span, top));
+          z = fmin(fmax(rha(__ddiv_rn(-lo, s)), 0.0), top);
+        }
+        // every warp serving the segment writes the same values
+        if (lane == 0) {
+          p.scale[o][seg] = s;
+          p.zero[o][seg] = (int)z;
+          c_s[warp][o] = s;
+          c_z[warp][o] = z;
+          c_seg[warp][o] = seg;
+        }
+        __syncwarp();
       }
       const float inv_sf = (float)(1.0 / s);
       const float zf = (float)z, topf = (float)top;
+      const int zi = (int)z;
       const float* xr = a.stash[o] + out_row * a.ld_stash;
       uint8_t* cr = p.codes[o] ? p.codes[o] + out_row * p.ldc : nullptr;
       float* dr = p.deq_out[o] ? p.deq_out[o] + out_row * p.ldxe : nullptr;
       int rs = 0;
-      for (int j = lane * 4; j < K; j += 128) {
-        float v4[4];
-        if (j + 3 < K) {
-          const float4 t4 = *reinterpret_cast<const float4*>(xr + j);
-          v4[0] = t4.x; v4[1] = t4.y; v4[2] = t4.z; v4[3] = t4.w;
-        } else {
-          for (int e = 0; e < 4; ++e) v4[e] = (j + e < K) ? xr[j + e] : 0.f;
-        }
+      auto proc = [&](int j, const float4 t4) {
+        const float v4[4] = {t4.x, t4.y, t4.z, t4.w};
         uint32_t packed = 0;
         int code[4];
         bool slow = false;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {   // f32 estimate of rha(xe/s), branch-free
+          // magic-number rounding (FP32 pipe) instead of FRND/F2I on the XU pipe
           const float qf = __fmul_rn(v4[e], inv_sf);
-          const float t = __fadd_rn(fabsf(qf), 0.5f);
-          const float n = floorf(t);
-          const float fr = t - n;
-          slow |= (fr < 0x1p-12f) || (fr > 1.0f - 0x1p-12f);
+          const float aq = fabsf(qf);
+          const float n = __fsub_rn(__fadd_rn(aq, 12582912.0f), 12582912.0f);  // rint, aq < 2^22
+          slow |= fabsf(__fsub_rn(aq, n)) > 0.5f - 0x1p-12f;                   // near a .5 tie
           const float v = fminf(fmaxf(__fadd_rn(qf < 0.0f ? -n : n, zf), 0.0f), topf);
-          code[e] = (int)v;
+          code[e] = __float_as_int(__fadd_rn(v, 8388608.0f)) - 0x4B000000;    // (int)v in [0, 255]
         }
         if (slow) {
 #pragma unroll
@@ -830,7 +1136,7 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, 
           if (j + e < K) {
             rs += code[e];
             packed |= (uint32_t)code[e] << (8 * e);
-            if (dr) dr[j + e] = __double2float_rn(__dmul_rn(s, (double)(code[e] - (int)z)));
+            if (dr) dr[j + e] = __double2float_rn(__dmul_rn(s, i2d_alu(code[e] - zi)));
           }
         }
         if (cr) {
@@ -838,6 +1144,24 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, 
           else
             for (int e = 0; e < 4 && j + e < K; ++e) cr[j + e] = (uint8_t)(packed >> (8 * e));
         }
+      };
+      for (int j0 = lane * 4; j0 < K; j0 += 128 * kP2Batch) {
+        float4 v[kP2Batch];
+#pragma unroll
+        for (int b = 0; b < kP2Batch; ++b) {
+          const int j = j0 + 128 * b;
+          if (j + 3 < K) {
+            v[b] = __ldcs(reinterpret_cast<const float4*>(xr + j));
+          } else {
+            v[b].x = (j < K) ? xr[j] : 0.f;
+            v[b].y = (j + 1 < K) ? xr[j + 1] : 0.f;
+            v[b].z = (j + 2 < K) ? xr[j + 2] : 0.f;
+            v[b].w = 0.f;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kP2Batch; ++b)
+          if (j0 + 128 * b < K) proc(j0 + 128 * b, v[b]);
       }
       rs = warp_sum(rs);
       if (lane == 0 && cr) p.rowsum[o][out_row] = rs;
@@ -931,10 +1255,29 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     // pass 1: CTA shared-memory FWHT (v3); 1/sqrt(b) is a power of two for b = 1024, 4096
     (void)blocks;
     static bool at1 = false, at2 = false, at4 = false;
+    static bool a41 = false, a42 = false, a44 = false;
     const int rows_per_cta = 4096 / b;
     int b1 = (a.total_rows + rows_per_cta - 1) / rows_per_cta;
     if (b1 > num_sms() * 3) b1 = num_sms() * 3;
-    switch (b) {
+    // v4 (register-first FWHT): 16-byte aligned rows and reciprocals, short tail
+    const bool v4 = (q->K - b) <= kV4Tail * (b / 16) &&
+                    (reinterpret_cast<uintptr_t>(q->x) & 15) == 0;
+    if (v4) {
+      switch (b) {
+        case 1024:
+          allow_max_smem(aq4_pass1<1024, true>, a41);
+          aq4_pass1<1024, true><<<b1, kV4Threads, sizeof(V4Smem<1024>), st>>>(p, a);
+          break;
+        case 2048:
+          allow_max_smem(aq4_pass1<2048, false>, a42);
+          aq4_pass1<2048, false><<<b1, kV4Threads, sizeof(V4Smem<2048>), st>>>(p, a);
+          break;
+        default:
+          allow_max_smem(aq4_pass1<4096, true>, a44);
+          aq4_pass1<4096, true><<<b1, kV4Threads, sizeof(V4Smem<4096>), st>>>(p, a);
+          break;
+      }
+    } else switch (b) {
       case 1024:
         allow_max_smem(aq3_pass1<1024, true>, at1);
         aq3_pass1<1024, true><<<b1, kV3Threads, sizeof(V3Smem<1024>), st>>>(p, a);
@@ -949,7 +1292,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
         break;
     }
     int b2 = (a.total_rows + 3) / 4;
-    if (b2 > cap) b2 = cap;
+    if (b2 > num_sms() * 16) b2 = num_sms() * 16;
     aq2_pass2<<<b2, kV2Threads, 0, st>>>(p, a);
     if (q->xe_out[0] && q->ldxe != q->K) return QCB_ERR_DIM;  // debug copy layout unsupported
     return launch_status();
