@@ -141,7 +141,9 @@ typedef struct QcbActQuant {
   long long ldxe;
   float* deq_out[3];         /* nullable: f32(s*(code-z)) fake-quant outputs     */
   void* workspace;           /* qcb_act_quant_workspace_bytes(...) bytes         */
-  const double* chan_recip[3]; /* nullable: 1/chan_scale (else computed per call) */
+  const double* chan_recip[3]; /* nullable: signed reciprocals s_j/c_j (j < b) and   */
+                               /* 1/c_j (j >= b), as qcb_weight_prep writes them;    */
+                               /* else computed per call                             */
 } QcbActQuant;
 
 int qcb_act_quant(const QcbActQuant* q, void* stream);
@@ -160,7 +162,7 @@ typedef struct QcbWeightPrep {
   int* colsum;               /* [N]                                              */
   float* w_eff;              /* nullable [K][N]: rotated weights                 */
   float* w_deq;              /* nullable [K][N]: dequantized weights             */
-  double* chan_recip_out;    /* nullable [K]: 1/chan_scale for qcb_act_quant     */
+  double* chan_recip_out;    /* nullable [K]: signed reciprocals for act_quant    */
 } QcbWeightPrep;
 
 int qcb_weight_prep(const QcbWeightPrep* q, void* stream);

@@ -85,6 +85,29 @@ QC_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
       : "memory");
 }
 
+// L2 eviction-priority policies (createpolicy) and hinted accesses
+QC_DEV uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+QC_DEV uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+QC_DEV void st_f32_hint(float* a, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+QC_DEV void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                           uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 QC_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 QC_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 QC_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -327,6 +350,26 @@ QC_DEV double d_round24(double d) {
   unsigned long long u = (unsigned long long)__double_as_longlong(d);
   u += 0x0FFFFFFFull + ((u >> 29) & 1ull);
   u &= ~0x1FFFFFFFull;
+  return __longlong_as_double((long long)u);
+}
+
+// Branch-free companion of d_round24_fast: 1 when q is within 64 ulp64 of an
+// f32 rounding tie or outside the f32 normal range (zero is safe), i.e. when
+// an estimate of q may round to f32 differently from the exact value.
+QC_DEV uint32_t f32_round_risk(double q) {
+  const uint32_t lo = (uint32_t)__double2loint(q), hi = (uint32_t)__double2hiint(q);
+  const uint32_t ex = (hi >> 20) & 0x7FFu;
+  const bool nonzero = ((hi & 0x7FFFFFFFu) | lo) != 0u;
+  const bool range = (ex - (1023u - 125u)) > 251u;                // ex - 1023 outside [-125, 126]
+  const bool tie = ((lo & 0x1FFFFFFFu) - ((1u << 28) - 63u)) < 127u;  // |t - 2^28| < 64
+  return (uint32_t)(nonzero & (range | tie));
+}
+
+// q rounded to a 24-bit significand by round-half-up on the magnitude: equal
+// to (double)(float)q whenever f32_round_risk(q) == 0 (ties never reach it).
+QC_DEV double d_round24_fast(double q) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(q);
+  u = (u + 0x10000000ull) & ~0x1FFFFFFFull;
   return __longlong_as_double((long long)u);
 }
 

@@ -169,9 +169,122 @@ __global__ void __launch_bounds__(256) gemm_f64_big_k(const GemmF64P P) {
   }
 }
 
+// Pipelined large-tile variant (16-byte aligned operands, K % 16 == 0): k tile
+// 16, double-buffered f64 shared tiles, the next tile's global data prefetched
+// into registers (two 16-byte loads per operand per thread) while the current
+// one feeds the DFMA chains; one barrier per k tile.
+constexpr int kPK = 16;
+
+struct F64PipeSmem {
+  double As[2][kPK][kBT];
+  double Ws[2][kPK][kBT];
+};
+
+__global__ void __launch_bounds__(256, 1) gemm_f64_pipe_k(const GemmF64P P) {
+  const QcbGemmF64& g = P.g;
+  extern __shared__ __align__(16) uint8_t f64_smem[];
+  F64PipeSmem& sm = *reinterpret_cast<F64PipeSmem*>(f64_smem);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * kBT, n0 = blockIdx.x * kBT;
+  const int seg_rows = g.seg_rows > 0 ? g.seg_rows : g.M;
+  const int seg_valid = g.seg_valid > 0 ? g.seg_valid : seg_rows;
+  // this thread's two A rows (fixed over k) and two W (k, n-quad) slots
+  const float* arow[2];
+  int akq[2], wk[2], wn[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int idx = tid + 256 * l;   // 0..511
+    const int mm = idx >> 2, m = m0 + mm;
+    akq[l] = idx & 3;
+    arow[l] = nullptr;
+    if (m < g.M) {
+      const int seg = m / seg_rows, r = m - seg * seg_rows;
+      const long long row = g.a_row0 ? g.a_row0[seg] + r : (long long)m;
+      if (r < seg_valid) arow[l] = g.a + row * g.lda;
+    }
+    wk[l] = idx >> 5;
+    wn[l] = n0 + 4 * (idx & 31);
+  }
+  float4 pa[2], pw[2];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      pa[l] = arow[l] ? __ldg(reinterpret_cast<const float4*>(arow[l] + k0 + 4 * akq[l]))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      pw[l] = (wn[l] < g.N)
+                  ? __ldg(reinterpret_cast<const float4*>(g.w + (long long)(k0 + wk[l]) * g.ldw + wn[l]))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const int idx = tid + 256 * l, mm = idx >> 2, kb = 4 * akq[l];
+      sm.As[buf][kb + 0][mm] = (double)pa[l].x;
+      sm.As[buf][kb + 1][mm] = (double)pa[l].y;
+      sm.As[buf][kb + 2][mm] = (double)pa[l].z;
+      sm.As[buf][kb + 3][mm] = (double)pa[l].w;
+      double* wr = &sm.Ws[buf][wk[l]][4 * (idx & 31)];
+      wr[0] = (double)pw[l].x;
+      wr[1] = (double)pw[l].y;
+      wr[2] = (double)pw[l].z;
+      wr[3] = (double)pw[l].w;
+    }
+  };
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  const int nk = g.K / kPK;
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) fetch((t + 1) * kPK);
+#pragma unroll
+    for (int kk = 0; kk < kPK; ++kk) {
+      double a[8], w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = sm.As[buf][kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = sm.Ws[buf][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], w[j], acc[i][j]);
+    }
+    if (t + 1 < nk) stash(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + ty + 16 * i;
+    if (m >= g.M) continue;
+    const int seg = m / seg_rows, r = m - seg * seg_rows;
+    if (r >= seg_valid) continue;
+    const long long orow = g.out_row0 ? g.out_row0[seg] + r : (long long)m;
+    const long long rrow = g.resid_row0 ? g.resid_row0[seg] + r : (long long)m;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + tx + 16 * j;
+      if (n < g.N) g.out[orow * g.ldo + n] = f64_epilogue(g, acc[i][j], rrow, n);
+    }
+  }
+}
+
 int gemm_f64_launch(const QcbGemmF64* g, cudaStream_t st) {
   GemmF64P P{*g};
-  if ((long long)g->M * g->N >= 256LL * 1024) {   // enough tiles for the big variant
+  const bool aligned = g->K % kPK == 0 && g->N % 4 == 0 && g->lda % 4 == 0 && g->ldw % 4 == 0 &&
+                       (reinterpret_cast<uintptr_t>(g->a) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(g->w) & 15) == 0;
+  if ((long long)g->M * g->N >= 256LL * 1024 && aligned) {
+    static bool attr = false;
+    allow_max_smem(gemm_f64_pipe_k, attr);
+    dim3 grid((g->N + kBT - 1) / kBT, (g->M + kBT - 1) / kBT);
+    gemm_f64_pipe_k<<<grid, 256, sizeof(F64PipeSmem), st>>>(P);
+  } else if ((long long)g->M * g->N >= 256LL * 1024) {   // enough tiles for the big variant
     dim3 grid((g->N + kBT - 1) / kBT, (g->M + kBT - 1) / kBT);
     gemm_f64_big_k<<<grid, 256, 0, st>>>(P);
   } else {

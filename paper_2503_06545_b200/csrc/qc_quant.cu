@@ -271,7 +271,7 @@ QC_DEV int code_of(float xe, float inv_sf, double s, float z, float top) {
 }
 
 struct AQ2 {
-  const double* rc[3];  // 1 / chan_scale
+  const double* rc[3];  // 1 / chan_scale (v4: rotation signs folded in, see recip_k)
   float* stash[3];      // xe [nseg*seg_rows][K]
   long long ld_stash;
   int total_rows;       // nseg * seg_valid
@@ -309,18 +309,43 @@ QC_DEV double v2_row_sum(double v, double* red_slot, int rowslot, int part) {
 
 // f32(f32(((x - mean) / sd) * g + b) * scale1 + shift), the LN prologue of
 // model.py:137-142 + modulation, via x * (1/sd) with an exact fallback.
-QC_DEV float ln_elem(float x, double mean, double sd, double rsd, double g, double b,
-                     float scale1, float shift) {
-  const double xm = (double)(x) - mean;
+// w = u + b with u = xm * (1/sd) * g carrying a few ulp64(u) of error against
+// the reference's (xm / sd) * g: w's f32 rounding is certain unless w lies
+// within 64 (1 + |u| / |w|) ulp64(w) of an f32 tie (covers cancellation
+// without a separate test; w == 0 and the f32 range edges always qualify).
+QC_DEV bool ln_near_tie(double w, double u) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(w);
+  const int ex = (int)((bits >> 52) & 0x7FF) - 1023;
+  if (ex < -125 || ex > 126) return true;
+  const int d = (int)((unsigned)bits & 0x1FFFFFFFu) - (1 << 28);
+  return fabs(i2d_alu(d)) * fabs(w) < 64.0 * (fabs(w) + fabs(u));
+}
+
+// rare exact paths, kept out of line so they cost no registers in the hot loops
+__device__ __noinline__ float ln_exact(double xm, double sd, double g, double b, float scale1,
+                                       float shift) {
+  const double vv = __dadd_rn(__dmul_rn(__ddiv_rn(xm, sd), g), b);
+  return __fadd_rn(__fmul_rn(__double2float_rn(vv), scale1), shift);
+}
+__device__ __noinline__ double div_exact_f32(double hd, double c) {
+  return (double)__double2float_rn(__ddiv_rn(hd, c));
+}
+
+QC_DEV float ln_from_xm(double xm, double sd, double rsd, double g, double b, float scale1,
+                        float shift) {
   const double u = __dmul_rn(__dmul_rn(xm, rsd), g);
   const double v = __dadd_rn(u, b);
   double vv;
-  if (fabs(u) <= 4.0 * fabs(v) && !f64_near_f32_tie(v)) {
+  if (!ln_near_tie(v, u)) {
     vv = v;
   } else {
     vv = __dadd_rn(__dmul_rn(__ddiv_rn(xm, sd), g), b);
   }
   return __fadd_rn(__fmul_rn(__double2float_rn(vv), scale1), shift);
+}
+QC_DEV float ln_elem(float x, double mean, double sd, double rsd, double g, double b,
+                     float scale1, float shift) {
+  return ln_from_xm((double)x - mean, sd, rsd, g, b, scale1, shift);
 }
 
 template <int WPR, bool kPow2Scale>
@@ -410,7 +435,7 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass1(const ActQuantParams p, 
           const double bb = p.ln_b ? (double)__ldg(p.ln_b + col) : 0.0;
           const double u = __dmul_rn(__dmul_rn((double)xv[r] - mean, rsd), g);
           const double v = __dadd_rn(u, bb);
-          slow |= (uint32_t)(!(fabs(u) <= 4.0 * fabs(v)) || f64_near_f32_tie(v)) << r;
+          slow |= (uint32_t)ln_near_tie(v, u) << r;
           hb[lane + 32 * r] = __fadd_rn(__fmul_rn(__double2float_rn(v), p.scale1), p.shift);
         }
         if (__any_sync(0xffffffffu, slow != 0)) {
@@ -837,6 +862,15 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
   double* const fb = sm.f[rl] + 17 * lt;
   double* const fc = sm.f[rl] + (lt & 15) + 17 * GS * (lt >> 4);
   auto row_sync = [&]() { named_bar_sync(1 + rl, TPR); };
+  // LN affine parameters as f64, once per CTA (dynamic tail of the smem block)
+  double* const ln_g64 = reinterpret_cast<double*>(v4_smem + sizeof(V4Smem<B>));
+  double* const ln_b64 = ln_g64 + K;
+  if (p.prologue == QCB_PRO_LN_MOD) {
+    for (int i = tid; i < K; i += kV4Threads) {
+      ln_g64[i] = p.ln_g ? (double)p.ln_g[i] : 1.0;
+      ln_b64[i] = p.ln_b ? (double)p.ln_b[i] : 0.0;
+    }
+  }
 
   for (int o = 0; o < 3; ++o) {
     uint32_t m = 0;
@@ -849,6 +883,10 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
     sm.run_mn[o][tid] = INFINITY;
     sm.run_mx[o][tid] = -INFINITY;
   }
+  // input rows stream through L2 (evict first); the stash should survive in L2
+  // until pass 2 reads it (evict last)
+  const uint64_t pol_stream = l2_policy_evict_first();
+  const uint64_t pol_keep = l2_policy_evict_last();
   // the slot's k-th row
   const int stride_rows = gridDim.x * R;
   auto row_of = [&](int k) { return blockIdx.x * R + k * stride_rows + rl; };
@@ -859,7 +897,8 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
     long long in_row, out_row;
     v2_row_index(p, gr, seg, mrow, in_row, out_row);
     mbar_arrive_expect_tx(&sm.full[rl][k & 1], row_bytes);
-    bulk_load(sm.xrow[rl][k & 1], p.x + in_row * p.ldx, row_bytes, &sm.full[rl][k & 1]);
+    bulk_load_hint(sm.xrow[rl][k & 1], p.x + in_row * p.ldx, row_bytes, &sm.full[rl][k & 1],
+                   pol_stream);
   };
   if (lt == 0) {
     mbar_init(&sm.full[rl][0], 1);
@@ -920,18 +959,26 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
       ht[i] = (t < T) ? xs[B + t] : 0.f;
     }
     if (p.prologue == QCB_PRO_LN_MOD) {
-      double s = 0.0;
+      double s0 = 0.0, s1 = 0.0;   // two chains
 #pragma unroll
-      for (int j = 0; j < 16; ++j) s += (double)h[j];
+      for (int i = 0; i < 8; ++i) {
+        s0 += (double)h[2 * i];
+        s1 += (double)h[2 * i + 1];
+      }
+      double s = s0 + s1;
 #pragma unroll
       for (int i = 0; i < kV4Tail; ++i) s += (double)ht[i];
       const double mean = slot_sum(s, sm.red[0]) / K;
-      double v = 0.0;
+      double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double d = (double)h[j] - mean;
-        v += d * d;
+      for (int i = 0; i < 8; ++i) {   // x - mean parked in the thread's own stage-A slots
+        const double d0 = (double)h[2 * i] - mean, d1 = (double)h[2 * i + 1] - mean;
+        fa[SA * (2 * i)] = d0;
+        fa[SA * (2 * i + 1)] = d1;
+        v0 += d0 * d0;
+        v1 += d1 * d1;
       }
+      double v = v0 + v1;
 #pragma unroll
       for (int i = 0; i < kV4Tail; ++i) {
         if (lt + TPR * i < T) {
@@ -942,21 +989,31 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
       const double vt = slot_sum(v, sm.red[1]);
       const double sd = sqrt(vt / K + 1e-5);
       const double rsd = 1.0 / sd;
+      // fast path x*(1/sd) for all 16, one sticky flag; exact division only
+      // for elements next to an f32 tie or with cancellation (ln_from_xm)
+      uint32_t lslow = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int col = lt + TPR * j;
-        const double g = p.ln_g ? (double)__ldg(p.ln_g + col) : 1.0;
-        const double bb = p.ln_b ? (double)__ldg(p.ln_b + col) : 0.0;
-        h[j] = ln_elem(h[j], mean, sd, rsd, g, bb, p.scale1, p.shift);
+        const double u = __dmul_rn(__dmul_rn(fa[SA * j], rsd), ln_g64[col]);
+        const double w = __dadd_rn(u, ln_b64[col]);
+        lslow |= (uint32_t)ln_near_tie(w, u) << j;
+        h[j] = __fadd_rn(__fmul_rn(__double2float_rn(w), p.scale1), p.shift);
+      }
+      if (lslow) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if ((lslow >> j) & 1u) {
+            const int col = lt + TPR * j;
+            h[j] = ln_exact(fa[SA * j], sd, ln_g64[col], ln_b64[col], p.scale1, p.shift);
+          }
+        }
       }
 #pragma unroll
       for (int i = 0; i < kV4Tail; ++i) {
         const int t = lt + TPR * i;
-        if (t < T) {
-          const double g = p.ln_g ? (double)__ldg(p.ln_g + B + t) : 1.0;
-          const double bb = p.ln_b ? (double)__ldg(p.ln_b + B + t) : 0.0;
-          ht[i] = ln_elem(ht[i], mean, sd, rsd, g, bb, p.scale1, p.shift);
-        }
+        if (t < T)
+          ht[i] = ln_elem(ht[i], mean, sd, rsd, ln_g64[B + t], ln_b64[B + t], p.scale1, p.shift);
       }
     } else if (p.prologue == QCB_PRO_GELU) {
 #pragma unroll
@@ -977,21 +1034,18 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
         const uint32_t sgm = sm.smask[o][tid];
         // ---- balance (exact f32(h / c), held in f64) + sign, stage A
         double v[16];
-        bool slow = false;
+        uint32_t slow = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 16; ++j) {   // rc carries the rotation sign
           const double q = __dmul_rn((double)h[j], __ldg(rc + lt + TPR * j));
-          slow |= f64_near_f32_tie(q);
-          v[j] = flip_sign(d_round24(q), (sgm >> j) & 1u);
+          slow |= f32_round_risk(q) << j;
+          v[j] = d_round24_fast(q);
         }
         if (slow) {   // exact IEEE division next to an f32 rounding boundary (rare)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const double hd = (double)h[j];
-            const int col = lt + TPR * j;
-            if (f64_near_f32_tie(__dmul_rn(hd, __ldg(rc + col))))
-              v[j] = flip_sign((double)__double2float_rn(__ddiv_rn(hd, c[col])), (sgm >> j) & 1u);
-          }
+          for (int j = 0; j < 16; ++j)
+            if ((slow >> j) & 1u)
+              v[j] = flip_sign(div_exact_f32((double)h[j], c[lt + TPR * j]), (sgm >> j) & 1u);
         }
         fwht_regs<4>(v);
 #pragma unroll
@@ -1007,7 +1061,7 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
                                                 : __double2float_rn(q);
             lo = fminf(lo, y);
             hi = fmaxf(hi, y);
-            so[B + t] = y;
+            st_f32_hint(so + B + t, y, pol_keep);
           }
         }
         row_sync();
@@ -1024,25 +1078,30 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
 #pragma unroll
           for (int jj = 0; jj < GS; ++jj) v[g * GS + jj] = fc[g * (TPR / 16) * 17 * GS + 17 * jj];
         fwht_regs<Q>(v);
+        float mn[2] = {lo, INFINITY};   // 2 min/max chains
+        float mx[2] = {hi, -INFINITY};
 #pragma unroll
         for (int g = 0; g < G; ++g)
 #pragma unroll
           for (int jj = 0; jj < GS; ++jj) {
-            const double vv = v[g * GS + jj];
-            const float xe = kPow2Scale ? __fmul_rn(__double2float_rn(vv), p.rscale)
+            const int r = g * GS + jj;
+            const double vv = v[r];
+            const float x1 = kPow2Scale ? __fmul_rn(__double2float_rn(vv), p.rscale)
                                         : __double2float_rn(__dmul_rn(vv, (double)p.rscale));
-            lo = fminf(lo, xe);
-            hi = fmaxf(hi, xe);
+            mn[r & 1] = fminf(mn[r & 1], x1);
+            mx[r & 1] = fmaxf(mx[r & 1], x1);
             const int e = (lt & 15) + 16 * jj + 16 * GS * ((lt >> 4) + (TPR / 16) * g);
-            so[e] = xe;
+            st_f32_hint(so + e, x1, pol_keep);
           }
+        lo = fminf(mn[0], mn[1]);
+        hi = fmaxf(mx[0], mx[1]);
         row_sync();   // f is rewritten by the next output / row
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           lo = fminf(lo, h[j]);
           hi = fmaxf(hi, h[j]);
-          so[lt + TPR * j] = h[j];
+          st_f32_hint(so + lt + TPR * j, h[j], pol_keep);
         }
 #pragma unroll
         for (int i = 0; i < kV4Tail; ++i) {
@@ -1050,7 +1109,7 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
           if (t < T) {
             lo = fminf(lo, ht[i]);
             hi = fmaxf(hi, ht[i]);
-            so[B + t] = ht[i];
+            st_f32_hint(so + B + t, ht[i], pol_keep);
           }
         }
       }
@@ -1145,6 +1204,53 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, 
             for (int e = 0; e < 4 && j + e < K; ++e) cr[j + e] = (uint8_t)(packed >> (8 * e));
         }
       };
+      if ((K & 3) == 0 && cr && !dr && (p.ldc & 3) == 0) {
+        // hot path: packed f32x2 estimate of clip(rha(xe/s) + z) per float4,
+        // one near-tie test per float4, bytes packed with PRMT, row sum by DP4A
+        const float2 inv2 = make_float2(inv_sf, inv_sf), z2 = make_float2(zf, zf);
+        const float2 mg = make_float2(12582912.0f, 12582912.0f);
+        const float2 nmg = make_float2(-12582912.0f, -12582912.0f);
+        const float2 m1 = make_float2(-1.0f, -1.0f);
+        const float2 b23 = make_float2(8388608.0f, 8388608.0f);
+        auto codes2 = [&](float2 x, float& dmax) -> uint32_t {
+          const float2 q = __fmul2_rn(x, inv2);
+          const float2 n = __fadd2_rn(__fadd2_rn(q, mg), nmg);   // rint(q), |q| < 2^22
+          const float2 d = __ffma2_rn(n, m1, q);                  // q - n, exact
+          dmax = fmaxf(dmax, fmaxf(fabsf(d.x), fabsf(d.y)));
+          float2 v = __fadd2_rn(n, z2);
+          v.x = fminf(fmaxf(v.x, 0.0f), topf);
+          v.y = fminf(fmaxf(v.y, 0.0f), topf);
+          const float2 k = __fadd2_rn(v, b23);                    // code in the low byte
+          return __byte_perm(__float_as_uint(k.x), __float_as_uint(k.y), 0x0040);
+        };
+        for (int j0 = lane * 4; j0 < K; j0 += 128 * kP2Batch) {
+          float4 v[kP2Batch];
+#pragma unroll
+          for (int b = 0; b < kP2Batch; ++b)
+            if (j0 + 128 * b < K) v[b] = __ldcs(reinterpret_cast<const float4*>(xr + j0 + 128 * b));
+#pragma unroll
+          for (int b = 0; b < kP2Batch; ++b) {
+            const int j = j0 + 128 * b;
+            if (j >= K) break;
+            float dmax = 0.0f;
+            const uint32_t lo2 = codes2(make_float2(v[b].x, v[b].y), dmax);
+            const uint32_t hi2 = codes2(make_float2(v[b].z, v[b].w), dmax);
+            uint32_t packed = __byte_perm(lo2, hi2, 0x5410);
+            if (dmax > 0.5f - 0x1p-12f) {   // near a .5 tie: the reference's f64 sequence
+              const float e4[4] = {v[b].x, v[b].y, v[b].z, v[b].w};
+              packed = 0;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                packed |= (uint32_t)code_of(e4[e], inv_sf, s, zf, topf) << (8 * e);
+            }
+            rs = __dp4a(packed, 0x01010101u, (unsigned)rs);
+            *reinterpret_cast<uint32_t*>(cr + j) = packed;
+          }
+        }
+        rs = warp_sum(rs);
+        if (lane == 0) p.rowsum[o][out_row] = rs;
+        continue;
+      }
       for (int j0 = lane * 4; j0 < K; j0 += 128 * kP2Batch) {
         float4 v[kP2Batch];
 #pragma unroll
@@ -1169,9 +1275,13 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, 
   }
 }
 
-__global__ void recip_k(const double* c, double* rc, int K) {
+// reciprocal table 1/c; with `signs`, the rotation signs of the first b
+// columns are folded in (s_j / c_j), which is what the v4 kernel consumes
+__global__ void recip_k(const double* c, const float* signs, int b, double* rc, int K) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < K) rc[i] = 1.0 / c[i];
+  if (i >= K) return;
+  const double r = 1.0 / c[i];
+  rc[i] = (signs && i < b && signs[i] < 0.f) ? -r : r;
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -1234,12 +1344,17 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     off += align256((size_t)8 * 3 * q->K);
     const size_t stash_bytes = align256((size_t)4 * q->K * q->seg_rows * q->nseg);
     a.ld_stash = q->K;
+    // v4 (register-first FWHT): 16-byte aligned rows, short tail; it takes the
+    // signed reciprocal table (qcb_weight_prep's chan_recip_out), v3 the plain one
+    const bool v4 = (q->K - b) <= kV4Tail * (b / 16) &&
+                    (reinterpret_cast<uintptr_t>(q->x) & 15) == 0;
     for (int o = 0; o < q->n_out; ++o) {
       a.rc[o] = rcbuf + (size_t)o * q->K;
-      if (q->chan_scale[o] && q->chan_recip[o]) {
+      if (q->chan_scale[o] && q->chan_recip[o] && v4) {
         a.rc[o] = q->chan_recip[o];
       } else if (q->chan_scale[o]) {
-        recip_k<<<(q->K + 255) / 256, 256, 0, st>>>(q->chan_scale[o], rcbuf + (size_t)o * q->K, q->K);
+        recip_k<<<(q->K + 255) / 256, 256, 0, st>>>(q->chan_scale[o], v4 ? q->signs[o] : nullptr,
+                                                     b, rcbuf + (size_t)o * q->K, q->K);
       }
       if (q->xe_out[o] && q->ldxe == q->K) {
         a.stash[o] = q->xe_out[o];
@@ -1259,22 +1374,20 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     const int rows_per_cta = 4096 / b;
     int b1 = (a.total_rows + rows_per_cta - 1) / rows_per_cta;
     if (b1 > num_sms() * 3) b1 = num_sms() * 3;
-    // v4 (register-first FWHT): 16-byte aligned rows and reciprocals, short tail
-    const bool v4 = (q->K - b) <= kV4Tail * (b / 16) &&
-                    (reinterpret_cast<uintptr_t>(q->x) & 15) == 0;
     if (v4) {
+      const size_t ln_bytes = q->prologue == QCB_PRO_LN_MOD ? (size_t)16 * q->K : 0;
       switch (b) {
         case 1024:
           allow_max_smem(aq4_pass1<1024, true>, a41);
-          aq4_pass1<1024, true><<<b1, kV4Threads, sizeof(V4Smem<1024>), st>>>(p, a);
+          aq4_pass1<1024, true><<<b1, kV4Threads, sizeof(V4Smem<1024>) + ln_bytes, st>>>(p, a);
           break;
         case 2048:
           allow_max_smem(aq4_pass1<2048, false>, a42);
-          aq4_pass1<2048, false><<<b1, kV4Threads, sizeof(V4Smem<2048>), st>>>(p, a);
+          aq4_pass1<2048, false><<<b1, kV4Threads, sizeof(V4Smem<2048>) + ln_bytes, st>>>(p, a);
           break;
         default:
           allow_max_smem(aq4_pass1<4096, true>, a44);
-          aq4_pass1<4096, true><<<b1, kV4Threads, sizeof(V4Smem<4096>), st>>>(p, a);
+          aq4_pass1<4096, true><<<b1, kV4Threads, sizeof(V4Smem<4096>) + ln_bytes, st>>>(p, a);
           break;
       }
     } else switch (b) {
@@ -1385,8 +1498,11 @@ __global__ void __launch_bounds__(kQThreads) weight_prep_cols(const WeightPrepPa
     p.zero[n] = (int)z;
     p.colsum[n] = cs;
   }
-  if (n == 0 && p.rc_out && p.c)
-    for (int k = threadIdx.x; k < K; k += blockDim.x) p.rc_out[k] = 1.0 / p.c[k];
+  if (n == 0 && p.rc_out && p.c)   // signed reciprocal table (see recip_k)
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      const double r = 1.0 / p.c[k];
+      p.rc_out[k] = (k < p.b && p.signs[k] < 0.f) ? -r : r;
+    }
 }
 
 int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st) {
