@@ -479,6 +479,46 @@ QC_DEV bool gelu_fast(float xf, float& y) {
   return true;
 }
 
+// Certified fast path for every x < 6.  g~ = 0.5 x (1 + erf(x / sqrt2)) from
+// CUDA's f64 erf / erfc (<= 4 ulp) on t = x * (1/sqrt2) (1 ulp from the
+// reference's x / sqrt2, propagated as 2 t^2 ulp).  The reference forms
+// 1 + erf for x < -sqrt2 as 1 - (1 - erfc), two roundings of size ~2^-53
+// next to a result of size erfc.  Relative bound on g~ vs the reference's
+// f64 value: rho < 2^-53 (128 + 8 t^2 + 8 / (1 + erf)) -- accepted when g~
+// is further than that from an f32 rounding tie (and in the f32 normal
+// range), else the exact cephes replica decides.
+QC_DEV bool gelu_fast2(float xf, float& y) {
+  if (xf >= 6.0f) {
+    y = xf;
+    return true;
+  }
+  const double x = (double)xf;
+  const double t = __dmul_rn(x, 0.70710678118654752440);
+  const double at = fabs(t);
+  double ope;   // 1 + erf(t)
+  if (at < 1.0) {
+    ope = 1.0 + erf(t);
+  } else if (t > 0.0) {
+    ope = 2.0 - erfc(t);
+  } else {
+    ope = erfc(at);
+  }
+  const double g = 0.5 * x * ope;
+  // window in ulp64 units of g's binade
+  const double w = 128.0 + 8.0 * t * t + 8.0 / ope;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(g);
+  const int ex = (int)((bits >> 52) & 0x7FF) - 1023;
+  if (g == 0.0 && xf == 0.0) {   // +-0 in, +-0 out
+    y = __double2float_rn(g);
+    return true;
+  }
+  if (ex < -125 || ex > 126 || !(w < 1.0e8)) return false;
+  const int d = abs((int)((unsigned)bits & 0x1FFFFFFFu) - (1 << 28));
+  if ((double)d <= w) return false;
+  y = __double2float_rn(g);
+  return true;
+}
+
 __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, int rows, int cols) {
   __shared__ float q_val[8][256];
   __shared__ int q_row[8][256];

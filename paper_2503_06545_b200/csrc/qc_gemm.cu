@@ -52,6 +52,10 @@ struct GemmCfg {
 };
 
 // one output column's epilogue parameters: a single 16-byte broadcast load
+// Tiles inside one segment (`uni`) carry the segment's values folded in:
+//   sw = f64(sa * sw[n]) (the reference's joint scale), cs = za * colsum[n] - 2^31
+// (biased so the accumulator converts to f64 with one DADD); other tiles carry
+// the raw sw[n], colsum[n].
 struct __align__(16) ColParam {
   double sw;
   int zw;
@@ -206,13 +210,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = (tile % p.num_n_tiles) * BN;
       // per-tile column parameters -> smem (buffer `acc`; see the barrier note)
       ColParam* t_col = col + acc * BN;
+      const int seg0 = m0 / p.seg_rows;
+      const int m_last = (m0 + kBlockM - 1 < p.M ? m0 + kBlockM - 1 : p.M - 1);
+      const bool uni = MODE != QCB_EPI_ACC && m_last / p.seg_rows == seg0;
+      const double sa0 = uni ? p.sa[seg0] : 0.0;
+      const int za0 = uni ? p.za[seg0] : 0;
       for (int i = et; i < BN; i += 32 * kEpiWarps) {
         const int n = n0 + i;
         const bool ok = n < p.N;
         ColParam cp;
-        cp.sw = ok ? __ldg(p.sw + n) : 0.0;
+        const double sw = ok ? __ldg(p.sw + n) : 0.0;
+        const int cs = ok ? __ldg(p.colsum + n) : 0;
+        cp.sw = uni ? __dmul_rn(sa0, sw) : sw;
         cp.zw = ok ? __ldg(p.zw + n) : 0;
-        cp.cs = ok ? __ldg(p.colsum + n) : 0;
+        cp.cs = uni ? (int)((unsigned)(za0 * cs) - 0x80000000u) : cs;
         t_col[i] = cp;
       }
       // One barrier per tile: a warp can only refill this buffer two tiles
@@ -240,40 +251,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       // first output row of this warp's 32-row slab (TMA store path)
       const long long orow_slab = __shfl_sync(0xffffffffu, orow, 0);
 
+      // residual rows are independent of the MMA: the first chunk's loads are
+      // issued before waiting for the accumulator, each next chunk's during the
+      // current chunk's math (register double buffer)
+      float rv_next[32];
+      auto load_resid = [&](int c, float (&dst)[32]) {
+        const int nb = n0 + c * 32;
+        if (!resid_mode || !row_ok || c >= BN / 32 || nb >= p.N) return;
+        const float* rp = p.resid + rrow * p.ldr + nb;
+        if (nb + 32 <= p.N && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 t4 = __ldcs(reinterpret_cast<const float4*>(rp + j));
+            dst[j] = t4.x; dst[j + 1] = t4.y; dst[j + 2] = t4.z; dst[j + 3] = t4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) dst[j] = (nb + j < p.N) ? rp[j] : 0.f;
+        }
+      };
+      if (resid_mode) load_resid(half, rv_next);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += 2) {
         const int nb = n0 + c * 32;
         if (nb >= p.N) break;
+        float rv[32];
+        if (resid_mode) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rv[j] = rv_next[j];
+          load_resid(c + 2, rv_next);
+        }
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         float v[32];
-        float rv[32];
-        if (resid_mode && row_ok) {
-          const float* rp = p.resid + rrow * p.ldr + nb;
-          if (nb + 32 <= p.N && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 t4 = *reinterpret_cast<const float4*>(rp + j);
-              rv[j] = t4.x; rv[j + 1] = t4.y; rv[j + 2] = t4.z; rv[j + 3] = t4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) rv[j] = (nb + j < p.N) ? rp[j] : 0.f;
-          }
-        }
         // y = f32(f64(sa*sw) * acc); int->f64 by a magic add on the FP64 pipe
         // so only the final rounding uses the conversion (XU) pipe.
+        if (uni) {
+          // acc + 2^31 as an unsigned low word under exponent 2^52: one DADD
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const ColParam cp = t_col[c * 32 + j];
-          const int accv = (int)r[j] - cp.zw * tr - za * cp.cs;
-          if (MODE == QCB_EPI_ACC) {
-            v[j] = __int_as_float(accv);
-          } else {
-            v[j] = __double2float_rn(__dmul_rn(__dmul_rn(sa, cp.sw), i2d_alu(accv)));
+          for (int j = 0; j < 32; ++j) {
+            const ColParam cp = t_col[c * 32 + j];
+            const int accb = (int)r[j] - cp.zw * tr - cp.cs;
+            const double d = __hiloint2double(0x43300000, accb) - 4503601774854144.0;
+            v[j] = __double2float_rn(__dmul_rn(cp.sw, d));
+          }
+          if (!__all_sync(0xffffffffu, row_ok)) {   // padding rows are written as 0
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = row_ok ? v[j] : 0.0f;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const ColParam cp = t_col[c * 32 + j];
+            const int accv = (int)r[j] - cp.zw * tr - za * cp.cs;
+            if (MODE == QCB_EPI_ACC) {
+              v[j] = __int_as_float(accv);
+            } else {
+              v[j] = __double2float_rn(__dmul_rn(__dmul_rn(sa, cp.sw), i2d_alu(accv)));
+            }
           }
         }
         if (MODE == QCB_EPI_GELU || MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID) {
@@ -467,7 +505,113 @@ static int launch_mode(const QcbGemm* g, cudaStream_t st) {
   }
 }
 
+// ---------------------------------------------------------------- small M
+// M <= kSmallM rows (the cross-attention K/V projections of the single cond
+// token: one row per video).  A 128-row UMMA tile would be >98% padding, so
+// this path streams each weight column once: one warp per output column, the
+// A rows staged in shared memory, u8 x u8 -> s32 dot products by DP4A (exact
+// integers, identical to the UMMA accumulator), then the same epilogue.
+constexpr int kSmallM = 16;
+constexpr int kSmallWarps = 8;
+
+__global__ void __launch_bounds__(32 * kSmallWarps) gemm_u8_small_m(const QcbGemm g) {
+  extern __shared__ __align__(16) uint8_t a_sm[];   // [M][Kp] codes, Kp = K rounded to 16
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Kp = (g.K + 15) & ~15;
+  const int M = g.M;
+  for (int i = threadIdx.x; i < M * (Kp / 16); i += blockDim.x) {
+    const int m = i / (Kp / 16), c = i - m * (Kp / 16);
+    uint4 v = *reinterpret_cast<const uint4*>(g.a_codes + (long long)m * g.lda + 16 * c);
+    const int k0 = 16 * c;
+    if (k0 + 16 > g.K) {   // zero the bytes past K (codes padding is unspecified)
+      uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int b = 0; b < 16; ++b)
+        if (k0 + b >= g.K) w4[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
+      v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    *reinterpret_cast<uint4*>(a_sm + m * Kp + 16 * c) = v;
+  }
+  __syncthreads();
+  const int n = blockIdx.x * kSmallWarps + warp;
+  if (n >= g.N) return;
+  const uint8_t* wc = g.w_codes + (long long)n * g.ldw;
+  uint32_t acc[kSmallM];
+#pragma unroll
+  for (int m = 0; m < kSmallM; ++m) acc[m] = 0u;
+  constexpr int kBatch = 8;   // 16-byte weight loads in flight per lane
+  for (int c0 = lane; c0 < Kp / 16; c0 += 32 * kBatch) {
+    uint4 w[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int c = c0 + 32 * b;
+      w[b] = c < Kp / 16 ? __ldcs(reinterpret_cast<const uint4*>(wc + 16 * c)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int c = c0 + 32 * b;
+      if (c >= Kp / 16) break;
+#pragma unroll
+      for (int m = 0; m < kSmallM; ++m) {
+        if (m < M) {
+          const uint4 a = *reinterpret_cast<const uint4*>(a_sm + m * Kp + 16 * c);
+          acc[m] = __dp4a(a.x, w[b].x, acc[m]);
+          acc[m] = __dp4a(a.y, w[b].y, acc[m]);
+          acc[m] = __dp4a(a.z, w[b].z, acc[m]);
+          acc[m] = __dp4a(a.w, w[b].w, acc[m]);
+        }
+      }
+    }
+  }
+  // warp sums; lane m keeps row m's raw accumulator
+  uint32_t mine = 0u;
+#pragma unroll
+  for (int m = 0; m < kSmallM; ++m) {
+    if (m < M) {
+      uint32_t v = acc[m];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == m) mine = v;
+    }
+  }
+  const int m = lane;
+  if (m >= M) return;
+  const int seg_rows = g.seg_rows > 0 ? g.seg_rows : M;
+  const int seg_valid = g.seg_valid > 0 ? g.seg_valid : seg_rows;
+  const int seg = m / seg_rows, mrow = m - seg * seg_rows;
+  if (mrow >= seg_valid) return;
+  if (g.seg_active && !g.seg_active[seg]) return;
+  const int za = g.a_zero[seg];
+  const int accv = (int)mine - g.w_zero[n] * (g.a_rowsum[m] - g.K * za) - za * g.w_colsum[n];
+  const long long orow = g.out_row0 ? g.out_row0[seg] + mrow : (long long)m;
+  float y;
+  if (g.epilogue == QCB_EPI_ACC) {
+    y = __int_as_float(accv);
+  } else {
+    y = __double2float_rn(__dmul_rn(__dmul_rn(g.a_scale[seg], g.w_scale[n]), i2d_alu(accv)));
+    if (g.epilogue == QCB_EPI_GELU) {
+      y = gelu_f32_ref(y);
+    } else if (g.epilogue == QCB_EPI_GATE_RESID || g.epilogue == QCB_EPI_RESID) {
+      const long long rrow = g.resid_row0 ? g.resid_row0[seg] + mrow : (long long)m;
+      const float r = g.resid[rrow * g.ldr + n];
+      const float gate = g.gate ? g.gate[seg] : g.gate_scalar;
+      y = g.epilogue == QCB_EPI_RESID ? __fadd_rn(r, y) : __fadd_rn(r, __fmul_rn(gate, y));
+    }
+  }
+  g.out[orow * g.ldo + n] = y;
+}
+
 int gemm_u8_launch(const QcbGemm* g, cudaStream_t st) {
+  if (g->M <= kSmallM && g->block_n <= 0 && g->epilogue != QCB_EPI_BIAS) {
+    const size_t smem = (size_t)g->M * ((g->K + 15) & ~15);
+    if (smem <= 200 * 1024) {
+      static bool attr = false;
+      allow_max_smem(gemm_u8_small_m, attr);
+      const int blocks = (g->N + kSmallWarps - 1) / kSmallWarps;
+      gemm_u8_small_m<<<blocks, 32 * kSmallWarps, smem, st>>>(*g);
+      return launch_status();
+    }
+  }
   int bn = g->block_n > 0 ? g->block_n : pick_block_n(g->N);
   switch (bn) {
     case 256: return launch_mode<256>(g, st);

@@ -73,7 +73,9 @@ class TestGemmU8:
 
     @pytest.mark.parametrize("M,K,N,bn", [(2048, 1152, 1152, 0), (1024, 4608, 1152, 0),
                                           (640, 1152, 4608, 256), (300, 200, 72, 0),
-                                          (256, 1152, 1152, 128), (256, 1152, 1152, 64)])
+                                          (256, 1152, 1152, 128), (256, 1152, 1152, 64),
+                                          (2, 4096, 1152, 0), (5, 200, 72, 0),
+                                          (16, 1152, 300, 0)])
     def test_random_accumulators_exact(self, D, M, K, N, bn):
         from paper_2503_06545_b200 import _native as Nat
         rng = np.random.default_rng(M + K + N)
@@ -83,12 +85,44 @@ class TestGemmU8:
         a = act_from_codes(D, ca.astype(np.uint8), 0.01, za)
         w = packed_from_codes(D, cw.astype(np.uint8), np.full(N, 0.02), zw)
         acc = D.gemm_u8(a, w, epilogue=Nat.EPI_ACC, block_n=bn).cpu().numpy()
-        rows = np.r_[0:64, M - 64:M]
+        rows = np.r_[0:64, M - 64:M] if M > 128 else np.arange(M)
         assert np.array_equal(acc[rows], O.int_acc(ca[rows], za, cw, zw))
         # full check via exact f64 products of integers (< 2^53)
         full = (torch.from_numpy((ca - za).astype(np.float64)).cuda() @
                 torch.from_numpy((cw - zw[None]).astype(np.float64)).cuda()).cpu().numpy()
         assert np.array_equal(acc.astype(np.float64), full)
+
+    def test_small_m_segments(self, D):
+        """One row per video (the cross-attention K/V of the cond token):
+        small-M path with per-segment params, gate and residual epilogues."""
+        from paper_2503_06545_b200 import _native as Nat
+        rng = np.random.default_rng(31)
+        nseg, K, N = 3, 4096, 200
+        ca = rng.integers(0, 256, size=(nseg, K)).astype(np.uint8)
+        cw = rng.integers(0, 64, size=(K, N)).astype(np.uint8)
+        sa = np.array([2.0 ** -7, 3.0 * 2.0 ** -9, 0.015625], np.float64)
+        za = np.array([3, 140, 17], np.int32)
+        sw = O.scale_up16(rng.uniform(1e-3, 1e-2, size=N))
+        zw = rng.integers(0, 64, size=N).astype(np.int32)
+        a = D.ActCodes(t(np.pad(ca, ((0, 0), (0, D.round16(K) - K)))),
+                       t(ca.astype(np.int64).sum(1).astype(np.int32)), t(sa), t(za), K)
+        w = packed_from_codes(D, cw, sw, zw)
+        want_y = np.concatenate([O.matmul_int_single_rounding(
+            ca[v:v + 1], sa[v], za[v], cw, sw, zw) for v in range(nseg)])
+        resid = rng.standard_normal((nseg, N)).astype(np.float32)
+        gates = np.array([0.5, -1.25, 0.37], np.float32)
+        for mode in (Nat.EPI_STORE, Nat.EPI_GATE_RESID, Nat.EPI_RESID):
+            out = torch.zeros((nseg, N), dtype=torch.float32, device="cuda")
+            D.gemm_u8(a, w, out=out, epilogue=mode, resid=t(resid), gate_vec=t(gates),
+                      seg_rows=1, seg_valid=1)
+            got = out.cpu().numpy()
+            if mode == Nat.EPI_STORE:
+                want = want_y
+            elif mode == Nat.EPI_GATE_RESID:
+                want = resid + gates[:, None] * want_y
+            else:
+                want = resid + want_y
+            assert np.array_equal(got, want), mode
 
     def test_segments_and_epilogues(self, D):
         """Per-video params, padded segments, GELU / gate+residual / residual."""
@@ -305,6 +339,7 @@ class TestFp:
         rng = np.random.default_rng(12)
         x = np.concatenate([
             rng.standard_normal(300_000) * 2.0, rng.uniform(-40, 40, 50_000),
+            rng.uniform(-14, -1.4, 1_000_000), rng.standard_normal(1_000_000) * 3.0,
             np.linspace(-1.4143, -1.4141, 2001), np.linspace(1.4141, 1.4143, 2001),
             np.linspace(5.99, 6.01, 2001), [0.0, -0.0, 1e-30, -1e-30, 37.0, -37.0, -39.0]])
         x = x.astype(np.float32)
