@@ -798,9 +798,8 @@ __global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, 
 // ------------------------------------------------------------------ v4 pass 1
 // Streaming register-first FWHT.  Each of the R = 4096 / b row slots of a CTA
 // is served by TPR = b / 16 threads and walks its own sequence of rows; the
-// slot's next two rows are in flight as 1-D bulk async copies (TMA engine)
-// into a double-buffered shared-memory row, so HBM reads overlap the FP64
-// work.  Row slots synchronise only among themselves (named barriers).
+// slot's next row is in flight as a 1-D bulk async copy (TMA engine) into
+// the slot's shared-memory row, so HBM reads overlap the FP64 work.  Row slots synchronise only among themselves (named barriers).
 // Thread lt of a slot owns, per radix-16 stage:
 //   stage A (bits NB-4..NB-1): e = lt + TPR j           (from the smem row)
 //   stage B (bits 0..3):       e = 16 lt + j
@@ -810,14 +809,18 @@ __global__ void __launch_bounds__(kV3Threads) aq3_pass1(const ActQuantParams p, 
 // registers store coalesced runs of xe.  Element e lives at f[e + (e >> 4)].
 constexpr int kV4Threads = 256;
 constexpr int kV4Tail = 4;   // max tail elements (K - b) per thread
+// Input rows in flight per slot.  One suffices: a row is read into registers
+// right after it lands, and computing it takes far longer than the next
+// row's HBM latency; the smaller footprint allows 3 CTAs per SM.
+constexpr int kV4Bufs = 1;
 
 template <int B>
 struct V4Smem {
   static constexpr int R = 4096 / B;
   static constexpr int kRowMax = B + kV4Tail * (B / 16);
-  float xrow[R][2][kRowMax];      // double-buffered input rows (bulk copies)
+  float xrow[R][kV4Bufs][kRowMax];  // input row ring per slot (bulk copies)
   double f[R][B + B / 16];        // FWHT work row
-  uint64_t full[R][2];            // bulk-copy completion barriers
+  uint64_t full[R][kV4Bufs];       // bulk-copy completion barriers
   double red[2][kV4Threads / 32]; // LN partial sums (mean, variance)
   uint32_t smask[3][kV4Threads];  // sign bits of the thread's 16 stage-A elements
   float run_mn[3][kV4Threads];    // per-thread running min / max per output
@@ -842,8 +845,8 @@ QC_DEV double flip_sign(double x, uint32_t bit) {
   return __longlong_as_double(__double_as_longlong(x) ^ ((long long)bit << 63));
 }
 
-template <int B, bool kPow2Scale>
-__global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams p, const AQ2 a) {
+template <int B, bool kPow2Scale, int kMinCtas>
+__global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuantParams p, const AQ2 a) {
   constexpr int R = 4096 / B;               // row slots per CTA
   constexpr int TPR = B / 16;               // threads per row slot
   constexpr int WPR = TPR / 32;             // warps per row slot (>= 2)
@@ -896,16 +899,15 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
     int seg, mrow;
     long long in_row, out_row;
     v2_row_index(p, gr, seg, mrow, in_row, out_row);
-    mbar_arrive_expect_tx(&sm.full[rl][k & 1], row_bytes);
-    bulk_load_hint(sm.xrow[rl][k & 1], p.x + in_row * p.ldx, row_bytes, &sm.full[rl][k & 1],
+    mbar_arrive_expect_tx(&sm.full[rl][k % kV4Bufs], row_bytes);
+    bulk_load_hint(sm.xrow[rl][k % kV4Bufs], p.x + in_row * p.ldx, row_bytes,
+                   &sm.full[rl][k % kV4Bufs],
                    pol_stream);
   };
   if (lt == 0) {
-    mbar_init(&sm.full[rl][0], 1);
-    mbar_init(&sm.full[rl][1], 1);
+    for (int i = 0; i < kV4Bufs; ++i) mbar_init(&sm.full[rl][i], 1);
     fence_barrier_init();
-    issue(0);
-    issue(1);
+    for (int i = 0; i < kV4Bufs; ++i) issue(i);
   }
   __syncthreads();
 
@@ -948,8 +950,8 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
       cur_seg = seg;
     }
     // ---- row from shared memory + prologue, in registers
-    mbar_wait(&sm.full[rl][k & 1], (k >> 1) & 1);
-    const float* xs = sm.xrow[rl][k & 1];
+    mbar_wait(&sm.full[rl][k % kV4Bufs], (k / kV4Bufs) & 1);
+    const float* xs = sm.xrow[rl][k % kV4Bufs];
     float h[16], ht[kV4Tail];
 #pragma unroll
     for (int j = 0; j < 16; ++j) h[j] = xs[lt + TPR * j];
@@ -1023,7 +1025,7 @@ __global__ void __launch_bounds__(kV4Threads, 2) aq4_pass1(const ActQuantParams 
     }
     // every thread of the slot has read the smem row: refill it with row k+2
     row_sync();
-    if (lt == 0) issue(k + 2);
+    if (lt == 0) issue(k + kV4Bufs);
 
     for (int o = 0; o < p.n_out; ++o) {
       const double* c = p.c[o];
@@ -1370,25 +1372,29 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     // pass 1: CTA shared-memory FWHT (v3); 1/sqrt(b) is a power of two for b = 1024, 4096
     (void)blocks;
     static bool at1 = false, at2 = false, at4 = false;
-    static bool a41 = false, a42 = false, a44 = false;
+    static bool a41 = false, a42 = false, a44 = false, a41l = false, a42l = false, a44l = false;
     const int rows_per_cta = 4096 / b;
     int b1 = (a.total_rows + rows_per_cta - 1) / rows_per_cta;
     if (b1 > num_sms() * 3) b1 = num_sms() * 3;
     if (v4) {
-      const size_t ln_bytes = q->prologue == QCB_PRO_LN_MOD ? (size_t)16 * q->K : 0;
-      switch (b) {
-        case 1024:
-          allow_max_smem(aq4_pass1<1024, true>, a41);
-          aq4_pass1<1024, true><<<b1, kV4Threads, sizeof(V4Smem<1024>) + ln_bytes, st>>>(p, a);
-          break;
-        case 2048:
-          allow_max_smem(aq4_pass1<2048, false>, a42);
-          aq4_pass1<2048, false><<<b1, kV4Threads, sizeof(V4Smem<2048>) + ln_bytes, st>>>(p, a);
-          break;
-        default:
-          allow_max_smem(aq4_pass1<4096, true>, a44);
-          aq4_pass1<4096, true><<<b1, kV4Threads, sizeof(V4Smem<4096>) + ln_bytes, st>>>(p, a);
-          break;
+      // the LN prologue's f64 affine tables take 16 K bytes of smem: 2 CTAs per
+      // SM there (128 registers), 3 CTAs per SM otherwise (80 registers)
+      const bool ln = q->prologue == QCB_PRO_LN_MOD;
+      const size_t ln_bytes = ln ? (size_t)16 * q->K : 0;
+      const int cap = num_sms() * (ln ? 2 : 3);
+      if (b1 > cap) b1 = cap;
+      switch (b * 2 + (ln ? 1 : 0)) {
+#define QC_AQ4(BB, P2, MC, FLAG)                                                            \
+  allow_max_smem(aq4_pass1<BB, P2, MC>, FLAG);                                              \
+  aq4_pass1<BB, P2, MC><<<b1, kV4Threads, sizeof(V4Smem<BB>) + ln_bytes, st>>>(p, a);       \
+  break;
+        case 2048: QC_AQ4(1024, true, 3, a41)
+        case 2049: QC_AQ4(1024, true, 2, a41l)
+        case 4096: QC_AQ4(2048, false, 3, a42)
+        case 4097: QC_AQ4(2048, false, 2, a42l)
+        case 8192: QC_AQ4(4096, true, 3, a44)
+        default: QC_AQ4(4096, true, 2, a44l)
+#undef QC_AQ4
       }
     } else switch (b) {
       case 1024:

@@ -136,6 +136,7 @@ class QuantCacheEngine:
         self.block_cost = block_mac_cost(self.cfg)
         self.head_macs = head_mac_cost(self.cfg)
         self.gemm_profile: Optional[list] = None   # set to [] to time every u8 GEMM
+        self.quant_profile: Optional[list] = None  # set to [] to time every act_quant
         self._upload_weights(act_absmax or {})
         self._alloc()
 
@@ -278,8 +279,19 @@ class QuantCacheEngine:
                 a = self.ac[o]
                 acs.append(Dv.ActCodes(self.codes[o][:M, :Dv.round16(p.K)],
                                        a.rowsum[:M], a.scale[:nseg], a.zero[:nseg], p.K))
+            qprof = self.quant_profile
+            if qprof is not None:
+                q0 = torch.cuda.Event(enable_timing=True)
+                q1 = torch.cuda.Event(enable_timing=True)
+                q0.record()
             Dv.act_quant(x, bits, trs, seg_rows=seg_rows, seg_valid=seg_valid, nseg=nseg,
                          x_row0=x_row0, ln=ln, mod=mod, out=acs, gelu=gelu_in)
+            if qprof is not None:
+                q1.record()
+                # algorithmic bytes: f32 rows read once, u8 codes written once per output
+                K = pws[0].K
+                rows = nseg * seg_valid
+                qprof.append((q0, q1, rows * K * 4 + len(pws) * rows * K, sites[0]))
             targets = outs or [out]
             prof = self.gemm_profile
             for o, p in enumerate(pws):
