@@ -347,15 +347,15 @@ def run_ours(args):
     # Kernel rooflines from one extra, separately profiled step (CUDA events
     # around every u8 GEMM and every quantizer call on the engine's stream), so
     # the timed region above carries no per-launch events.
-    eng.gemm_profile, eng.quant_profile = [], []
+    eng.gemm_profile, eng.quant_profile, eng.phase_profile = [], [], []
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
     eng.generate(seeds(900), device_noise_seed=900, x0_dev=x0, cond_dev=cond, return_device=True)
     p1.record(stream)
     torch.cuda.synchronize()
     prof_step = p0.elapsed_time(p1) / 1e3
-    gprof, qprof = eng.gemm_profile, eng.quant_profile
-    eng.gemm_profile = eng.quant_profile = None
+    gprof, qprof, pprof = eng.gemm_profile, eng.quant_profile, eng.phase_profile
+    eng.gemm_profile = eng.quant_profile = eng.phase_profile = None
 
     def _agg(prof):
         tot_work, tot_t, sites = 0, 0.0, {}
@@ -371,6 +371,11 @@ def run_ours(args):
 
     g_ops, g_time, per_site = _agg(gprof)
     q_bytes, q_time, q_sites = _agg(qprof)
+    phases = {"act_quant": q_time * 1e3, "gemm_u8": g_time * 1e3}
+    for name, e_s, e_e in pprof:
+        phases[name] = phases.get(name, 0.0) + e_s.elapsed_time(e_e)
+    phases["other_and_gaps"] = prof_step * 1e3 - sum(phases.values())
+    phases = {k: round(v, 3) for k, v in phases.items()}
     peak = measured_int8_peak(torch) if rank == 0 else {"tops": None}
     # e2e through the public API (host latents in, host latents out)
     e2e_vps = None
@@ -440,6 +445,7 @@ def run_ours(args):
         "executed_bit_macs_per_video": executed / (args.steps * B),
         "roofline": dominant,
         "roofline_kernels": {"act_quant": roof_quant, "gemm_u8": roof_gemm},
+        "profiled_step_ms": {"total": round(prof_step * 1e3, 3), **phases},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_vps, "unit": "videos/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

@@ -13,7 +13,8 @@
  *
  * Reference interfaces replaced (paths under /root/reference/pkg/src/ditrt):
  *   qcb_gemm_u8        tensor.py:68-112   matmul_int (+ model.py:187-198 epilogues)
- *   qcb_gemm_f64       tensor.py:43-65    mm / matmul_fp (FP sites, head)
+ *   qcb_gemm_f64       tensor.py:43-65    mm / matmul_fp (FP sites)
+ *   qcb_head_gemm      model.py:228       mm(x, head_w) + head_b (certified int8)
  *   qcb_act_quant      quant.py:83-123,163-165  compute_minmax_params + quantize
  *                      on BalanceTransform.apply_to_activation, with the
  *                      LN/modulation prologue of model.py:182,189,196
@@ -116,6 +117,34 @@ typedef struct QcbGemmF64 {
 } QcbGemmF64;
 
 int qcb_gemm_f64(const QcbGemmF64* g, void* stream);
+
+/* Noise head out = f32(mm(x, W)) + bias (model.py:228 with tensor.py:43-60) on
+ * the int8 tensor cores: x rows and W columns split into base-128 digit planes,
+ * one exact u8 GEMM per digit diagonal, f64 combination with an error bound;
+ * elements whose bound straddles an f32 rounding boundary are recomputed with
+ * the reference's ascending-k f64 FMA chain, so every output equals mm's.
+ * qcb_head_prep writes W's planes / statistics into `prep` once
+ * (qcb_head_prep_bytes); qcb_head_gemm runs per call with a workspace of
+ * qcb_head_workspace_bytes(nseg * seg_rows, K, N).  K and N must be multiples of 4. */
+typedef struct QcbHeadGemm {
+  int nseg, seg_rows, seg_valid; /* rows = nseg * seg_rows; rows >= seg_valid of a */
+  int K, N;                      /* segment are padding (not written)             */
+  const float* x;                /* rows via x_row0 per segment (nullable)        */
+  long long ldx;
+  const long long* x_row0;
+  const void* prep;              /* from qcb_head_prep                            */
+  const float* bias;             /* nullable [N]                                  */
+  float* out;                    /* [rows][ldo] (rows via out_row0, nullable)     */
+  long long ldo;
+  const long long* out_row0;
+  void* workspace;
+  int* fallback_count;           /* nullable device int: exact recomputations     */
+} QcbHeadGemm;
+
+size_t qcb_head_prep_bytes(int K, int N);
+size_t qcb_head_workspace_bytes(long long rows, int K, int N);
+int qcb_head_prep(const float* w, int K, int N, void* prep, void* stream);
+int qcb_head_gemm(const QcbHeadGemm* g, void* stream);
 
 /* ---------------------------------------------------------------- quantizer */
 typedef struct QcbActQuant {

@@ -41,6 +41,13 @@ class QcbGemmF64(C.Structure):
                 ("resid_row0", vp), ("bias", vp), ("gate_scalar", f32), ("epilogue", i32)]
 
 
+class QcbHeadGemm(C.Structure):
+    _fields_ = [("nseg", i32), ("seg_rows", i32), ("seg_valid", i32), ("K", i32), ("N", i32),
+                ("x", vp), ("ldx", i64), ("x_row0", vp), ("prep", vp), ("bias", vp),
+                ("out", vp), ("ldo", i64), ("out_row0", vp), ("workspace", vp),
+                ("fallback_count", vp)]
+
+
 class QcbActQuant(C.Structure):
     _fields_ = [("x", vp), ("ldx", i64), ("x_row0", vp), ("K", i32), ("seg_rows", i32),
                 ("seg_valid", i32), ("nseg", i32), ("prologue", i32), ("ln_g", vp),
@@ -119,6 +126,8 @@ def lib():
     sigs = {
         "qcb_gemm_u8": [P(QcbGemm), vp],
         "qcb_gemm_f64": [P(QcbGemmF64), vp],
+        "qcb_head_gemm": [P(QcbHeadGemm), vp],
+        "qcb_head_prep": [vp, i32, i32, vp, vp],
         "qcb_act_quant": [P(QcbActQuant), vp],
         "qcb_weight_prep": [P(QcbWeightPrep), vp],
         "qcb_ln_mod": [P(QcbLnMod), vp],
@@ -140,6 +149,10 @@ def lib():
         fn.restype = C.c_int
     h.qcb_act_quant_workspace_bytes.argtypes = [i32, i32, i32, i32]
     h.qcb_act_quant_workspace_bytes.restype = C.c_size_t
+    h.qcb_head_prep_bytes.argtypes = [i32, i32]
+    h.qcb_head_prep_bytes.restype = C.c_size_t
+    h.qcb_head_workspace_bytes.argtypes = [i64, i32, i32]
+    h.qcb_head_workspace_bytes.restype = C.c_size_t
     h.qcb_reduce_workspace_bytes.argtypes = [i32]
     h.qcb_reduce_workspace_bytes.restype = C.c_size_t
     h.qcb_device_sm_count.restype = C.c_int
@@ -149,7 +162,8 @@ def lib():
     return h
 
 
-EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_act_quant", "qcb_act_quant_workspace_bytes", "qcb_weight_prep", "qcb_ln_mod",
+EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_head_gemm", "qcb_head_prep",
+            "qcb_head_prep_bytes", "qcb_head_workspace_bytes", "qcb_act_quant", "qcb_act_quant_workspace_bytes", "qcb_weight_prep", "qcb_ln_mod",
             "qcb_attention_f64", "qcb_ddpm_step", "qcb_gelu_inplace", "qcb_reduce_hlc", "qcb_reduce_srap",
             "qcb_reduce_l1", "qcb_reduce_workspace_bytes", "qcb_policy_plan_reuse",
             "qcb_policy_sim_mask", "qcb_policy_plan_finish", "qcb_policy_observe",

@@ -28,6 +28,25 @@ extern "C" int qcb_gemm_u8(const QcbGemm* g, void* stream) {
   return gemm_u8_launch(g, (cudaStream_t)stream);
 }
 
+extern "C" int qcb_head_prep(const float* w, int K, int N, void* prep, void* stream) {
+  if (!w || !prep) return QCB_ERR_VALUE;
+  if (K <= 0 || N <= 0) return QCB_ERR_DIM;
+  if (7LL * K * 255LL * 255LL > 2147483647LL) return QCB_ERR_OVERFLOW;
+  return qc::head_prep_launch(w, K, N, prep, (cudaStream_t)stream);
+}
+
+extern "C" int qcb_head_gemm(const QcbHeadGemm* g, void* stream) {
+  if (!g || !g->x || !g->prep || !g->out || !g->workspace) return QCB_ERR_VALUE;
+  if (g->nseg <= 0 || g->seg_rows <= 0 || g->K <= 0 || g->N <= 0) return QCB_ERR_DIM;
+  if (g->seg_valid <= 0 || g->seg_valid > g->seg_rows || g->ldo < g->N || g->ldx < g->K)
+    return QCB_ERR_DIM;
+  if (g->K % 4 || g->N % 4 || g->ldx % 4 || (reinterpret_cast<uintptr_t>(g->x) & 15))
+    return QCB_ERR_DIM;   // 16-byte row vectors (digits, outputs, exact fallback)
+  if (7LL * g->K * 255LL * 255LL > 2147483647LL) return QCB_ERR_OVERFLOW;
+  if ((long long)g->nseg * g->seg_rows * g->N >= (1LL << 31)) return QCB_ERR_DIM;
+  return qc::head_gemm_launch(g, (cudaStream_t)stream);
+}
+
 extern "C" int qcb_gemm_f64(const QcbGemmF64* g, void* stream) {
   if (!g || !g->a || !g->w || !g->out) return QCB_ERR_VALUE;
   if (g->M <= 0 || g->N <= 0 || g->K <= 0) return QCB_ERR_DIM;

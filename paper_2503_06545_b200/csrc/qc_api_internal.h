@@ -31,6 +31,8 @@ int num_sms();
 int pick_block_n(int N);
 int gemm_u8_launch(const QcbGemm* g, cudaStream_t st);
 int gemm_f64_launch(const QcbGemmF64* g, cudaStream_t st);
+int head_prep_launch(const float* w, int K, int N, void* prep, cudaStream_t st);
+int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st);
 int act_quant_launch(const QcbActQuant* q, cudaStream_t st);
 int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st);
 int ln_mod_launch(const QcbLnMod* q, cudaStream_t st);

@@ -245,11 +245,20 @@ __global__ void __launch_bounds__(256, 1) gemm_f64_pipe_k(const GemmF64P P) {
     if (t + 1 < nk) fetch((t + 1) * kPK);
 #pragma unroll
     for (int kk = 0; kk < kPK; ++kk) {
+      // rows 2 ty + 32 i' + {0,1}, columns 2 tx + 32 j' + {0,1}: 16-byte loads
       double a[8], w[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = sm.As[buf][kk][ty + 16 * i];
+      for (int i = 0; i < 4; ++i) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&sm.As[buf][kk][2 * ty + 32 * i]);
+        a[2 * i] = t2.x;
+        a[2 * i + 1] = t2.y;
+      }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) w[j] = sm.Ws[buf][kk][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&sm.Ws[buf][kk][2 * tx + 32 * j]);
+        w[2 * j] = t2.x;
+        w[2 * j + 1] = t2.y;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f64_pipe_k(const GemmF64P P) {
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int m = m0 + ty + 16 * i;
+    const int m = m0 + 2 * ty + 32 * (i >> 1) + (i & 1);
     if (m >= g.M) continue;
     const int seg = m / seg_rows, r = m - seg * seg_rows;
     if (r >= seg_valid) continue;
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f64_pipe_k(const GemmF64P P) {
     const long long rrow = g.resid_row0 ? g.resid_row0[seg] + r : (long long)m;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int n = n0 + tx + 16 * j;
+      const int n = n0 + 2 * tx + 32 * (j >> 1) + (j & 1);
       if (n < g.N) g.out[orow * g.ldo + n] = f64_epilogue(g, acc[i][j], rrow, n);
     }
   }

@@ -242,6 +242,49 @@ def gemm_f64(a: torch.Tensor, w: torch.Tensor, out=None, epilogue: int = N.EPI_S
     return out
 
 
+class HeadWeights:
+    """W [K][N] f32 prepared once for head_gemm (digit planes, column stats, W^T)."""
+
+    def __init__(self, w: torch.Tensor, stream=None):
+        assert w.dtype == torch.float32 and w.is_cuda and w.dim() == 2
+        self.K, self.N = int(w.shape[0]), int(w.shape[1])
+        w = w.contiguous()
+        nbytes = int(N.lib().qcb_head_prep_bytes(self.K, self.N))
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=w.device)
+        N.check(N.lib().qcb_head_prep(N.ptr(w), self.K, self.N, N.ptr(self.buf),
+                                      N.stream_ptr(stream)), "head_prep")
+        count(1)
+
+
+_HWS = Workspace()
+
+
+def head_gemm(a: torch.Tensor, hw: HeadWeights, out=None, bias=None, seg_rows=None,
+              seg_valid=None, nseg: int = 1, a_row0=None, out_row0=None, stream=None,
+              fallback_count: Optional[torch.Tensor] = None):
+    """f32(mm(a, W)) + bias bit-exactly via certified int8 tensor-core digit GEMMs
+    (exact f64 FMA chains for uncertified elements)."""
+    dev = _dev()
+    K = a.shape[-1]
+    if K != hw.K:
+        raise DimensionError(f"matmul shapes {tuple(a.shape)} x ({hw.K}, {hw.N})")
+    seg_rows = seg_rows or (a.shape[0] // nseg)
+    seg_valid = seg_valid or seg_rows
+    rows = nseg * seg_rows
+    if out is None:
+        out = torch.empty((rows, hw.N), dtype=torch.float32, device=dev)
+    ws = _HWS.get(int(N.lib().qcb_head_workspace_bytes(rows, K, hw.N)))
+    g = N.QcbHeadGemm()
+    g.nseg, g.seg_rows, g.seg_valid, g.K, g.N = nseg, seg_rows, seg_valid, K, hw.N
+    g.x, g.ldx, g.x_row0 = N.ptr(a), a.stride(0), N.ptr(a_row0)
+    g.prep, g.bias = N.ptr(hw.buf), N.ptr(bias)
+    g.out, g.ldo, g.out_row0 = N.ptr(out), out.stride(0), N.ptr(out_row0)
+    g.workspace, g.fallback_count = N.ptr(ws), N.ptr(fallback_count)
+    N.check(N.lib().qcb_head_gemm(C.byref(g), N.stream_ptr(stream)), "head_gemm")
+    count(10)
+    return out
+
+
 def ln_mod(x: torch.Tensor, gamma=None, beta=None, scale1: float = 1.0, shift: float = 0.0,
            out=None, seg_rows=None, seg_valid=None, nseg: int = 1, x_row0=None,
            out_row0=None, stream=None):
@@ -314,9 +357,13 @@ def reduce_hlc(out: N.QcbFeat, ref: N.QcbFeat, prev: N.QcbFeat, rows: int, cols:
 
 
 def reduce_srap(a: N.QcbFeat, b: N.QcbFeat, rows: int, cols: int, nseg: int,
-                res: torch.Tensor, seg_active=None, stream=None):
+                res: torch.Tensor, seg_active=None, stream=None,
+                workspace: Optional[Workspace] = None):
+    """workspace: a dedicated scratch when this runs concurrently with other
+    reductions (side stream); default the shared one."""
+    ws = N.ptr((workspace or _RWS).get(int(N.lib().qcb_reduce_workspace_bytes(nseg))))
     N.check(N.lib().qcb_reduce_srap(a, b, rows, cols, nseg, N.ptr(seg_active), N.ptr(res),
-                                    _rws(nseg), N.stream_ptr(stream)), "reduce_srap")
+                                    ws, N.stream_ptr(stream)), "reduce_srap")
     count(1)
     return res
 

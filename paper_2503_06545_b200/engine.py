@@ -24,6 +24,7 @@ values (D, S, V) stay on device until the end of the run.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
@@ -99,7 +100,27 @@ class VideoState:
 class EngineOptions:
     attention: str = "precise"     # "precise" (f64 softmax kernel) | "fast" (bf16 SDPA)
     noise: str = "numpy"           # "numpy" (reference RNG stream) | "device" (Philox)
+    head: str = "int8"             # "int8" (certified digit GEMMs) | "f64" (FMA chains);
+                                   # both give the reference's mm bit for bit
     record_features: bool = False
+
+
+class _PhaseEvents:
+    """Records (name, start event, end event) around a phase on the current stream."""
+
+    def __init__(self, prof: list, name: str):
+        self.prof, self.name = prof, name
+
+    def __enter__(self):
+        self.e0 = torch.cuda.Event(enable_timing=True)
+        self.e1 = torch.cuda.Event(enable_timing=True)
+        self.e0.record()
+        return self
+
+    def __exit__(self, *exc):
+        self.e1.record()
+        self.prof.append((self.name, self.e0, self.e1))
+        return False
 
 
 class QuantCacheEngine:
@@ -137,6 +158,7 @@ class QuantCacheEngine:
         self.head_macs = head_mac_cost(self.cfg)
         self.gemm_profile: Optional[list] = None   # set to [] to time every u8 GEMM
         self.quant_profile: Optional[list] = None  # set to [] to time every act_quant
+        self.phase_profile: Optional[list] = None  # set to [] to time the other phases
         self._upload_weights(act_absmax or {})
         self._alloc()
 
@@ -174,6 +196,7 @@ class QuantCacheEngine:
             self.fpw.append(fp)
             self.packed.append(pk)
         self.head_w = self._t(m.head_w)
+        self.head_prep = Dv.HeadWeights(self.head_w) if self.opts.head == "int8" else None
         self.head_b = self._t(m.head_b)
         # modulation scalars for every (t, layer): t_emb @ mod on device (f64 acc)
         temb = self._t(np.stack([timestep_embedding(t, self.d) for t in range(self.T)]))
@@ -218,6 +241,10 @@ class QuantCacheEngine:
         self.mask = torch.zeros((L, nv), dtype=torch.int32, device=dev)
         self.hist_l1 = torch.zeros((self.th.history_k + 1, nv), dtype=torch.float64, device=dev)
         self.hlc = torch.zeros((L, nv, 2), dtype=torch.float64, device=dev)
+        # the next step's reuse plan + SRAP similarities run on a side stream
+        # while this step's FP64 noise head runs (see _early_plan)
+        self.side = torch.cuda.Stream(device=dev)
+        self._srap_ws = Dv.Workspace()
         n_idx = 2 * max(1 << 15, 16 * L * (nv + 4) + 64)
         self.idx_host = torch.zeros(n_idx, dtype=torch.int64).pin_memory()
         self.idx_dev = torch.zeros(n_idx, dtype=torch.int64, device=dev)
@@ -253,6 +280,13 @@ class QuantCacheEngine:
 
     def rows(self, slot: int) -> int:
         return slot * self.Sp
+
+    def _ph(self, name: str):
+        """CUDA-event bracket for a phase when phase profiling is on."""
+        prof = self.phase_profile
+        if prof is None:
+            return contextlib.nullcontext()
+        return _PhaseEvents(prof, name)
 
     def slot_view(self, slot: int) -> torch.Tensor:
         return self.arena[slot * self.Sp: slot * self.Sp + self.S]
@@ -372,14 +406,16 @@ class QuantCacheEngine:
         # spatial-temporal self-attention
         self._site(l, None, bits, A, n, x_row0=xin_row0, ln=(ln1g, ln1b), mod=(sc1, sh1),
                    outs=[self.q, self.k, self.v], sites=("sta_q", "sta_k", "sta_v"))
-        self._attention(self.q, self.k, self.v, self.att, n, self.S, self.Sp)
+        with self._ph("attention"):
+            self._attention(self.q, self.k, self.v, self.att, n, self.S, self.Sp)
         self._site(l, "sta_o", bits, self.att, n, epi=N.EPI_GATE_RESID, out=A,
                    out_row0=out_row0, resid=A, resid_row0=xin_row0, gate=g1)
         # cross-attention on the single cond token
         self._site(l, "ca_q", bits, A, n, x_row0=out_row0, ln=(ln2g, ln2b), out=self.q2)
         self._site(l, None, bits, self.cond, n, x_row0=cond_row0, seg_rows=1, seg_valid=1,
                    outs=[self.k2, self.v2], sites=("ca_k", "ca_v"))
-        self._attention(self.q2, self.k2, self.v2, self.att, n, 1, 1)
+        with self._ph("attention"):
+            self._attention(self.q2, self.k2, self.v2, self.att, n, 1, 1)
         self._site(l, "ca_o", bits, self.att, n, epi=N.EPI_RESID, out=A, out_row0=out_row0,
                    resid=A, resid_row0=out_row0)
         # FFN.  On the integer path GELU (model.py:197) runs as its own in-place
@@ -389,9 +425,49 @@ class QuantCacheEngine:
         self._site(l, "ffn1", bits, A, n, x_row0=out_row0, ln=(ln3g, ln3b), mod=(sc3, sh3),
                    epi=N.EPI_STORE if int_path else N.EPI_GELU, out=self.hid)
         if int_path:
-            Dv.gelu_inplace(self.hid, rows=n * self.Sp)
+            with self._ph("gelu"):
+                Dv.gelu_inplace(self.hid, rows=n * self.Sp)
         self._site(l, "ffn2", bits, self.hid, n, epi=N.EPI_GATE_RESID, out=A,
                    out_row0=out_row0, resid=A, resid_row0=out_row0, gate=g3)
+
+    # ------------------------------------------------------------------ plan
+    def _srap_tables(self, vids) -> List[List[int]]:
+        """Row tables for one SRAP launch over every (layer, video) pair:
+        prev[l-1] vs prev[l] (schedule.py:298-305)."""
+        L = self.L
+        return [[self.rows(vs.prev[l - 1]) if l > 0 and vs.prev[l - 1] is not None else 0
+                 for l in range(L) for vs in vids],
+                [self.rows(vs.prev[l]) if vs.prev[l] is not None else 0
+                 for l in range(L) for vs in vids]]
+
+    def _plan_reuse_srap(self, t: int, nv: int, do_srap: bool, tabs, stream,
+                         workspace=None):
+        """plan_reuse (HLC liveness, schedule.py:285-291) + SRAP similarities of
+        the layers it marks for recompute (schedule.py:296-306) on `stream`."""
+        lib, pol, L, S, d = N.lib(), self.pol.data_ptr(), self.L, self.S, self.d
+        sp = N.stream_ptr(stream)
+        N.check(lib.qcb_policy_plan_reuse(pol, nv, L, t, self.thc, sp), "plan_reuse")
+        Dv.count(1)
+        if do_srap:
+            N.check(lib.qcb_policy_sim_mask(pol, nv, L, self.thc, N.ptr(self.mask), sp),
+                    "sim_mask")
+            Dv.count(1)
+            Dv.reduce_srap(Dv.feat(self.arena, tabs[0]), Dv.feat(self.arena, tabs[1]), S, d,
+                           L * nv, self.srap.view(L * nv, 3), seg_active=self.mask.view(L * nv),
+                           stream=stream, workspace=workspace)
+
+    def _early_plan(self, tn: int, vids, main):
+        """Launch step tn's plan_reuse + SRAP on the side stream (after everything
+        queued on `main` so far); returns (tn, completion event)."""
+        do_srap = self.tog.srap and tn != 0   # seen >= 1 here: boundary iff tn == 0
+        tabs = self._upload_idx(self._srap_tables(vids)) if do_srap else []
+        ready = torch.cuda.Event()
+        ready.record(main)
+        self.side.wait_event(ready)
+        self._plan_reuse_srap(tn, len(vids), do_srap, tabs, self.side, self._srap_ws)
+        done = torch.cuda.Event()
+        done.record(self.side)
+        return (tn, done)
 
     # ------------------------------------------------------------------ run
     def generate(self, seeds: Sequence[int], device_noise_seed: Optional[int] = None,
@@ -433,6 +509,7 @@ class QuantCacheEngine:
             gen = torch.Generator(device=self.dev)
             gen.manual_seed(int(device_noise_seed if device_noise_seed is not None else seeds[0]))
         pol = self.pol.data_ptr()
+        self._early = None
         lib = N.lib()
         sp = N.stream_ptr()
         for t in range(T - 1, -1, -1):
@@ -443,31 +520,27 @@ class QuantCacheEngine:
             for j in range(nh):
                 pre.append([self.rows(vs.x) for vs in vids])
                 pre.append([self.rows(vs.hist[j]) for vs in vids])
-            boundary = vids[0].seen == 0 or t == 0
-            do_srap = self.tog.srap and not boundary
-            if do_srap:
-                # one launch for every (layer, video) pair: prev[l-1] vs prev[l]
-                pre.append([self.rows(vs.prev[l - 1]) if l > 0 and vs.prev[l - 1] is not None
-                            else 0 for l in range(L) for vs in vids])
-                pre.append([self.rows(vs.prev[l]) if vs.prev[l] is not None else 0
-                            for l in range(L) for vs in vids])
+            early = self._early if (self._early is not None and self._early[0] == t) else None
+            self._early = None
+            if early is None:
+                do_srap = self.tog.srap and not (vids[0].seen == 0 or t == 0)
+                if do_srap:
+                    pre += self._srap_tables(vids)
             tabs = self._upload_idx(pre)
+            ph = self._ph("plan")
+            ph.__enter__()
             for j in range(nh):
                 Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]), Dv.feat(self.arena, tabs[2 * j + 1]),
                              S, d, nv, self.hist_l1[j])
-            N.check(lib.qcb_policy_plan_reuse(pol, nv, L, t, self.thc, sp), "plan_reuse")
-            Dv.count(1)
-            if do_srap:
-                N.check(lib.qcb_policy_sim_mask(pol, nv, L, self.thc, N.ptr(self.mask), sp),
-                        "sim_mask")
-                Dv.count(1)
-                Dv.reduce_srap(Dv.feat(self.arena, tabs[2 * nh]),
-                               Dv.feat(self.arena, tabs[2 * nh + 1]), S, d, L * nv,
-                               self.srap.view(L * nv, 3), seg_active=self.mask.view(L * nv))
+            if early is None:
+                self._plan_reuse_srap(t, nv, do_srap, tabs[2 * nh:], st)
+            else:
+                st.wait_event(early[1])   # plan_reuse / SRAP of this step ran on the side stream
             N.check(lib.qcb_policy_plan_finish(pol, nv, L, t, self.thc, N.ptr(self.srap),
                                                N.ptr(self.hist_l1), nh,
                                                N.ptr(self.draws[t]), 0, sp), "plan_finish")
             Dv.count(1)
+            ph.__exit__(None, None, None)
             self.pol_host.copy_(self.pol, non_blocking=True)
             st.synchronize()
             raw = self.pol_host.numpy()
@@ -514,10 +587,11 @@ class QuantCacheEngine:
                     if any(need_d):
                         base = 3 * len(groups)
                         act = tl[base + 3].to(torch.int32)
-                        Dv.reduce_hlc(Dv.feat(self.arena, tl[base]),
-                                      Dv.feat(self.arena, tl[base + 1]),
-                                      Dv.feat(self.arena, tl[base + 2]), S, d, nv,
-                                      self.hlc[l], seg_active=act)
+                        with self._ph("hlc"):
+                            Dv.reduce_hlc(Dv.feat(self.arena, tl[base]),
+                                          Dv.feat(self.arena, tl[base + 1]),
+                                          Dv.feat(self.arena, tl[base + 2]), S, d, nv,
+                                          self.hlc[l], seg_active=act)
 
                 # host mirror of the cache / prev references (schedule.py:349-351)
                 for v, vs in enumerate(vids):
@@ -538,11 +612,22 @@ class QuantCacheEngine:
                 x_now = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
                 collect_features.append((t, x_now, feats))
             # ---------------- head + sampler update ----------------
-            tabh = self._upload_idx([[self.rows(c) for c in cur]])
-            Dv.gemm_f64(self.arena, self.head_w, out=self.eps, epilogue=N.EPI_BIAS,
-                        bias=self.head_b, seg_rows=self.Sp, seg_valid=S, a_row0=tabh[0],
-                        M=nv * self.Sp)
             self.pol_trace[t].copy_(self.pol, non_blocking=True)
+            if t > 0:
+                # the next step's reuse plan depends only on the cache state just
+                # observed (schedule.py:286-309): overlap it with the head
+                self._early = self._early_plan(t - 1, vids, st)
+            tabh = self._upload_idx([[self.rows(c) for c in cur]])
+            with self._ph("head"):
+                if self.head_prep is not None:
+                    Dv.head_gemm(self.arena, self.head_prep, out=self.eps, bias=self.head_b,
+                                 seg_rows=self.Sp, seg_valid=S, nseg=nv, a_row0=tabh[0])
+                else:
+                    Dv.gemm_f64(self.arena, self.head_w, out=self.eps, epilogue=N.EPI_BIAS,
+                                bias=self.head_b, seg_rows=self.Sp, seg_valid=S,
+                                a_row0=tabh[0], M=nv * self.Sp)
+            ph = self._ph("sampler")
+            ph.__enter__()
             if t > 0:
                 if self.opts.noise == "numpy":
                     for v, vs in enumerate(vids):
@@ -572,6 +657,7 @@ class QuantCacheEngine:
                 if len(vs.hist) > self.th.history_k:
                     vs.pool.dec(vs.hist.pop(0))
                 vs.x = new
+            ph.__exit__(None, None, None)
         out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
         if return_device:
             return out, vids

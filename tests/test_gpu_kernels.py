@@ -326,6 +326,45 @@ class TestFp:
             w = rng.standard_normal((k, n)).astype(np.float32)
             assert np.array_equal(D.gemm_f64(t(a), t(w)).cpu().numpy(), O.seq_mm(a, w))
 
+    @pytest.mark.parametrize("case", ["normal", "dynamic_range", "cancellation"])
+    def test_head_gemm_certified_exact(self, D, case):
+        """model.py:228 noise head via certified int8 digit GEMMs == mm + bias bit
+        for bit (tensor.py:43-60), incl. padded segments and the exact fallback."""
+        from paper_2503_06545_b200 import _native as Nat
+        rng = np.random.default_rng({"normal": 1, "dynamic_range": 2, "cancellation": 3}[case])
+        nseg, seg_rows, seg_valid, K, N = 2, 160, 150, 1152, 264
+        x = rng.standard_normal((nseg * seg_rows, K)).astype(np.float32) * 3
+        w = (rng.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32)
+        b = (rng.standard_normal(N) * 0.1).astype(np.float32)
+        if case == "dynamic_range":
+            x[::7] *= np.float32(1e-6)
+            x[3, ::5] = np.float32(1e-30)
+            x[5] = 0.0
+            x[9, :K // 2] *= np.float32(1e6)
+            w[:, 4] = 0.0
+            w[::11, 8] *= np.float32(1e-9)
+        elif case == "cancellation":
+            # rows whose products cancel to (near) zero and to values near f32 ties
+            x[1::2, K // 2:] = x[1::2, :K // 2]
+            w[K // 2:, ::3] = -w[:K // 2, ::3]
+            w[K // 2:, 1::3] = -w[:K // 2, 1::3] * np.float32(1 + 2 ** -20)
+        hw = D.HeadWeights(t(w))
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        got = D.head_gemm(t(x), hw, bias=t(b), seg_rows=seg_rows, seg_valid=seg_valid,
+                          nseg=nseg, fallback_count=cnt).cpu().numpy()
+        want = D.gemm_f64(t(x), t(w), epilogue=Nat.EPI_BIAS, bias=t(b), seg_rows=seg_rows,
+                          seg_valid=seg_valid).cpu().numpy()
+        valid = np.concatenate([np.arange(v * seg_rows, v * seg_rows + seg_valid)
+                                for v in range(nseg)])
+        assert np.array_equal(got[valid].view(np.int32), want[valid].view(np.int32)), \
+            (case, int(cnt.item()))
+        # the oracle's sequential mm on a few rows (pins gemm_f64 too)
+        rows = valid[[0, 3, 5, 9, 151]] if case != "normal" else valid[:4]
+        ref = O.seq_mm(x[rows], w) + b
+        assert np.array_equal(got[rows], ref)
+        if case == "cancellation":
+            assert cnt.item() > 0   # the exact fallback ran
+
     def test_attention_matches_reference(self, D):
         rng = np.random.default_rng(6)
         for S, Skv, d, h in [(8, 8, 16, 2), (64, 64, 64, 4), (64, 1, 64, 4), (200, 200, 32, 2)]:

@@ -33,3 +33,25 @@ ref = (a[:256].double() @ w.double()).float()
 print(json.dumps({"M": args.M, "K": args.K, "N": args.N, "us": us,
                   "dfma_tflops": 2 * args.M * args.K * args.N / us / 1e6,
                   "max_abs_diff_vs_torch_f64_256rows": (out[:256] - ref).abs().max().item()}))
+
+# certified int8 head at the same shape (+ bias), vs the f64 kernel, bit-compared
+from paper_2503_06545_b200 import _native as Nat
+bias = torch.randn(args.N, device="cuda") * 0.1
+hw = D.HeadWeights(w)
+cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+out2 = torch.empty_like(out)
+for _ in range(2):
+    D.head_gemm(a, hw, out=out2, bias=bias)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(args.iters):
+    D.head_gemm(a, hw, out=out2, bias=bias)
+e1.record()
+torch.cuda.synchronize()
+us2 = e0.elapsed_time(e1) / args.iters * 1e3
+D.head_gemm(a, hw, out=out2, bias=bias, fallback_count=cnt)
+ref = D.gemm_f64(a, w, epilogue=Nat.EPI_BIAS, bias=bias)
+same = bool(torch.equal(out2.view(torch.int32), ref.view(torch.int32)))
+print(json.dumps({"head_int8_us": us2, "f64_us": us, "speedup": us / us2,
+                  "fallback_elements": int(cnt.item()), "elements": args.M * args.N,
+                  "bit_identical": same}))
