@@ -138,7 +138,7 @@ typedef struct QcbHeadGemm {
   long long ldo;
   const long long* out_row0;
   void* workspace;
-  int* fallback_count;           /* nullable device int: exact recomputations     */
+  int* fallback_count;           /* nullable device int += exact recomputations   */
 } QcbHeadGemm;
 
 size_t qcb_head_prep_bytes(int K, int N);

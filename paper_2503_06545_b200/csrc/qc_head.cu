@@ -377,11 +377,13 @@ struct HeadFallback {
   const long long* out_row0;
   const int* list;
   const int* count;
+  int* total;   // nullable running total of exact recomputations
 };
 
 // The reference's ascending-k f64 FMA chain for the listed elements.
 __global__ void __launch_bounds__(256) head_fallback(const HeadFallback h) {
   const int n = *h.count;
+  if (h.total && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(h.total, n);
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const long long idx = h.list[t];
     const long long i = idx / h.N;
@@ -488,12 +490,10 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
   HeadFallback fb{g->x, g->ldx, g->x_row0, g->seg_rows, N, K,
                   reinterpret_cast<const float*>(prep + P.wt), g->bias, g->out, g->ldo,
                   g->out_row0, reinterpret_cast<const int*>(ws + W.list),
-                  reinterpret_cast<const int*>(ws + W.count)};
+                  reinterpret_cast<const int*>(ws + W.count), g->fallback_count};
   head_fallback<<<num_sms() * 4, 256, 0, st>>>(fb);
   rc = launch_status();
   if (rc) return rc;
-  if (g->fallback_count)
-    cudaMemcpyAsync(g->fallback_count, ws + W.count, 4, cudaMemcpyDeviceToDevice, st);
   return launch_status();
 }
 

@@ -197,6 +197,8 @@ class QuantCacheEngine:
             self.packed.append(pk)
         self.head_w = self._t(m.head_w)
         self.head_prep = Dv.HeadWeights(self.head_w) if self.opts.head == "int8" else None
+        # running count of head outputs recomputed by the exact f64 chain
+        self.head_fallbacks = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.head_b = self._t(m.head_b)
         # modulation scalars for every (t, layer): t_emb @ mod on device (f64 acc)
         temb = self._t(np.stack([timestep_embedding(t, self.d) for t in range(self.T)]))
@@ -621,7 +623,8 @@ class QuantCacheEngine:
             with self._ph("head"):
                 if self.head_prep is not None:
                     Dv.head_gemm(self.arena, self.head_prep, out=self.eps, bias=self.head_b,
-                                 seg_rows=self.Sp, seg_valid=S, nseg=nv, a_row0=tabh[0])
+                                 seg_rows=self.Sp, seg_valid=S, nseg=nv, a_row0=tabh[0],
+                                 fallback_count=self.head_fallbacks)
                 else:
                     Dv.gemm_f64(self.arena, self.head_w, out=self.eps, epilogue=N.EPI_BIAS,
                                 bias=self.head_b, seg_rows=self.Sp, seg_valid=S,

@@ -364,6 +364,11 @@ class TestFp:
         assert np.array_equal(got[rows], ref)
         if case == "cancellation":
             assert cnt.item() > 0   # the exact fallback ran
+        # fallback_count accumulates across calls
+        before = int(cnt.item())
+        D.head_gemm(t(x), hw, bias=t(b), seg_rows=seg_rows, seg_valid=seg_valid, nseg=nseg,
+                    fallback_count=cnt)
+        assert int(cnt.item()) == 2 * before
 
     def test_attention_matches_reference(self, D):
         rng = np.random.default_rng(6)
