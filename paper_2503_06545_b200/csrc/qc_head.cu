@@ -35,7 +35,7 @@ static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 struct HeadPrepLayout {   // one-time weight side
   size_t bd[kHeadDigits];   // B_d codes [N][ldb_d], ldb_d = a16((d+1) K)
   size_t csum;              // s32 [kHeadDigits][N]
-  size_t cstat;             // f64 [N][4]: f_j, |w_j|_1, |w_j|_2, 0
+  size_t cstat;             // f64 [N][8]: certificate column factors (head_prep_cols)
   size_t wt;                // f32 [N][K] (W^T for the exact fallback)
   size_t ones;              // f64 [N] = 1.0 (w_scale), s32 [N] = 64 (w_zero) after it
   size_t zeros64;
@@ -52,7 +52,7 @@ static HeadPrepLayout prep_layout(int K, int N) {
   L.csum = off;
   off = a256(off + (size_t)4 * kHeadDigits * N);
   L.cstat = off;
-  off = a256(off + (size_t)8 * 4 * N);
+  off = a256(off + (size_t)8 * 8 * N);
   L.wt = off;
   off = a256(off + (size_t)4 * N * K);
   L.ones = off;
@@ -66,7 +66,7 @@ static HeadPrepLayout prep_layout(int K, int N) {
 struct HeadWsLayout {     // per call
   size_t planes;  // u8 [M][ldp], ldp = a16(kHeadDigits K)
   size_t rsum;    // s32 [kHeadDigits][M] (prefix over planes)
-  size_t rstat;   // f64 [M][4]: e_i, |x_i|_1, |x_i|_2, 0
+  size_t rstat;   // f64 [M][8]: certificate row factors (head_slice_rows)
   size_t acc;     // s32 [kHeadDigits][M][N]
   size_t list;    // s32 [M*N] flagged elements (i*N + j)
   size_t count;   // s32
@@ -82,7 +82,7 @@ static HeadWsLayout ws_layout(long long M, int K, int N) {
   L.rsum = off;
   off = a256(off + (size_t)4 * kHeadDigits * M);
   L.rstat = off;
-  off = a256(off + (size_t)8 * 4 * M);
+  off = a256(off + (size_t)8 * 8 * M);
   L.acc = off;
   off = a256(off + (size_t)4 * kHeadDigits * M * N);
   L.list = off;
@@ -101,11 +101,13 @@ QC_DEV void head_digits(double r, int (&D)[kHeadDigits]) {
   double v = r * 64.0;
 #pragma unroll
   for (int s = 0; s < kHeadDigits; ++s) {
-    const double q = rint(v);
+    const double q = (v + 6755399441055744.0) - 6755399441055744.0;   // rint, |v| <= 64
     D[s] = (int)q;
     v = (v - q) * 128.0;
   }
 }
+
+QC_DEV double up(double v) { return v * (1.0 + 0x1p-40); }   // generous upward padding
 
 // 2^n as f64 for |n| < 1000 (exact, no library call)
 QC_DEV double pow2(int n) { return __longlong_as_double((long long)(1023 + n) << 52); }
@@ -174,11 +176,14 @@ __global__ void head_prep_cols(const float* __restrict__ w, int K, int N, uint8_
       pre += cs[d];   // B_d holds E_0..E_d
       csum[(size_t)d * N + j] = pre;
     }
-    double* cst = reinterpret_cast<double*>(base + L.cstat) + (size_t)j * 4;
-    cst[0] = (double)f;
-    cst[1] = l1;
-    cst[2] = sqrt(l2);
-    cst[3] = sqrt(rho);
+    // certificate column factors (see head_combine): 2^f, |E|_2 2^f, |w|_1, 2^(f-49), |w|_2
+    double* cst = reinterpret_cast<double*>(base + L.cstat) + (size_t)j * 8;
+    cst[0] = pow2(f);
+    cst[1] = up(sqrt(rho)) * pow2(f);
+    cst[2] = up(l1);
+    cst[3] = pow2(f - 49);
+    cst[4] = up(sqrt(l2));
+    cst[5] = cst[6] = cst[7] = 0.0;
     reinterpret_cast<double*>(base + L.ones)[j] = 1.0;
     reinterpret_cast<int*>(base + L.zeros64)[j] = 64;
   }
@@ -203,13 +208,13 @@ __global__ void __launch_bounds__(32 * kHeadSliceWarps)
   const size_t ldp = a16((size_t)kHeadDigits * K);
   uint8_t* prow = ws + L.planes + (size_t)i * ldp;
   int* rsum = reinterpret_cast<int*>(ws + L.rsum);
-  double* rst = reinterpret_cast<double*>(ws + L.rstat) + (size_t)i * 4;
+  double* rst = reinterpret_cast<double*>(ws + L.rstat) + (size_t)i * 8;
   const int seg = (int)(i / h.seg_rows), r = (int)(i - (long long)seg * h.seg_rows);
   if (r >= h.seg_valid) {   // padding row: zero digits
     for (int k = lane; k < kHeadDigits * K; k += 32) prow[k] = 64;
     if (lane == 0) {
       for (int d = 0; d < kHeadDigits; ++d) rsum[(size_t)d * h.M + i] = 64 * (d + 1) * K;
-      rst[0] = rst[1] = rst[2] = rst[3] = 0.0;
+      for (int u = 0; u < 8; ++u) rst[u] = 0.0;
     }
     return;
   }
@@ -265,10 +270,15 @@ __global__ void __launch_bounds__(32 * kHeadSliceWarps)
       pre += cs[d];
       rsum[(size_t)d * h.M + i] = pre;
     }
-    rst[0] = (double)e;
-    rst[1] = l1;
-    rst[2] = sqrt(l2);
-    rst[3] = sqrt((double)rho);
+    // certificate row factors (see head_combine)
+    const double Kd = (double)K;
+    rst[0] = pow2(e - 12);
+    rst[1] = 6.04 * up(sqrt((double)rho)) * pow2(e - 61);
+    rst[2] = pow2(e - 49);
+    rst[3] = up(l1) + Kd * pow2(e - 49);
+    rst[4] = (double)kHeadDigits * pow2(e - 65);
+    rst[5] = (Kd - 1.0) * 0x1p-53 * up(sqrt(l2));
+    rst[6] = rst[7] = 0.0;
   }
 }
 
@@ -286,82 +296,87 @@ struct HeadCombine {
   int* count;
 };
 
-QC_DEV double up(double v) { return v * (1.0 + 0x1p-40); }   // generous upward padding
+// 4 consecutive columns per thread over kCombineRows rows.  With the per-row
+// (r*) and per-column (c*) factors prepared by the slicing kernels:
+//   S^ = s r0 c0 with s = sum_d acc_d 2^-7d             (r0 c0 = 2^(e+f-12), exact)
+//   T1 = r1 c1      dropped pairs: 6.04 |D|_2 |E|_2 2^(e+f-61)  (Cauchy-Schwarz)
+//   T2 = r2 c2 + r3 c3    truncation: 2^(e-49) |w|_1 + 2^(f-49) (|x|_1 + K 2^(e-49))
+//   T3 = r4 c0 (|acc_0| + 65 K)    combination: 7 2^(e+f-65) sum_d |acc_d| 2^-7d
+//   T4 = r5 c4      the reference's rounding: (K-1) 2^-53 |x|_2 |w|_2
+constexpr int kCombineRows = 16;   // rows per thread (column factors stay in registers)
 
-// 4 consecutive outputs (i, j..j+3) per thread
-__global__ void __launch_bounds__(256) head_combine(const HeadCombine c) {
-  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int nq = c.N >> 2;
-  if (q >= c.M * nq) return;
-  const long long i = q / nq;
-  const int j0 = (int)(q - i * nq) * 4;
-  const int seg = (int)(i / c.seg_rows), r = (int)(i - (long long)seg * c.seg_rows);
-  if (r >= c.seg_valid) return;
-  const size_t mn = (size_t)c.M * c.N;
-  const size_t base = (size_t)i * c.N + j0;
-  double s[4] = {0.0, 0.0, 0.0, 0.0}, sabs[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int d = kHeadDigits - 1; d >= 0; --d) {   // small terms first
-    const int4 a4 = __ldcs(reinterpret_cast<const int4*>(c.acc + d * mn + base));
-    const double sc = pow2(-7 * d);
-    const int av[4] = {a4.x, a4.y, a4.z, a4.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      s[u] += (double)av[u] * sc;
-      sabs[u] += fabs((double)av[u]) * sc;
-    }
-  }
-  const double e = c.rstat[i * 4], xl1 = up(c.rstat[i * 4 + 1]), xl2 = up(c.rstat[i * 4 + 2]);
-  const double rx = c.rstat[i * 4 + 3];
-  const double K = (double)c.K;
-  const long long orow = c.out_row0 ? c.out_row0[seg] + r : i;
-  float res[4];
-  bool all_ok = true;
+__global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= c.N) return;
+  // the thread's 4 columns: certificate factors once
+  double c0[4], c1[4], c2[4], c3[4], c4[4];
+  float bj[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int j = j0 + u;
-    const double f = c.cstat[(size_t)j * 4], wl1 = up(c.cstat[(size_t)j * 4 + 1]),
-                 wl2 = up(c.cstat[(size_t)j * 4 + 2]);
-    const int ef = (int)e + (int)f;
-    const double S = s[u] * pow2(ef - 12);
-    // T1: dropped diagonals d >= kHeadDigits (all their digits have s, t >= 1):
-    // sum_k |D_s E_t| <= |D_s|_2 |E_t|_2 <= rho_x rho_w (Cauchy-Schwarz), and
-    // sum_{d>=7} pairs(d) 2^(-12-7d) <= 6.04 2^-61
-    const double t1 = up(rx * c.cstat[(size_t)j * 4 + 3]) * 6.04 * pow2(ef - 61);
-    // T2: truncation |dx| <= 2^(e-49), |dw| <= 2^(f-49)
-    const double t2 = pow2((int)e - 49) * wl1 + pow2((int)f - 49) * (xl1 + K * pow2((int)e - 49));
-    // T3: f64 combination, kHeadDigits additions
-    const double t3 = sabs[u] * (double)kHeadDigits * pow2(ef - 12 - 53);
-    // T4: the reference's sequential rounding (Cauchy-Schwarz bound on sum |x w|)
-    const double t4 = (K - 1.0) * 0x1p-53 * xl2 * wl2;
-    const double E = up(t1 + t2 + t3 + t4) * (1.0 + 0x1p-20);
-    const double aS = fabs(S);
-    bool ok = aS < 0x1p126 && aS > 0x1p-125;
-    float y = 0.0f;
-    if (ok) {
-      y = __double2float_rn(S);
-      const uint32_t yb = __float_as_uint(y);
-      const float dn = __uint_as_float(y > 0.0f ? yb - 1u : yb + 1u);   // toward -inf
-      const float upn = __uint_as_float(y > 0.0f ? yb + 1u : yb - 1u);  // toward +inf
-      const double lo = 0.5 * ((double)y + (double)dn);
-      const double hi = 0.5 * ((double)y + (double)upn);
-      ok = (S - E > lo) && (S + E < hi);
-    }
-    if (ok) {
-      res[u] = c.bias ? __fadd_rn(y, c.bias[j]) : y;
-    } else {
-      all_ok = false;
-      res[u] = 0.0f;
-      const int slot = atomicAdd(c.count, 1);
-      c.list[slot] = (int)(i * c.N + j);
-    }
+    const double* cf = c.cstat + (size_t)(j0 + u) * 8;
+    c0[u] = cf[0];
+    c1[u] = cf[1];
+    c2[u] = cf[2];
+    c3[u] = cf[3];
+    c4[u] = cf[4];
+    bj[u] = c.bias ? c.bias[j0 + u] : 0.0f;
   }
-  float* op = c.out + orow * c.ldo + j0;
-  if (all_ok && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
-    *reinterpret_cast<float4*>(op) = make_float4(res[0], res[1], res[2], res[3]);
-  } else {
+  const size_t mn = (size_t)c.M * c.N;
+  const double k65 = 65.0 * (double)c.K;
+  const long long i_end = min((long long)(blockIdx.y + 1) * kCombineRows, c.M);
+  for (long long i = (long long)blockIdx.y * kCombineRows; i < i_end; ++i) {
+    const int seg = (int)(i / c.seg_rows), r = (int)(i - (long long)seg * c.seg_rows);
+    if (r >= c.seg_valid) continue;
+    const size_t base = (size_t)i * c.N + j0;
+    int4 a4[kHeadDigits];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) op[u] = res[u];   // flagged ones are rewritten by the fallback
+    for (int d = 0; d < kHeadDigits; ++d)
+      a4[d] = __ldcs(reinterpret_cast<const int4*>(c.acc + d * mn + base));
+    const double* rf = c.rstat + i * 8;
+    const double r0 = rf[0], r1 = rf[1], r2 = rf[2], r3 = rf[3], r4 = rf[4], r5 = rf[5];
+    const long long orow = c.out_row0 ? c.out_row0[seg] + r : i;
+    float res[4];
+    bool all_ok = true;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double s = 0.0;
+#pragma unroll
+      for (int d = kHeadDigits - 1; d >= 0; --d) {   // small terms first
+        const int av = u == 0 ? a4[d].x : u == 1 ? a4[d].y : u == 2 ? a4[d].z : a4[d].w;
+        s = fma(i2d_alu(av), pow2(-7 * d), s);   // exact products, rounded sums (T3)
+      }
+      const int a0 = u == 0 ? a4[0].x : u == 1 ? a4[0].y : u == 2 ? a4[0].z : a4[0].w;
+      const double S = (s * r0) * c0[u];
+      const double E = (r1 * c1[u] + r2 * c2[u] + r3 * c3[u] +
+                        r4 * c0[u] * (fabs(i2d_alu(a0)) + k65) + r5 * c4[u]) * (1.0 + 0x1p-20);
+      const double aS = fabs(S);
+      bool ok = aS < 0x1p126 && aS > 0x1p-125;
+      float y = 0.0f;
+      if (ok) {
+        y = __double2float_rn(S);
+        const uint32_t yb = __float_as_uint(y);
+        const float dn = __uint_as_float(y > 0.0f ? yb - 1u : yb + 1u);   // toward -inf
+        const float upn = __uint_as_float(y > 0.0f ? yb + 1u : yb - 1u);  // toward +inf
+        const double lo = 0.5 * ((double)y + (double)dn);
+        const double hi = 0.5 * ((double)y + (double)upn);
+        ok = (S - E > lo) && (S + E < hi);
+      }
+      if (ok) {
+        res[u] = c.bias ? __fadd_rn(y, bj[u]) : y;
+      } else {
+        all_ok = false;
+        res[u] = 0.0f;
+        const int slot = atomicAdd(c.count, 1);
+        c.list[slot] = (int)(i * c.N + j0 + u);
+      }
+    }
+    float* op = c.out + orow * c.ldo + j0;
+    if (all_ok && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
+      *reinterpret_cast<float4*>(op) = make_float4(res[0], res[1], res[2], res[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) op[u] = res[u];   // flagged ones are rewritten by the fallback
+    }
   }
 }
 
@@ -484,7 +499,8 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
                 reinterpret_cast<const double*>(prep + P.cstat),
                 reinterpret_cast<const int*>(ws + W.acc), g->bias, g->out, g->ldo, g->out_row0,
                 reinterpret_cast<int*>(ws + W.list), reinterpret_cast<int*>(ws + W.count)};
-  head_combine<<<(unsigned)((M * (N / 4) + 255) / 256), 256, 0, st>>>(c);
+  head_combine<<<dim3((unsigned)((N / 4 + 127) / 128),
+                     (unsigned)((M + kCombineRows - 1) / kCombineRows)), 128, 0, st>>>(c);
   rc = launch_status();
   if (rc) return rc;
   HeadFallback fb{g->x, g->ldx, g->x_row0, g->seg_rows, N, K,
