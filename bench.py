@@ -347,7 +347,7 @@ def run_ours(args):
     # Kernel rooflines from one extra, separately profiled step (CUDA events
     # around every u8 GEMM and every quantizer call on the engine's stream), so
     # the timed region above carries no per-launch events.
-    eng.gemm_profile, eng.quant_profile, eng.phase_profile = [], [], []
+    eng.gemm_profile, eng.quant_profile, eng.phase_profile, eng.host_profile = [], [], [], []
     eng.head_fallbacks.zero_()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
@@ -356,6 +356,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     prof_step = p0.elapsed_time(p1) / 1e3
     gprof, qprof, pprof = eng.gemm_profile, eng.quant_profile, eng.phase_profile
+    host_loop_ms = sum(eng.host_profile) * 1e3
+    eng.host_profile = None
     head_fb = int(eng.head_fallbacks.item()) / float(T * B * S * d)
     eng.gemm_profile = eng.quant_profile = eng.phase_profile = None
 
@@ -449,6 +451,7 @@ def run_ours(args):
         "roofline_kernels": {"act_quant": roof_quant, "gemm_u8": roof_gemm},
         "profiled_step_ms": {"total": round(prof_step * 1e3, 3), **phases},
         "head_exact_fallback_fraction": head_fb,
+        "host_block_loop_ms": round(host_loop_ms, 3),
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_vps, "unit": "videos/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

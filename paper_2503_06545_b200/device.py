@@ -37,10 +37,16 @@ def pow2_floor(n: int) -> int:
     return 1 << (int(n).bit_length() - 1)
 
 
+_DEV = None
+
+
 def _dev() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("QuantCache B200 kernels need a CUDA device (no CPU fallback)")
-    return torch.device("cuda", torch.cuda.current_device())
+    global _DEV
+    if _DEV is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("QuantCache B200 kernels need a CUDA device (no CPU fallback)")
+        _DEV = torch.device("cuda", torch.cuda.current_device())
+    return _DEV
 
 
 @dataclass

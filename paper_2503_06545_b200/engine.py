@@ -25,6 +25,7 @@ values (D, S, V) stay on device until the end of the run.
 from __future__ import annotations
 
 import contextlib
+import time
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
@@ -159,6 +160,8 @@ class QuantCacheEngine:
         self.gemm_profile: Optional[list] = None   # set to [] to time every u8 GEMM
         self.quant_profile: Optional[list] = None  # set to [] to time every act_quant
         self.phase_profile: Optional[list] = None  # set to [] to time the other phases
+        self.host_profile: Optional[list] = None   # set to []: host s from plan sync to the
+                                                   # end of the block loop, per step
         self._upload_weights(act_absmax or {})
         self._alloc()
 
@@ -545,16 +548,21 @@ class QuantCacheEngine:
             ph.__exit__(None, None, None)
             self.pol_host.copy_(self.pol, non_blocking=True)
             st.synchronize()
+            if self.host_profile is not None:
+                t_sync = time.perf_counter()
             raw = self.pol_host.numpy()
             plans = [N.QcbPolicyVideo.from_buffer_copy(
                 raw[v * self.pol_size:(v + 1) * self.pol_size].tobytes()) for v in range(nv)]
             for vs in vids:
                 vs.seen += 1
+            # plain Python copies of the decisions (ctypes field access is slow)
+            act_tab = [list(p.action) for p in plans]
+            abits_of = [int(p.abits) for p in plans]
             # ---------------- execute blocks ----------------
             cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
             feats = [] if collect_features is not None else None
             for l in range(L):
-                acts = [p.action[l] for p in plans]
+                acts = [act_tab[v][l] for v in range(nv)]
                 outs = list(cur)
                 rec = []
                 for v in range(nv):
@@ -570,7 +578,7 @@ class QuantCacheEngine:
                     # group recomputing videos by activation bits
                     groups: Dict[int, List[int]] = {}
                     for v in rec:
-                        groups.setdefault(plans[v].abits, []).append(v)
+                        groups.setdefault(abits_of[v], []).append(v)
                     need_d = [acts[v] == N.ACT_RECOMPUTE and vids[v].prev[l] is not None
                               for v in range(nv)]
                     tabl = []
@@ -597,7 +605,7 @@ class QuantCacheEngine:
 
                 # host mirror of the cache / prev references (schedule.py:349-351)
                 for v, vs in enumerate(vids):
-                    if plans[v].action[l] == N.ACT_RECOMPUTE and t > 0:
+                    if acts[v] == N.ACT_RECOMPUTE and t > 0:
                         vs.pool.dec(vs.cache[l])
                         vs.cache[l] = vs.pool.inc(outs[v])
                     vs.pool.dec(vs.prev[l])
@@ -607,6 +615,8 @@ class QuantCacheEngine:
                 if feats is not None:
                     feats.append(torch.stack([self.slot_view(s) for s in cur]).cpu().numpy())
             # observe_block for every layer of the step (schedule.py:330-351)
+            if self.host_profile is not None:
+                self.host_profile.append(time.perf_counter() - t_sync)
             N.check(lib.qcb_policy_observe_all(pol, nv, L, t, self.thc, N.ptr(self.hlc), sp),
                     "observe_all")
             Dv.count(1)
