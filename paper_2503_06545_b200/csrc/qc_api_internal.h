@@ -1,5 +1,6 @@
 // Internal launcher declarations shared by the .cu translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/qcb200.h"
@@ -32,6 +33,8 @@ int pick_block_n(int N);
 int gemm_u8_launch(const QcbGemm* g, cudaStream_t st);
 int gemm_f64_launch(const QcbGemmF64* g, cudaStream_t st);
 int head_prep_launch(const float* w, int K, int N, void* prep, cudaStream_t st);
+// 2-D u8 tensor map [rows][ld] (K valid columns), box kBlockK x box_rows, SWIZZLE_128B
+int make_map_u8(CUtensorMap* map, const void* base, int rows, int K, long long ld, int box_rows);
 int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st);
 int act_quant_launch(const QcbActQuant* q, cudaStream_t st);
 int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st);

@@ -384,7 +384,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 // 2-D u8 K-major operand [rows][ld] (K valid columns), box 128 bytes x box_rows.
-static int make_map_u8(CUtensorMap* map, const void* base, int rows, int K, long long ld,
+int make_map_u8(CUtensorMap* map, const void* base, int rows, int K, long long ld,
                        int box_rows) {
   auto enc = get_encode_fn();
   if (!enc) return QCB_ERR_CUDA;

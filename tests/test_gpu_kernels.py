@@ -326,13 +326,15 @@ class TestFp:
             w = rng.standard_normal((k, n)).astype(np.float32)
             assert np.array_equal(D.gemm_f64(t(a), t(w)).cpu().numpy(), O.seq_mm(a, w))
 
-    @pytest.mark.parametrize("case", ["normal", "dynamic_range", "cancellation"])
+    @pytest.mark.parametrize("case", ["normal", "dynamic_range", "cancellation", "odd_k"])
     def test_head_gemm_certified_exact(self, D, case):
         """model.py:228 noise head via certified int8 digit GEMMs == mm + bias bit
         for bit (tensor.py:43-60), incl. padded segments and the exact fallback."""
         from paper_2503_06545_b200 import _native as Nat
-        rng = np.random.default_rng({"normal": 1, "dynamic_range": 2, "cancellation": 3}[case])
-        nseg, seg_rows, seg_valid, K, N = 2, 160, 150, 1152, 264
+        rng = np.random.default_rng({"normal": 1, "dynamic_range": 2, "cancellation": 3,
+                                     "odd_k": 4}[case])
+        nseg, seg_rows, seg_valid, N = 2, 160, 150, 264
+        K = 200 if case == "odd_k" else 1152
         x = rng.standard_normal((nseg * seg_rows, K)).astype(np.float32) * 3
         w = (rng.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32)
         b = (rng.standard_normal(N) * 0.1).astype(np.float32)
@@ -359,7 +361,7 @@ class TestFp:
         assert np.array_equal(got[valid].view(np.int32), want[valid].view(np.int32)), \
             (case, int(cnt.item()))
         # the oracle's sequential mm on a few rows (pins gemm_f64 too)
-        rows = valid[[0, 3, 5, 9, 151]] if case != "normal" else valid[:4]
+        rows = valid[[0, 3, 5, 9, 151]] if case not in ("normal", "odd_k") else valid[:4]
         ref = O.seq_mm(x[rows], w) + b
         assert np.array_equal(got[rows], ref)
         if case == "cancellation":
