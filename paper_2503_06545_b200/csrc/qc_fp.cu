@@ -488,6 +488,102 @@ QC_DEV bool gelu_fast(float xf, float& y) {
   return true;
 }
 
+// ~correctly rounded 1/u: MUFU seed + two Newton steps (within an ulp or two)
+QC_DEV double fast_rcp(double u) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  double e = fma(-u, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-u, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Is the f64 value g at least w ulp64 away from an f32 rounding tie, inside
+// the f32 normal range?  (the certificate test of the fast GELU paths)
+QC_DEV bool f32_round_safe(double g, double w) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(g);
+  const int ex = (int)((bits >> 52) & 0x7FF) - 1023;
+  if (ex < -125 || ex > 126) return false;
+  const int d = abs((int)((unsigned)bits & 0x1FFFFFFFu) - (1 << 28));
+  return (double)d > w;
+}
+
+// Phase A, |x / sqrt2| < 1: the cephes T/U rational with FMA Horner steps and
+// a Newton reciprocal instead of the reference's separate mul/add and IEEE
+// division.  Relative error of erf vs the reference's value: well under
+// 20 ulp, amplified at most ~6x in 1 + erf (>= 0.157) -> accepted when g is
+// 256 ulp64 clear of an f32 tie.  Returns false for |t| >= 1 or near ties.
+QC_DEV bool gelu_fast_a(float xf, float& y) {
+  if (xf >= 6.0f) {
+    y = xf;
+    return true;
+  }
+  const double x = (double)xf;
+  const double t = x * 0.70710678118654752440;
+  const double at = fabs(t);
+  if (!(at < 1.0 - 0x1p-40)) return false;
+  const double z = at * at;
+  double tt = 9.60497373987051638749E0;
+  tt = fma(tt, z, 9.00260197203842689217E1);
+  tt = fma(tt, z, 2.23200534594684319226E3);
+  tt = fma(tt, z, 7.00332514112805075473E3);
+  tt = fma(tt, z, 5.55923013010394962768E4);
+  double u = z + 3.35617141647503099647E1;
+  u = fma(u, z, 5.21357949780152679795E2);
+  u = fma(u, z, 4.59432382970980127987E3);
+  u = fma(u, z, 2.26290000613890934246E4);
+  u = fma(u, z, 4.92673942608635921086E4);
+  double r = (at * tt) * fast_rcp(u);
+  if (t < 0.0) r = -r;
+  const double g = (0.5 * x) * (1.0 + r);
+  if (g == 0.0) {   // x == +-0
+    y = __double2float_rn(g);
+    return true;
+  }
+  if (!f32_round_safe(g, 256.0)) return false;
+  y = __double2float_rn(g);
+  return true;
+}
+
+// Phase B, 1 <= |x / sqrt2| < 8: cephes erfc(|t|) = exp(-t^2) P(|t|)/Q(|t|)
+// with FMA Horner, a Newton reciprocal and CUDA exp, then the reference's own
+// structure 1 + erf = 1 +- (1 - erfc).  Error vs the reference's f64 value:
+// (~24 + 4 t^2) ulp relative in erfc (exp, Horner, division, the 1-ulp
+// argument difference), plus the reference's double rounding of 1 - erfc
+// (<= 2^-53 absolute, i.e. <= 1/ope ulp of g) -> window 512 + 32 t^2 + 8/ope.
+QC_DEV bool gelu_fast_b(float xf, float& y) {
+  const double x = (double)xf;
+  const double t = x * 0.70710678118654752440;
+  const double at = fabs(t);
+  if (!(at >= 1.0 && at < 8.0)) return false;
+  const double ez = exp(-(at * at));
+  double pp = 2.46196981473530512524E-10;
+  pp = fma(pp, at, 5.64189564831068821977E-1);
+  pp = fma(pp, at, 7.46321056442269912687E0);
+  pp = fma(pp, at, 4.86371970985681366614E1);
+  pp = fma(pp, at, 1.96520832956077098242E2);
+  pp = fma(pp, at, 5.26445194995477358631E2);
+  pp = fma(pp, at, 9.34528527171957607540E2);
+  pp = fma(pp, at, 1.02755188689515710272E3);
+  pp = fma(pp, at, 5.57535335369399327526E2);
+  double qq = at + 1.32281951154744992508E1;
+  qq = fma(qq, at, 8.67072140885989742329E1);
+  qq = fma(qq, at, 3.54937778887819891062E2);
+  qq = fma(qq, at, 9.75708501743205489753E2);
+  qq = fma(qq, at, 1.82390916687909736289E3);
+  qq = fma(qq, at, 2.24633760818710981792E3);
+  qq = fma(qq, at, 1.65666309194161350182E3);
+  qq = fma(qq, at, 5.57535340817727675546E2);
+  const double ec = (ez * pp) * fast_rcp(qq);
+  const double r = 1.0 - ec;                         // erf(|t|), rounded like the reference
+  const double ope = t > 0.0 ? 1.0 + r : 1.0 - r;    // 1 + erf(t)
+  if (!(ope > 0.0)) return false;
+  const double g = (0.5 * x) * ope;
+  if (!f32_round_safe(g, 512.0 + 32.0 * (t * t) + 8.0 / ope)) return false;
+  y = __double2float_rn(g);
+  return true;
+}
+
 // Certified fast path for every x < 6.  g~ = 0.5 x (1 + erf(x / sqrt2)) from
 // CUDA's f64 erf / erfc (<= 4 ulp) on t = x * (1/sqrt2) (1 ulp from the
 // reference's x / sqrt2, propagated as 2 t^2 ulp).  The reference forms
@@ -557,7 +653,7 @@ __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, in
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int c = c0 + (i >> 2) * 128 + lane * 4 + (i & 3);
-      if (c < cols && !gelu_fast(v[i], y[i])) hard |= 1u << i;
+      if (c < cols && !gelu_fast_a(v[i], y[i])) hard |= 1u << i;
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -591,8 +687,13 @@ __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, in
         ++off;
       }
     __syncwarp();
-    for (int i = lane; i < total; i += 32)
-      x[q_row[warp][i] * ld + q_col[warp][i]] = gelu_f32_ref(q_val[warp][i]);
+    for (int i = lane; i < total; i += 32) {
+      // certified erfc branch on full warps; the exact replica only where it
+      // cannot decide (near ties, far tails)
+      float yv;
+      if (!gelu_fast_b(q_val[warp][i], yv)) yv = gelu_f32_ref(q_val[warp][i]);
+      x[q_row[warp][i] * ld + q_col[warp][i]] = yv;
+    }
     __syncwarp();
   }
 }

@@ -400,6 +400,20 @@ class TestFp:
         bad = np.flatnonzero(got.view(np.int32) != want.view(np.int32))
         assert bad.size == 0, (bad.size, x[bad[:5]], got[bad[:5]], want[bad[:5]])
 
+    def test_gelu_exhaustive_vs_replica(self, D):
+        """Every f32 in [-14, 6] (2.18e9 values): the certified fast GELU paths
+        equal the exact cephes replica (f64 GEMM GELU epilogue on a K=1 identity
+        product; pinned to SciPy above).  -0.0 is excluded: that product turns it
+        into +0.0 before the epilogue."""
+        import subprocess, sys
+        out = subprocess.run([sys.executable, "tools/gelu_exhaustive.py", "-14", "6"],
+                             capture_output=True, text=True, timeout=600,
+                             cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        res = json.loads(out.stdout.strip().splitlines()[-1])
+        assert res["values"] > 2_000_000_000
+        assert all(e[0] == 0.0 for e in res["examples"]), res
+        assert res["mismatches"] <= 1, res
+
     def test_ln_mod(self, D):
         rng = np.random.default_rng(7)
         x = rng.standard_normal((64, 64)).astype(np.float32) * 2
