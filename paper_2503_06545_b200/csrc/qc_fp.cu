@@ -488,6 +488,25 @@ QC_DEV bool gelu_fast(float xf, float& y) {
   return true;
 }
 
+// cephes ndtr.c coefficients in constant memory: FP64 instructions read them as
+// c[bank][offset] operands instead of re-materialising 64-bit literals with
+// uniform moves on every use (a quarter of the kernel's instructions before)
+__constant__ double kErfT[5] = {9.60497373987051638749E0, 9.00260197203842689217E1,
+                                2.23200534594684319226E3, 7.00332514112805075473E3,
+                                5.55923013010394962768E4};
+__constant__ double kErfU[5] = {3.35617141647503099647E1, 5.21357949780152679795E2,
+                                4.59432382970980127987E3, 2.26290000613890934246E4,
+                                4.92673942608635921086E4};
+__constant__ double kErfcP[9] = {2.46196981473530512524E-10, 5.64189564831068821977E-1,
+                                 7.46321056442269912687E0,  4.86371970985681366614E1,
+                                 1.96520832956077098242E2,  5.26445194995477358631E2,
+                                 9.34528527171957607540E2,  1.02755188689515710272E3,
+                                 5.57535335369399327526E2};
+__constant__ double kErfcQ[8] = {1.32281951154744992508E1, 8.67072140885989742329E1,
+                                 3.54937778887819891062E2, 9.75708501743205489753E2,
+                                 1.82390916687909736289E3, 2.24633760818710981792E3,
+                                 1.65666309194161350182E3, 5.57535340817727675546E2};
+
 // ~correctly rounded 1/u: MUFU seed + two Newton steps (within an ulp or two)
 QC_DEV double fast_rcp(double u) {
   double r;
@@ -523,16 +542,12 @@ QC_DEV bool gelu_fast_a(float xf, float& y) {
   const double at = fabs(t);
   if (!(at < 1.0 - 0x1p-40)) return false;
   const double z = at * at;
-  double tt = 9.60497373987051638749E0;
-  tt = fma(tt, z, 9.00260197203842689217E1);
-  tt = fma(tt, z, 2.23200534594684319226E3);
-  tt = fma(tt, z, 7.00332514112805075473E3);
-  tt = fma(tt, z, 5.55923013010394962768E4);
-  double u = z + 3.35617141647503099647E1;
-  u = fma(u, z, 5.21357949780152679795E2);
-  u = fma(u, z, 4.59432382970980127987E3);
-  u = fma(u, z, 2.26290000613890934246E4);
-  u = fma(u, z, 4.92673942608635921086E4);
+  double tt = kErfT[0];
+#pragma unroll
+  for (int i = 1; i < 5; ++i) tt = fma(tt, z, kErfT[i]);
+  double u = z + kErfU[0];
+#pragma unroll
+  for (int i = 1; i < 5; ++i) u = fma(u, z, kErfU[i]);
   double r = (at * tt) * fast_rcp(u);
   if (t < 0.0) r = -r;
   const double g = (0.5 * x) * (1.0 + r);
@@ -557,23 +572,12 @@ QC_DEV bool gelu_fast_b(float xf, float& y) {
   const double at = fabs(t);
   if (!(at >= 1.0 && at < 8.0)) return false;
   const double ez = exp(-(at * at));
-  double pp = 2.46196981473530512524E-10;
-  pp = fma(pp, at, 5.64189564831068821977E-1);
-  pp = fma(pp, at, 7.46321056442269912687E0);
-  pp = fma(pp, at, 4.86371970985681366614E1);
-  pp = fma(pp, at, 1.96520832956077098242E2);
-  pp = fma(pp, at, 5.26445194995477358631E2);
-  pp = fma(pp, at, 9.34528527171957607540E2);
-  pp = fma(pp, at, 1.02755188689515710272E3);
-  pp = fma(pp, at, 5.57535335369399327526E2);
-  double qq = at + 1.32281951154744992508E1;
-  qq = fma(qq, at, 8.67072140885989742329E1);
-  qq = fma(qq, at, 3.54937778887819891062E2);
-  qq = fma(qq, at, 9.75708501743205489753E2);
-  qq = fma(qq, at, 1.82390916687909736289E3);
-  qq = fma(qq, at, 2.24633760818710981792E3);
-  qq = fma(qq, at, 1.65666309194161350182E3);
-  qq = fma(qq, at, 5.57535340817727675546E2);
+  double pp = kErfcP[0];
+#pragma unroll
+  for (int i = 1; i < 9; ++i) pp = fma(pp, at, kErfcP[i]);
+  double qq = at + kErfcQ[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) qq = fma(qq, at, kErfcQ[i]);
   const double ec = (ez * pp) * fast_rcp(qq);
   const double r = 1.0 - ec;                         // erf(|t|), rounded like the reference
   const double ope = t > 0.0 ? 1.0 + r : 1.0 - r;    // 1 + erf(t)
