@@ -370,6 +370,9 @@ def run_ours(args):
     traces = [eng.traces_of(v) for v in vids_all]
     recs = [r for trs in traces for tv in trs for r in tv if r.layer != "head"]
     frac = sum(r.action == "recompute" for r in recs) / max(1, len(recs))
+    prune_frac = sum(r.action == "prune" for r in recs) / max(1, len(recs))
+    # SRAP similarities evaluated (one reduction segment each) per video-step
+    srap_per_step = sum(r.s is not None for r in recs) / max(1, len(recs) / cfg.num_blocks)
     executed = sum(r.macs for trs in traces for tv in trs for r in tv)
     # Kernel rooflines from one extra, separately profiled step (CUDA events
     # around every u8 GEMM and every quantizer call on the engine's stream), so
@@ -475,6 +478,8 @@ def run_ours(args):
                                   "v_low": th.v_low, "v_high": th.v_high}},
         "s_per_video": elapsed / (args.steps * B),
         "recompute_fraction": frac,
+        "prune_fraction": prune_frac,
+        "srap_segments_per_video_step": srap_per_step,
         "executed_bit_macs_per_video": executed / (args.steps * B),
         "roofline": dominant,
         "roofline_kernels": {"act_quant": roof_quant, "gemm_u8": roof_gemm},

@@ -244,9 +244,13 @@ typedef struct QcbFeat {
 /* sum|out-ref| and sum (out-prev)^2 per segment -> res[seg*2 + {0,1}] */
 int qcb_reduce_hlc(QcbFeat out, QcbFeat ref, QcbFeat prev, int rows, int cols, int nseg,
                    const int* seg_active, double* res, void* workspace, void* stream);
-/* <a,b>, <a,a>, <b,b> per segment -> res[seg*3 + {0,1,2}] */
+/* <a,b>, <a,a>, <b,b> per segment -> res[seg*3 + {0,1,2}].  dup_src
+ * (nullable, int64 [nseg]): index of the first segment with the same (a, b)
+ * rows; only those representatives are reduced and the others copied (results
+ * are identical: the reduction order depends only on rows/cols/nseg). */
 int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nseg,
-                    const int* seg_active, double* res, void* workspace, void* stream);
+                    const int* seg_active, const long long* dup_src, double* res,
+                    void* workspace, void* stream);
 /* sum|x - h| per segment -> res[seg] */
 int qcb_reduce_l1(QcbFeat x, QcbFeat h, int rows, int cols, int nseg, double* res,
                   void* workspace, void* stream);

@@ -135,7 +135,7 @@ def lib():
         "qcb_ddpm_step": [P(QcbDdpm), vp],
         "qcb_gelu_inplace": [vp, i64, i32, i32, vp],
         "qcb_reduce_hlc": [QcbFeat, QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp, vp],
-        "qcb_reduce_srap": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp, vp],
+        "qcb_reduce_srap": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp, vp, vp],
         "qcb_reduce_l1": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp],
         "qcb_policy_plan_reuse": [vp, i32, i32, i32, QcbThresholds, vp],
         "qcb_policy_sim_mask": [vp, i32, i32, QcbThresholds, vp, vp],

@@ -182,8 +182,30 @@ using namespace qc;
 constexpr int kMaxSegs = 4096;
 
 extern "C" size_t qcb_reduce_workspace_bytes(int nseg) {
-  return (size_t)kMaxSegs * sizeof(int) + (size_t)nseg * kMaxChunks * 3 * sizeof(double) + 256;
+  return (size_t)kMaxSegs * sizeof(int) + (size_t)nseg * kMaxChunks * 3 * sizeof(double) +
+         (size_t)nseg * sizeof(int) + 256;
 }
+
+namespace qc {
+// SRAP de-duplication inside one launch: segments with the same (a, b) rows
+// (a pruned chain compares one slot with itself for many layers) have the same
+// result -- the chunking and the fixed-order final sum depend only on
+// rows/cols/nseg -- so only representatives dup[s] == s are reduced.
+__global__ void srap_need_k(const int* seg_active, const long long* dup, int nseg, int* need) {
+  for (int s = threadIdx.x; s < nseg; s += blockDim.x) need[s] = 0;
+  __syncthreads();
+  for (int s = threadIdx.x; s < nseg; s += blockDim.x)
+    if (!seg_active || seg_active[s]) need[(int)dup[s]] = 1;
+}
+
+__global__ void srap_copy_k(const int* seg_active, const long long* dup, int nseg, double* res) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const int d = (int)dup[s];
+  if (d != s && (!seg_active || seg_active[s]))
+    for (int i = 0; i < 3; ++i) res[(size_t)s * 3 + i] = res[(size_t)d * 3 + i];
+}
+}  // namespace qc
 
 template <int KIND, int NV>
 static int launch_reduce(QcbFeat a, QcbFeat b, QcbFeat c, int rows, int cols, int nseg,
@@ -204,8 +226,19 @@ extern "C" int qcb_reduce_hlc(QcbFeat out, QcbFeat ref, QcbFeat prev, int rows, 
 }
 
 extern "C" int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nseg,
-                               const int* seg_active, double* res, void* ws, void* stream) {
-  return launch_reduce<1, 3>(a, b, a, rows, cols, nseg, seg_active, res, ws, stream);
+                               const int* seg_active, const long long* dup_src, double* res,
+                               void* ws, void* stream) {
+  if (!dup_src)
+    return launch_reduce<1, 3>(a, b, a, rows, cols, nseg, seg_active, res, ws, stream);
+  if (nseg <= 0 || nseg > kMaxSegs) return QCB_ERR_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* need = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + kMaxSegs * sizeof(int) +
+                                     (size_t)nseg * kMaxChunks * 3 * sizeof(double));
+  srap_need_k<<<1, 1024, 0, st>>>(seg_active, dup_src, nseg, need);
+  int rc = launch_reduce<1, 3>(a, b, a, rows, cols, nseg, need, res, ws, stream);
+  if (rc) return rc;
+  srap_copy_k<<<(nseg + 255) / 256, 256, 0, st>>>(seg_active, dup_src, nseg, res);
+  return launch_status();
 }
 
 extern "C" int qcb_reduce_l1(QcbFeat x, QcbFeat h, int rows, int cols, int nseg, double* res,

@@ -364,12 +364,14 @@ def reduce_hlc(out: N.QcbFeat, ref: N.QcbFeat, prev: N.QcbFeat, rows: int, cols:
 
 def reduce_srap(a: N.QcbFeat, b: N.QcbFeat, rows: int, cols: int, nseg: int,
                 res: torch.Tensor, seg_active=None, stream=None,
-                workspace: Optional[Workspace] = None):
+                workspace: Optional[Workspace] = None, dup_src=None):
     """workspace: a dedicated scratch when this runs concurrently with other
-    reductions (side stream); default the shared one."""
+    reductions (side stream); default the shared one.  dup_src (int64 [nseg],
+    optional): first segment with the same (a, b) rows -- duplicates are copied,
+    not re-reduced."""
     ws = N.ptr((workspace or _RWS).get(int(N.lib().qcb_reduce_workspace_bytes(nseg))))
-    N.check(N.lib().qcb_reduce_srap(a, b, rows, cols, nseg, N.ptr(seg_active), N.ptr(res),
-                                    ws, N.stream_ptr(stream)), "reduce_srap")
+    N.check(N.lib().qcb_reduce_srap(a, b, rows, cols, nseg, N.ptr(seg_active), N.ptr(dup_src),
+                                    N.ptr(res), ws, N.stream_ptr(stream)), "reduce_srap")
     count(1)
     return res
 

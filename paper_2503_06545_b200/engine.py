@@ -440,10 +440,14 @@ class QuantCacheEngine:
         """Row tables for one SRAP launch over every (layer, video) pair:
         prev[l-1] vs prev[l] (schedule.py:298-305)."""
         L = self.L
-        return [[self.rows(vs.prev[l - 1]) if l > 0 and vs.prev[l - 1] is not None else 0
-                 for l in range(L) for vs in vids],
-                [self.rows(vs.prev[l]) if vs.prev[l] is not None else 0
-                 for l in range(L) for vs in vids]]
+        ra = [self.rows(vs.prev[l - 1]) if l > 0 and vs.prev[l - 1] is not None else 0
+              for l in range(L) for vs in vids]
+        rb = [self.rows(vs.prev[l]) if vs.prev[l] is not None else 0
+              for l in range(L) for vs in vids]
+        # representative per distinct (a, b) pair: pruned chains alias one slot
+        first: Dict[tuple, int] = {}
+        dup = [first.setdefault((x, y), i) for i, (x, y) in enumerate(zip(ra, rb))]
+        return [ra, rb, dup]
 
     def _plan_reuse_srap(self, t: int, nv: int, do_srap: bool, tabs, stream,
                          workspace=None):
@@ -459,7 +463,7 @@ class QuantCacheEngine:
             Dv.count(1)
             Dv.reduce_srap(Dv.feat(self.arena, tabs[0]), Dv.feat(self.arena, tabs[1]), S, d,
                            L * nv, self.srap.view(L * nv, 3), seg_active=self.mask.view(L * nv),
-                           stream=stream, workspace=workspace)
+                           stream=stream, workspace=workspace, dup_src=tabs[2])
 
     def _early_plan(self, tn: int, vids, main):
         """Launch step tn's plan_reuse + SRAP on the side stream (after everything

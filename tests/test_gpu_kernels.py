@@ -463,6 +463,30 @@ class TestReductions:
             sl = slice(v * S, (v + 1) * S)
             assert r[v] == pytest.approx(O.variation([b[sl]], a[sl]), rel=1e-12)
 
+    def test_srap_dedup_equals_full(self, D):
+        """SRAP over (layer, video) segments with repeated slot pairs: reducing
+        only the representatives (dup_src) gives the full results bit for bit,
+        including inactive representatives needed by active duplicates."""
+        rng = np.random.default_rng(11)
+        S, d, nslot = 512, 1152, 4
+        arena = t(rng.standard_normal((nslot * S, d)).astype(np.float32))
+        pairs = [(0, 0), (0, 1), (0, 0), (2, 2), (1, 1), (2, 2), (0, 1), (3, 0), (2, 2)]
+        ra = torch.tensor([p[0] * S for p in pairs], dtype=torch.int64, device="cuda")
+        rb = torch.tensor([p[1] * S for p in pairs], dtype=torch.int64, device="cuda")
+        first = {}
+        dup = torch.tensor([first.setdefault(p, i) for i, p in enumerate(pairs)],
+                           dtype=torch.int64, device="cuda")
+        active = torch.tensor([0, 1, 1, 0, 1, 1, 1, 1, 0], dtype=torch.int32, device="cuda")
+        n = len(pairs)
+        full = torch.zeros(n * 3, dtype=torch.float64, device="cuda")
+        D.reduce_srap(D.feat(arena, ra), D.feat(arena, rb), S, d, n, full.view(n, 3))
+        ded = torch.full((n * 3,), -1.0, dtype=torch.float64, device="cuda")
+        D.reduce_srap(D.feat(arena, ra), D.feat(arena, rb), S, d, n, ded.view(n, 3),
+                      seg_active=active, dup_src=dup)
+        act = active.cpu().numpy().astype(bool)
+        f, g = full.view(n, 3).cpu().numpy(), ded.view(n, 3).cpu().numpy()
+        assert np.array_equal(f[act].view(np.int64), g[act].view(np.int64))
+
     def test_deterministic(self, D):
         rng = np.random.default_rng(10)
         a, b, c = (t(rng.standard_normal((4096, 1152)).astype(np.float32)) for _ in range(3))
