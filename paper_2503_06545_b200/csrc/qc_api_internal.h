@@ -30,7 +30,13 @@ inline void allow_max_smem(K kernel, bool& done) {
 
 int num_sms();
 int pick_block_n(int N);
-int gemm_u8_launch(const QcbGemm* g, cudaStream_t st);
+// Grouped launch: output column group j (group n columns) reduces over
+// K_j = (j+1)*k with row sums a_rowsum + j*rowsum_stride.
+struct GemmGroup {
+  int n, k;
+  long long rowsum_stride;
+};
+int gemm_u8_launch(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp = nullptr);
 int gemm_f64_launch(const QcbGemmF64* g, cudaStream_t st);
 int head_prep_launch(const float* w, int K, int N, void* prep, cudaStream_t st);
 // 2-D u8 tensor map [rows][ld] (K valid columns), box kBlockK x box_rows, SWIZZLE_128B

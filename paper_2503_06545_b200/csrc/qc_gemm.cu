@@ -84,6 +84,11 @@ struct GemmParams {
   int mode;
   const int* seg_active;  // nullable: skip tiles of inactive segments
   int tma_store;          // 1: each 32-row warp slab maps to contiguous output rows
+  // Grouped launch (0 = off): output columns [g*group_n, (g+1)*group_n) form
+  // group g, reduced over K_g = (g+1)*group_k with row sums rowsum + g*rowsum_stride
+  // (one launch for the head's digit diagonals, qc_head.cu).
+  int group_n, group_k;
+  long long rowsum_stride;
 };
 
 
@@ -111,7 +116,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
-  const int num_kb = (p.K + kBlockK - 1) / kBlockK;
+  // k-blocks of a tile (grouped launches: per column group)
+  auto tile_kb = [&](int n0) -> int {
+    const int k = p.group_n ? (n0 / p.group_n + 1) * p.group_k : p.K;
+    return (k + kBlockK - 1) / kBlockK;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -147,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!tile_active(tile)) continue;
         const int m0 = (tile / p.num_n_tiles) * kBlockM;
         const int n0 = (tile % p.num_n_tiles) * BN;
+        const int num_kb = tile_kb(n0);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
@@ -172,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        const int num_kb = tile_kb((tile % p.num_n_tiles) * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -238,16 +249,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int za = 0, rs = 0;
       float gate = p.gate_scalar;
       long long orow = m, rrow = m;
+      const int grp = p.group_n ? n0 / p.group_n : 0;
+      const int k_eff = p.group_n ? (grp + 1) * p.group_k : p.K;
       if (row_ok) {
         sa = p.sa[seg];
         za = p.za[seg];
-        rs = p.rowsum[m];
+        rs = p.rowsum[(size_t)grp * p.rowsum_stride + m];
         if (p.gate) gate = p.gate[seg];
         if (p.out_row0) orow = p.out_row0[seg] + mrow;
         if (p.resid_row0) rrow = p.resid_row0[seg] + mrow;
       }
       // acc = raw - zw*rowsum - za*colsum + K*za*zw = raw - zw*(rowsum - K*za) - za*colsum
-      const int tr = rs - p.K * za;
+      const int tr = rs - k_eff * za;
       // first output row of this warp's 32-row slab (TMA store path)
       const long long orow_slab = __shfl_sync(0xffffffffu, orow, 0);
 
@@ -423,7 +436,7 @@ int num_sms() {
 }
 
 template <int BN, int MODE>
-static int launch_bn(const QcbGemm* g, cudaStream_t st) {
+static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   using Cfg = GemmCfg<BN>;
   CUtensorMap ma, mb;
   int rc = make_map_u8(&ma, g->a_codes, g->M, g->K, g->lda, kBlockM);
@@ -453,6 +466,11 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st) {
   p.gate = g->gate;
   p.gate_scalar = g->gate_scalar;
   p.seg_active = g->seg_active;
+  if (grp) {
+    p.group_n = grp->n;
+    p.group_k = grp->k;
+    p.rowsum_stride = grp->rowsum_stride;
+  }
   // TMA-store epilogue when every 32-row slab is contiguous in the output.
   const int nseg = (g->M + p.seg_rows - 1) / p.seg_rows;
   const bool slab_contig = (p.seg_rows % 32 == 0) || (nseg == 1 && g->out_row0 == nullptr);
@@ -494,13 +512,13 @@ int pick_block_n(int N) {
 }
 
 template <int BN>
-static int launch_mode(const QcbGemm* g, cudaStream_t st) {
+static int launch_mode(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   switch (g->epilogue) {
-    case QCB_EPI_STORE: return launch_bn<BN, QCB_EPI_STORE>(g, st);
-    case QCB_EPI_GELU: return launch_bn<BN, QCB_EPI_GELU>(g, st);
-    case QCB_EPI_GATE_RESID: return launch_bn<BN, QCB_EPI_GATE_RESID>(g, st);
-    case QCB_EPI_RESID: return launch_bn<BN, QCB_EPI_RESID>(g, st);
-    case QCB_EPI_ACC: return launch_bn<BN, QCB_EPI_ACC>(g, st);
+    case QCB_EPI_STORE: return launch_bn<BN, QCB_EPI_STORE>(g, st, grp);
+    case QCB_EPI_GELU: return launch_bn<BN, QCB_EPI_GELU>(g, st, grp);
+    case QCB_EPI_GATE_RESID: return launch_bn<BN, QCB_EPI_GATE_RESID>(g, st, grp);
+    case QCB_EPI_RESID: return launch_bn<BN, QCB_EPI_RESID>(g, st, grp);
+    case QCB_EPI_ACC: return launch_bn<BN, QCB_EPI_ACC>(g, st, grp);
     default: return QCB_ERR_CONFIG;
   }
 }
@@ -601,8 +619,8 @@ __global__ void __launch_bounds__(32 * kSmallWarps) gemm_u8_small_m(const QcbGem
   g.out[orow * g.ldo + n] = y;
 }
 
-int gemm_u8_launch(const QcbGemm* g, cudaStream_t st) {
-  if (g->M <= kSmallM && g->block_n <= 0 && g->epilogue != QCB_EPI_BIAS) {
+int gemm_u8_launch(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
+  if (!grp && g->M <= kSmallM && g->block_n <= 0 && g->epilogue != QCB_EPI_BIAS) {
     const size_t smem = (size_t)g->M * ((g->K + 15) & ~15);
     if (smem <= 200 * 1024) {
       static bool attr = false;
@@ -613,12 +631,21 @@ int gemm_u8_launch(const QcbGemm* g, cudaStream_t st) {
     }
   }
   int bn = g->block_n > 0 ? g->block_n : pick_block_n(g->N);
+  if (grp && g->block_n <= 0) {   // tiles must not straddle column groups
+    bn = 0;
+    for (int c : {192, 128, 256, 64, 32})
+      if (grp->n % c == 0) {
+        bn = c;
+        break;
+      }
+  }
+  if (grp && (bn == 0 || grp->n % bn)) return QCB_ERR_CONFIG;
   switch (bn) {
-    case 256: return launch_mode<256>(g, st);
-    case 192: return launch_mode<192>(g, st);
-    case 128: return launch_mode<128>(g, st);
-    case 64: return launch_mode<64>(g, st);
-    case 32: return launch_mode<32>(g, st);
+    case 256: return launch_mode<256>(g, st, grp);
+    case 192: return launch_mode<192>(g, st, grp);
+    case 128: return launch_mode<128>(g, st, grp);
+    case 64: return launch_mode<64>(g, st, grp);
+    case 32: return launch_mode<32>(g, st, grp);
     default: return QCB_ERR_CONFIG;
   }
 }

@@ -33,7 +33,8 @@ static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // ------------------------------------------------------------------ layouts
 struct HeadPrepLayout {   // one-time weight side
-  size_t bd[kHeadDigits];   // B_d codes [N][ldb_d], ldb_d = a16((d+1) K)
+  size_t bstack;            // B_d codes stacked [kHeadDigits N][ldb], ldb = a16(kHeadDigits K):
+                            // row d N + n = [E_d .. E_0] of column n (zero padded)
   size_t csum;              // s32 [kHeadDigits][N]
   size_t cstat;             // f64 [N][8]: certificate column factors (head_prep_cols)
   size_t wt;                // f32 [N][K] (W^T for the exact fallback)
@@ -45,10 +46,8 @@ struct HeadPrepLayout {   // one-time weight side
 static HeadPrepLayout prep_layout(int K, int N) {
   HeadPrepLayout L{};
   size_t off = 0;
-  for (int d = 0; d < kHeadDigits; ++d) {
-    L.bd[d] = off;
-    off = a256(off + (size_t)N * a16((size_t)(d + 1) * K));
-  }
+  L.bstack = off;
+  off = a256(off + (size_t)kHeadDigits * N * a16((size_t)kHeadDigits * K));
   L.csum = off;
   off = a256(off + (size_t)4 * kHeadDigits * N);
   L.cstat = off;
@@ -56,9 +55,9 @@ static HeadPrepLayout prep_layout(int K, int N) {
   L.wt = off;
   off = a256(off + (size_t)4 * N * K);
   L.ones = off;
-  off = a256(off + (size_t)8 * N);
+  off = a256(off + (size_t)8 * kHeadDigits * N);
   L.zeros64 = off;
-  off = a256(off + (size_t)4 * N);
+  off = a256(off + (size_t)4 * kHeadDigits * N);
   L.total = off;
   return L;
 }
@@ -67,7 +66,7 @@ struct HeadWsLayout {     // per call
   size_t planes;  // u8 [M][ldp], ldp = a16(kHeadDigits K)
   size_t rsum;    // s32 [kHeadDigits][M] (prefix over planes)
   size_t rstat;   // f64 [M][8]: certificate row factors (head_slice_rows)
-  size_t acc;     // s32 [kHeadDigits][M][N]
+  size_t acc;     // s32 [M][kHeadDigits N] (diagonal d at columns d N ..)
   size_t list;    // s32 [M*N] flagged elements (i*N + j)
   size_t count;   // s32
   size_t one;     // f64 1.0, s32 64
@@ -153,9 +152,10 @@ __global__ void head_prep_cols(const float* __restrict__ w, int K, int N, uint8_
       cs[t] += E[t] + 64;
       sq[t] += (double)(E[t] * E[t]);
     }
+    const size_t ldb = a16((size_t)kHeadDigits * K);
 #pragma unroll
     for (int d = 0; d < kHeadDigits; ++d) {
-      uint8_t* bd = base + L.bd[d] + (size_t)j * a16((size_t)(d + 1) * K);
+      uint8_t* bd = base + L.bstack + ((size_t)d * N + j) * ldb;
 #pragma unroll
       for (int t = 0; t <= d; ++t) bd[(size_t)(d - t) * K + k] = (uint8_t)(E[t] + 64);
     }
@@ -184,8 +184,10 @@ __global__ void head_prep_cols(const float* __restrict__ w, int K, int N, uint8_
     cst[3] = pow2(f - 49);
     cst[4] = up(sqrt(l2));
     cst[5] = cst[6] = cst[7] = 0.0;
-    reinterpret_cast<double*>(base + L.ones)[j] = 1.0;
-    reinterpret_cast<int*>(base + L.zeros64)[j] = 64;
+    for (int d = 0; d < kHeadDigits; ++d) {
+      reinterpret_cast<double*>(base + L.ones)[(size_t)d * N + j] = 1.0;
+      reinterpret_cast<int*>(base + L.zeros64)[(size_t)d * N + j] = 64;
+    }
   }
 }
 
@@ -321,17 +323,17 @@ __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
     c4[u] = cf[4];
     bj[u] = c.bias ? c.bias[j0 + u] : 0.0f;
   }
-  const size_t mn = (size_t)c.M * c.N;
+  const size_t ldacc = (size_t)kHeadDigits * c.N;
   const double k65 = 65.0 * (double)c.K;
   const long long i_end = min((long long)(blockIdx.y + 1) * kCombineRows, c.M);
   for (long long i = (long long)blockIdx.y * kCombineRows; i < i_end; ++i) {
     const int seg = (int)(i / c.seg_rows), r = (int)(i - (long long)seg * c.seg_rows);
     if (r >= c.seg_valid) continue;
-    const size_t base = (size_t)i * c.N + j0;
+    const size_t base = (size_t)i * ldacc + j0;
     int4 a4[kHeadDigits];
 #pragma unroll
     for (int d = 0; d < kHeadDigits; ++d)
-      a4[d] = __ldcs(reinterpret_cast<const int4*>(c.acc + d * mn + base));
+      a4[d] = __ldcs(reinterpret_cast<const int4*>(c.acc + base + (size_t)d * c.N));
     const double* rf = c.rstat + i * 8;
     const double r0 = rf[0], r1 = rf[1], r2 = rf[2], r3 = rf[3], r4 = rf[4], r5 = rf[5];
     const long long orow = c.out_row0 ? c.out_row0[seg] + r : i;
@@ -471,28 +473,46 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
                     0, st>>>(hr, ws, W);
   int rc = launch_status();
   if (rc) return rc;
-  for (int d = 0; d < kHeadDigits; ++d) {
+  {   // every digit diagonal in one grouped launch: column group d reduces K_d = (d+1) K
     QcbGemm q{};
     q.M = (int)M;
-    q.N = N;
-    q.K = (d + 1) * K;
+    q.N = kHeadDigits * N;
+    q.K = kHeadDigits * K;
     q.seg_rows = (int)M;
     q.seg_valid = (int)M;
     q.a_codes = ws + W.planes;
     q.lda = (long long)a16((size_t)kHeadDigits * K);
     q.a_scale = reinterpret_cast<const double*>(ws + W.one);
     q.a_zero = reinterpret_cast<const int*>(ws + W.one + 8);
-    q.a_rowsum = reinterpret_cast<const int*>(ws + W.rsum) + (size_t)d * M;
-    q.w_codes = prep + P.bd[d];
-    q.ldw = (long long)a16((size_t)(d + 1) * K);
+    q.a_rowsum = reinterpret_cast<const int*>(ws + W.rsum);
+    q.w_codes = prep + P.bstack;
+    q.ldw = (long long)a16((size_t)kHeadDigits * K);
     q.w_scale = reinterpret_cast<const double*>(prep + P.ones);
     q.w_zero = reinterpret_cast<const int*>(prep + P.zeros64);
-    q.w_colsum = reinterpret_cast<const int*>(prep + P.csum) + (size_t)d * N;
-    q.out = reinterpret_cast<float*>(ws + W.acc) + (size_t)d * M * N;
-    q.ldo = N;
+    q.w_colsum = reinterpret_cast<const int*>(prep + P.csum);
+    q.out = reinterpret_cast<float*>(ws + W.acc);
+    q.ldo = (long long)kHeadDigits * N;
     q.epilogue = QCB_EPI_ACC;
-    rc = gemm_u8_launch(&q, st);
-    if (rc) return rc;
+    if (N % 32 == 0) {
+      const GemmGroup grp{N, K, M};
+      rc = gemm_u8_launch(&q, st, &grp);
+      if (rc) return rc;
+    } else {   // no tile width divides N: one launch per diagonal on the same layout
+      const long long ldb = q.ldw;
+      for (int d = 0; d < kHeadDigits; ++d) {
+        QcbGemm qd = q;
+        qd.N = N;
+        qd.K = (d + 1) * K;
+        qd.a_rowsum = reinterpret_cast<const int*>(ws + W.rsum) + (size_t)d * M;
+        qd.w_codes = prep + P.bstack + (size_t)d * N * ldb;
+        qd.w_scale = reinterpret_cast<const double*>(prep + P.ones) + (size_t)d * N;
+        qd.w_zero = reinterpret_cast<const int*>(prep + P.zeros64) + (size_t)d * N;
+        qd.w_colsum = reinterpret_cast<const int*>(prep + P.csum) + (size_t)d * N;
+        qd.out = reinterpret_cast<float*>(ws + W.acc) + (size_t)d * N;
+        rc = gemm_u8_launch(&qd, st);
+        if (rc) return rc;
+      }
+    }
   }
   HeadCombine c{M, N, K, g->seg_rows, g->seg_valid,
                 reinterpret_cast<const double*>(ws + W.rstat),
