@@ -409,36 +409,54 @@ __global__ void __launch_bounds__(256) head_fallback(const HeadFallback h) {
     const float* xr = h.x + ((h.x_row0 ? h.x_row0[seg] : (long long)seg * h.seg_rows) + r) * h.ldx;
     const float* wr = h.wt + (size_t)j * h.K;
     double s = 0.0;
-    // ascending k, 16 at a time: the next batch's 16-byte loads are in flight
-    // while the current one feeds the FMA chain (K % 4 == 0, rows 16B-aligned)
-    float4 xa[4], wa[4];
+    // ascending k in batches of 16 through a register ring of kFbDepth batches:
+    // each batch's 16-byte loads are issued kFbDepth batches ahead of its FMAs
+    // (K % 4 == 0, rows 16-byte aligned)
+    constexpr int kFbDepth = 4;
+    float4 xq[kFbDepth][4], wq[kFbDepth][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      xa[u] = __ldg(reinterpret_cast<const float4*>(xr) + u);
-      wa[u] = __ldg(reinterpret_cast<const float4*>(wr) + u);
-    }
+    for (int b = 0; b < kFbDepth; ++b)
+      if (16 * b + 16 <= h.K) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          xq[b][u] = __ldg(reinterpret_cast<const float4*>(xr + 16 * b) + u);
+          wq[b][u] = __ldg(reinterpret_cast<const float4*>(wr + 16 * b) + u);
+        }
+      }
     int k = 0;
-    for (; k + 16 <= h.K; k += 16) {
-      float4 xb[4], wb[4];
-      const bool more = k + 32 <= h.K;
+    for (; k + 16 * kFbDepth <= h.K; k += 16 * kFbDepth) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        xb[u] = more ? __ldg(reinterpret_cast<const float4*>(xr + k + 16) + u) : xa[u];
-        wb[u] = more ? __ldg(reinterpret_cast<const float4*>(wr + k + 16) + u) : wa[u];
-      }
+      for (int b = 0; b < kFbDepth; ++b) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        s = fma((double)xa[u].x, (double)wa[u].x, s);
-        s = fma((double)xa[u].y, (double)wa[u].y, s);
-        s = fma((double)xa[u].z, (double)wa[u].z, s);
-        s = fma((double)xa[u].w, (double)wa[u].w, s);
-      }
+        for (int u = 0; u < 4; ++u) {
+          s = fma((double)xq[b][u].x, (double)wq[b][u].x, s);
+          s = fma((double)xq[b][u].y, (double)wq[b][u].y, s);
+          s = fma((double)xq[b][u].z, (double)wq[b][u].z, s);
+          s = fma((double)xq[b][u].w, (double)wq[b][u].w, s);
+        }
+        const int kn = k + 16 * (b + kFbDepth);
+        if (kn + 16 <= h.K) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        xa[u] = xb[u];
-        wa[u] = wb[u];
+          for (int u = 0; u < 4; ++u) {
+            xq[b][u] = __ldg(reinterpret_cast<const float4*>(xr + kn) + u);
+            wq[b][u] = __ldg(reinterpret_cast<const float4*>(wr + kn) + u);
+          }
+        }
       }
     }
+    // full batches left in the ring, then the scalar tail
+#pragma unroll
+    for (int b = 0; b < kFbDepth; ++b)
+      if (k + 16 <= h.K) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          s = fma((double)xq[b][u].x, (double)wq[b][u].x, s);
+          s = fma((double)xq[b][u].y, (double)wq[b][u].y, s);
+          s = fma((double)xq[b][u].z, (double)wq[b][u].z, s);
+          s = fma((double)xq[b][u].w, (double)wq[b][u].w, s);
+        }
+        k += 16;
+      }
     for (; k < h.K; ++k) s = fma((double)xr[k], (double)wr[k], s);
     const float y = __double2float_rn(s);
     const long long orow = h.out_row0 ? h.out_row0[seg] + r : i;
