@@ -560,6 +560,38 @@ QC_DEV bool gelu_fast_a(float xf, float& y) {
   return true;
 }
 
+// Phase A for 8 elements without branches: every element runs the same
+// straight-line code and the certificate becomes a select (per-element early
+// exits cost more than the shared arithmetic).  Returns the hard mask.
+QC_DEV uint32_t gelu_phase_a8(const float (&v)[8], float (&y)[8], uint32_t valid) {
+  uint32_t hard = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double x = (double)v[i];
+    const double t = x * 0.70710678118654752440;
+    const double at = fabs(t);
+    const double z = at * at;
+    double tt = kErfT[0];
+#pragma unroll
+    for (int k = 1; k < 5; ++k) tt = fma(tt, z, kErfT[k]);
+    double u = z + kErfU[0];
+#pragma unroll
+    for (int k = 1; k < 5; ++k) u = fma(u, z, kErfU[k]);
+    double r = (at * tt) * fast_rcp(u);
+    r = t < 0.0 ? -r : r;
+    const double g = (0.5 * x) * (1.0 + r);
+    // certificate: f32-normal range and >= 256 ulp64 from an f32 tie, as integers
+    const unsigned long long gb = (unsigned long long)__double_as_longlong(g);
+    const unsigned ex = (unsigned)((gb >> 52) & 0x7FF);
+    const int dd = abs((int)((unsigned)gb & 0x1FFFFFFFu) - (1 << 28));
+    const bool ok = (at < 1.0 - 0x1p-40) && (ex - (1023u - 125u)) <= 251u && dd > 256;
+    const bool big = v[i] >= 6.0f, zero = v[i] == 0.0f;
+    y[i] = big ? v[i] : __double2float_rn(g);   // g = +-0 for x = +-0
+    if (((valid >> i) & 1u) && !big && !zero && !ok) hard |= 1u << i;
+  }
+  return hard;
+}
+
 // Phase B, 1 <= |x / sqrt2| < 8: cephes erfc(|t|) = exp(-t^2) P(|t|)/Q(|t|)
 // with FMA Horner, a Newton reciprocal and CUDA exp, then the reference's own
 // structure 1 + erf = 1 +- (1 - erfc).  Error vs the reference's f64 value:
@@ -654,11 +686,11 @@ __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, in
       }
     }
     float y[8];
+    uint32_t valid = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int c = c0 + (i >> 2) * 128 + lane * 4 + (i & 3);
-      if (c < cols && !gelu_fast_a(v[i], y[i])) hard |= 1u << i;
-    }
+    for (int i = 0; i < 8; ++i)
+      if (c0 + (i >> 2) * 128 + lane * 4 + (i & 3) < cols) valid |= 1u << i;
+    hard = gelu_phase_a8(v, y, valid);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = c0 + h * 128 + lane * 4;
