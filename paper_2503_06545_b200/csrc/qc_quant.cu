@@ -822,9 +822,6 @@ struct V4Smem {
   double f[R][B + B / 16];        // FWHT work row
   uint64_t full[R][kV4Bufs];       // bulk-copy completion barriers
   double red[2][kV4Threads / 32]; // LN partial sums (mean, variance)
-  uint32_t smask[3][kV4Threads];  // sign bits of the thread's 16 stage-A elements
-  float run_mn[3][kV4Threads];    // per-thread running min / max per output
-  float run_mx[3][kV4Threads];
 };
 
 // Radix-2^Q butterflies over groups of 2^Q consecutive registers.
@@ -875,17 +872,9 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
     }
   }
 
-  for (int o = 0; o < 3; ++o) {
-    uint32_t m = 0;
-    if (o < p.n_out && p.c[o]) {
-      const uint32_t* sg = reinterpret_cast<const uint32_t*>(p.signs[o]) + lt;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) m |= (__ldg(sg + TPR * j) >> 31) << j;
-    }
-    sm.smask[o][tid] = m;
-    sm.run_mn[o][tid] = INFINITY;
-    sm.run_mx[o][tid] = -INFINITY;
-  }
+  // per-thread running min / max per output (registers; o is 0..2)
+  float mn0 = INFINITY, mn1 = INFINITY, mn2 = INFINITY;
+  float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY;
   // input rows stream through L2 (evict first); the stash should survive in L2
   // until pass 2 reads it (evict last)
   const uint64_t pol_stream = l2_policy_evict_first();
@@ -913,7 +902,8 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
 
   auto flush = [&](int seg) {   // warp-level: running min/max -> the segment's keys
     for (int o = 0; o < p.n_out; ++o) {
-      float lo = sm.run_mn[o][tid], hi = sm.run_mx[o][tid];
+      float lo = o == 0 ? mn0 : (o == 1 ? mn1 : mn2);
+      float hi = o == 0 ? mx0 : (o == 1 ? mx1 : mx2);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
@@ -924,9 +914,9 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
         atomicMin(&k[0], f2key(lo));
         atomicMax(&k[1], f2key(hi));
       }
-      sm.run_mn[o][tid] = INFINITY;
-      sm.run_mx[o][tid] = -INFINITY;
     }
+    mn0 = mn1 = mn2 = INFINITY;
+    mx0 = mx1 = mx2 = -INFINITY;
   };
   auto slot_sum = [&](double v, double* red) {   // sum over the slot's warps
     v = warp_sum(v);
@@ -1033,7 +1023,6 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
       float lo = INFINITY, hi = -INFINITY;
       if (c) {
         const double* rc = a.rc[o];
-        const uint32_t sgm = sm.smask[o][tid];
         // ---- balance (exact f32(h / c), held in f64) + sign, stage A
         double v[16];
         uint32_t slow = 0;
@@ -1047,7 +1036,8 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if ((slow >> j) & 1u)
-              v[j] = flip_sign(div_exact_f32((double)h[j], c[lt + TPR * j]), (sgm >> j) & 1u);
+              v[j] = flip_sign(div_exact_f32((double)h[j], c[lt + TPR * j]),
+                               __ldg(rc + lt + TPR * j) < 0.0);   // rc carries the sign
         }
         fwht_regs<4>(v);
 #pragma unroll
@@ -1115,8 +1105,16 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
           }
         }
       }
-      sm.run_mn[o][tid] = fminf(sm.run_mn[o][tid], lo);
-      sm.run_mx[o][tid] = fmaxf(sm.run_mx[o][tid], hi);
+      if (o == 0) {
+        mn0 = fminf(mn0, lo);
+        mx0 = fmaxf(mx0, hi);
+      } else if (o == 1) {
+        mn1 = fminf(mn1, lo);
+        mx1 = fmaxf(mx1, hi);
+      } else {
+        mn2 = fminf(mn2, lo);
+        mx2 = fmaxf(mx2, hi);
+      }
     }
   }
   if (cur_seg >= 0) flush(cur_seg);
