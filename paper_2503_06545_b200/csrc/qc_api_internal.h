@@ -19,6 +19,26 @@ inline int launch_status() {
   return QCB_OK;
 }
 
+// Programmatic dependent launch: the kernel may begin (prologue: barrier init,
+// TMEM allocation, descriptor prefetch) while the previous kernel on the
+// stream drains; it must execute griddepcontrol.wait (pdl_wait()) before
+// touching anything that kernel wrote.  Every kernel launched this way does.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Opt a kernel into the full dynamic shared-memory carve-out once.
 template <typename K>
 inline void allow_max_smem(K kernel, bool& done) {

@@ -17,6 +17,14 @@
 
 namespace qc {
 
+// ---------------------------------------------------------------- PDL
+// Wait until the preceding grid on the stream completed and its writes are
+// visible (no-op when the kernel was launched without the PDL attribute).
+QC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next grid on the stream start launching (its pdl_wait still waits
+// for this grid's completion).
+QC_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // ---------------------------------------------------------------- smem / barriers
 QC_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -661,6 +661,8 @@ QC_DEV bool gelu_fast2(float xf, float& y) {
 }
 
 __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, int rows, int cols) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float q_val[8][256];
   __shared__ int q_row[8][256];
   __shared__ int q_col[8][256];
@@ -739,7 +741,7 @@ int gelu_launch(float* x, long long ld, int rows, int cols, cudaStream_t st) {
   long long blocks = (chunks + 7) / 8;
   const long long cap = (long long)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  gelu_inplace_k<<<(unsigned)blocks, 256, 0, st>>>(x, ld, rows, cols);
+  launch_pdl(gelu_inplace_k, dim3((unsigned)blocks), dim3(256), 0, st, x, ld, rows, cols);
   return launch_status();
 }
 

@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // setup above overlaps the previous kernel's tail (PDL); operands come after
+  pdl_wait();
+  pdl_trigger();
 
   auto tile_active = [&](int tile) -> bool {
     if (p.seg_active == nullptr) return true;
@@ -490,7 +493,8 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   }
   int tiles = p.num_m_tiles * p.num_n_tiles;
   int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_u8_tcgen05<BN, MODE><<<grid, kThreads, Cfg::kSmemBytes, st>>>(ma, mb, mo, p);
+  launch_pdl(gemm_u8_tcgen05<BN, MODE>, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, st, ma, mb,
+             mo, p);
   return launch_status();
 }
 

@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(kQThreads) act_quant_rows(const ActQuantParams
 }
 
 __global__ void init_keys(uint32_t* keys, int n) {
+  pdl_wait();
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) keys[i] = (i & 1) ? 0u : 0xFFFFFFFFu;
 }
@@ -844,6 +846,8 @@ QC_DEV double flip_sign(double x, uint32_t bit) {
 
 template <int B, bool kPow2Scale, int kMinCtas>
 __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuantParams p, const AQ2 a) {
+  pdl_wait();   // x rows / keys come from the preceding kernels
+  pdl_trigger();
   constexpr int R = 4096 / B;               // row slots per CTA
   constexpr int TPR = B / 16;               // threads per row slot
   constexpr int WPR = TPR / 32;             // warps per row slot (>= 2)
@@ -1126,6 +1130,8 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
 constexpr int kP2Batch = 4;
 
 __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, const AQ2 a) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.K;
   const double top = (double)((1 << p.bits) - 1);
@@ -1330,7 +1336,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
   p.rscale = (float)(1.0 / sqrt((double)b));
   p.keys = reinterpret_cast<uint32_t*>(q->workspace);
   const int nkeys = 2 * q->n_out * q->nseg;
-  init_keys<<<(nkeys + 255) / 256, 256, 0, st>>>(p.keys, nkeys);
+  launch_pdl(init_keys, dim3((nkeys + 255) / 256), dim3(256), 0, st, p.keys, nkeys);
   // v2: register FWHT for b in {1024, 2048, 4096} with a short tail
   const int wpr = b / 1024;
   const bool v2 = (b == 1024 || b == 2048 || b == 4096) && (q->K - b) <= 8 * 32 * wpr &&
@@ -1384,7 +1390,8 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
       switch (b * 2 + (ln ? 1 : 0)) {
 #define QC_AQ4(BB, P2, MC, FLAG)                                                            \
   allow_max_smem(aq4_pass1<BB, P2, MC>, FLAG);                                              \
-  aq4_pass1<BB, P2, MC><<<b1, kV4Threads, sizeof(V4Smem<BB>) + ln_bytes, st>>>(p, a);       \
+  launch_pdl(aq4_pass1<BB, P2, MC>, dim3(b1), dim3(kV4Threads), sizeof(V4Smem<BB>) + ln_bytes, \
+             st, p, a);                                                                    \
   break;
         case 2048: QC_AQ4(1024, true, 3, a41)
         case 2049: QC_AQ4(1024, true, 2, a41l)
@@ -1410,7 +1417,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     }
     int b2 = (a.total_rows + 3) / 4;
     if (b2 > num_sms() * 16) b2 = num_sms() * 16;
-    aq2_pass2<<<b2, kV2Threads, 0, st>>>(p, a);
+    launch_pdl(aq2_pass2, dim3(b2), dim3(kV2Threads), 0, st, p, a);
     if (q->xe_out[0] && q->ldxe != q->K) return QCB_ERR_DIM;  // debug copy layout unsupported
     return launch_status();
   }
