@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(128) attention_f64_k(const QcbAttention a) {
 // one key is exactly 1 (exp(0)/exp(0)), and mm(p, v) = f32(0 + 1.0*v) = v, so
 // every query row's output is the value row -- identical bits, one copy.
 __global__ void attention_single_key_k(const QcbAttention a) {
+  pdl_wait();
+  pdl_trigger();
   const int seg = blockIdx.y;
   const int d = a.heads * a.dh;
   const float* vrow = a.v + (long long)seg * a.kv_seg_stride * a.ldv;
@@ -439,7 +441,7 @@ __global__ void attention_single_key_k(const QcbAttention a) {
 int attention_f64_launch(const QcbAttention* a, cudaStream_t st) {
   if (a->Skv == 1) {
     dim3 grid((unsigned)min(a->S, 1024), a->nseg);
-    attention_single_key_k<<<grid, 128, 0, st>>>(*a);
+    launch_pdl(attention_single_key_k, grid, dim3(128), 0, st, *a);
     return launch_status();
   }
   if (a->dh > 256) return QCB_ERR_DIM;
@@ -747,6 +749,8 @@ int gelu_launch(float* x, long long ld, int rows, int cols, cudaStream_t st) {
 
 // ------------------------------------------------------------------ ddpm
 __global__ void ddpm_k(const QcbDdpm d) {
+  pdl_wait();
+  pdl_trigger();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.n) return;
   double m = __ddiv_rn(__dsub_rn((double)d.x[i], __dmul_rn(d.c1, (double)d.eps[i])), d.c2);
@@ -756,7 +760,7 @@ __global__ void ddpm_k(const QcbDdpm d) {
 
 int ddpm_launch(const QcbDdpm* d, cudaStream_t st) {
   const int th = 256;
-  ddpm_k<<<(unsigned)((d->n + th - 1) / th), th, 0, st>>>(*d);
+  launch_pdl(ddpm_k, dim3((unsigned)((d->n + th - 1) / th)), dim3(th), 0, st, *d);
   return launch_status();
 }
 

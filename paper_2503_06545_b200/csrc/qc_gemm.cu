@@ -537,6 +537,8 @@ constexpr int kSmallM = 16;
 constexpr int kSmallWarps = 8;
 
 __global__ void __launch_bounds__(32 * kSmallWarps) gemm_u8_small_m(const QcbGemm g) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t a_sm[];   // [M][Kp] codes, Kp = K rounded to 16
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Kp = (g.K + 15) & ~15;
@@ -630,7 +632,7 @@ int gemm_u8_launch(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
       static bool attr = false;
       allow_max_smem(gemm_u8_small_m, attr);
       const int blocks = (g->N + kSmallWarps - 1) / kSmallWarps;
-      gemm_u8_small_m<<<blocks, 32 * kSmallWarps, smem, st>>>(*g);
+      launch_pdl(gemm_u8_small_m, dim3(blocks), dim3(32 * kSmallWarps), smem, st, *g);
       return launch_status();
     }
   }

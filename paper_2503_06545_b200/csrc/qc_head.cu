@@ -203,6 +203,8 @@ struct HeadRows {
 // One warp per output row i: statistics, digits, planes, prefix rowsums.
 __global__ void __launch_bounds__(32 * kHeadSliceWarps)
     head_slice_rows(const HeadRows h, uint8_t* ws, HeadWsLayout L) {
+  pdl_wait();
+  pdl_trigger();
   const long long i = (long long)blockIdx.x * kHeadSliceWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= h.M) return;
@@ -308,6 +310,8 @@ struct HeadCombine {
 constexpr int kCombineRows = 16;   // rows per thread (column factors stay in registers)
 
 __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
+  pdl_wait();
+  pdl_trigger();
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= c.N) return;
   // the thread's 4 columns: certificate factors once
@@ -399,6 +403,8 @@ struct HeadFallback {
 
 // The reference's ascending-k f64 FMA chain for the listed elements.
 __global__ void __launch_bounds__(256) head_fallback(const HeadFallback h) {
+  pdl_wait();
+  pdl_trigger();
   const int n = *h.count;
   if (h.total && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(h.total, n);
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {

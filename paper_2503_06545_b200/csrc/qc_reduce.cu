@@ -50,6 +50,8 @@ template <int KIND, int NV>
 __global__ void __launch_bounds__(kRThreads)
     seg_reduce(FeatP f0, FeatP f1, FeatP f2, int rows, int cols, const int* seg_active,
                double* partials, int* tickets, double* res, int chunks) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double scratch[NV * 8];
   __shared__ bool last;
   const int seg = blockIdx.y;
@@ -192,6 +194,8 @@ namespace qc {
 // result -- the chunking and the fixed-order final sum depend only on
 // rows/cols/nseg -- so only representatives dup[s] == s are reduced.
 __global__ void srap_need_k(const int* seg_active, const long long* dup, int nseg, int* need) {
+  pdl_wait();
+  pdl_trigger();
   for (int s = threadIdx.x; s < nseg; s += blockDim.x) need[s] = 0;
   __syncthreads();
   for (int s = threadIdx.x; s < nseg; s += blockDim.x)
@@ -199,6 +203,8 @@ __global__ void srap_need_k(const int* seg_active, const long long* dup, int nse
 }
 
 __global__ void srap_copy_k(const int* seg_active, const long long* dup, int nseg, double* res) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nseg) return;
   const int d = (int)dup[s];
@@ -214,8 +220,8 @@ static int launch_reduce(QcbFeat a, QcbFeat b, QcbFeat c, int rows, int cols, in
   int* tickets = reinterpret_cast<int*>(ws);
   double* partials = reinterpret_cast<double*>(tickets + kMaxSegs);
   const int ch = chunks_for(rows, cols, nseg);
-  seg_reduce<KIND, NV><<<dim3(ch, nseg), kRThreads, 0, (cudaStream_t)stream>>>(
-      fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch);
+  launch_pdl(seg_reduce<KIND, NV>, dim3(ch, nseg), dim3(kRThreads), 0, (cudaStream_t)stream,
+             fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch);
   return launch_status();
 }
 
@@ -234,10 +240,11 @@ extern "C" int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nse
   cudaStream_t st = (cudaStream_t)stream;
   int* need = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + kMaxSegs * sizeof(int) +
                                      (size_t)nseg * kMaxChunks * 3 * sizeof(double));
-  srap_need_k<<<1, 1024, 0, st>>>(seg_active, dup_src, nseg, need);
+  launch_pdl(srap_need_k, dim3(1), dim3(1024), 0, st, seg_active, dup_src, nseg, need);
   int rc = launch_reduce<1, 3>(a, b, a, rows, cols, nseg, need, res, ws, stream);
   if (rc) return rc;
-  srap_copy_k<<<(nseg + 255) / 256, 256, 0, st>>>(seg_active, dup_src, nseg, res);
+  launch_pdl(srap_copy_k, dim3((nseg + 255) / 256), dim3(256), 0, st, seg_active, dup_src, nseg,
+             res);
   return launch_status();
 }
 
@@ -273,6 +280,8 @@ QC_DEV bool live(const QcbPolicyVideo& s, int l, int t) {
 }
 
 __global__ void plan_reuse_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nvid) return;
   QcbPolicyVideo& s = st[v];
@@ -294,6 +303,8 @@ __global__ void plan_reuse_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThre
 
 __global__ void sim_mask_k(const QcbPolicyVideo* st, int nvid, int L, QcbThresholds th,
                            int* flags) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nvid) return;
   const QcbPolicyVideo& s = st[v];
@@ -308,6 +319,8 @@ __global__ void sim_mask_k(const QcbPolicyVideo* st, int nvid, int L, QcbThresho
 __global__ void plan_finish_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
                               const double* srap, const double* hist_l1, int n_hist,
                               const double* draws, long long dstride) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nvid) return;
   QcbPolicyVideo& s = st[v];
@@ -389,6 +402,8 @@ QC_DEV void observe_one(QcbPolicyVideo& s, int l, int t, const QcbThresholds& th
 
 __global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
                           const double* hlc) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nvid) return;
   observe_one(st[v], l, t, th, hlc + (size_t)v * 2);
@@ -398,6 +413,8 @@ __global__ void observe_k(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresho
 // writes, so the per-layer updates can be applied together at the step's end).
 __global__ void observe_all_k(QcbPolicyVideo* st, int nvid, int L, int t, QcbThresholds th,
                               const double* hlc /*[L][nvid][2]*/) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nvid) return;
   for (int l = 0; l < L; ++l) observe_one(st[v], l, t, th, hlc + ((size_t)l * nvid + v) * 2);
@@ -410,14 +427,16 @@ static int launch_ok() { return launch_status(); }
 extern "C" int qcb_policy_plan_reuse(QcbPolicyVideo* st, int nvid, int L, int t,
                                      QcbThresholds th, void* stream) {
   if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
-  plan_reuse_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, t, th);
+  launch_pdl(plan_reuse_k, dim3((nvid + 63) / 64), dim3(64), 0, (cudaStream_t)stream, st, nvid, L,
+             t, th);
   return launch_ok();
 }
 
 extern "C" int qcb_policy_sim_mask(const QcbPolicyVideo* st, int nvid, int L, QcbThresholds th,
                                    int* flags, void* stream) {
   if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
-  sim_mask_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, th, flags);
+  launch_pdl(sim_mask_k, dim3((nvid + 63) / 64), dim3(64), 0, (cudaStream_t)stream, st, nvid, L,
+             th, flags);
   return launch_ok();
 }
 
@@ -426,21 +445,23 @@ extern "C" int qcb_policy_plan_finish(QcbPolicyVideo* st, int nvid, int L, int t
                                       const double* hist_l1, int n_hist, const double* draws,
                                       long long dstride, void* stream) {
   if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0 || n_hist < 0) return QCB_ERR_DIM;
-  plan_finish_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(
-      st, nvid, L, t, th, srap, hist_l1, n_hist, draws, dstride);
+  launch_pdl(plan_finish_k, dim3((nvid + 63) / 64), dim3(64), 0, (cudaStream_t)stream, st, nvid, L,
+             t, th, srap, hist_l1, n_hist, draws, dstride);
   return launch_ok();
 }
 
 extern "C" int qcb_policy_observe_all(QcbPolicyVideo* st, int nvid, int L, int t,
                                      QcbThresholds th, const double* hlc, void* stream) {
   if (L > QCB_MAX_LAYERS || L <= 0 || nvid <= 0) return QCB_ERR_DIM;
-  observe_all_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, L, t, th, hlc);
+  launch_pdl(observe_all_k, dim3((nvid + 63) / 64), dim3(64), 0, (cudaStream_t)stream, st, nvid, L,
+             t, th, hlc);
   return launch_ok();
 }
 
 extern "C" int qcb_policy_observe(QcbPolicyVideo* st, int nvid, int l, int t, QcbThresholds th,
                                   const double* hlc, void* stream) {
   if (l < 0 || l >= QCB_MAX_LAYERS || nvid <= 0) return QCB_ERR_DIM;
-  observe_k<<<(nvid + 63) / 64, 64, 0, (cudaStream_t)stream>>>(st, nvid, l, t, th, hlc);
+  launch_pdl(observe_k, dim3((nvid + 63) / 64), dim3(64), 0, (cudaStream_t)stream, st, nvid, l, t,
+             th, hlc);
   return launch_ok();
 }
