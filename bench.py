@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--timesteps", type=int, default=100)
     ap.add_argument("--wbits", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decisions", default="per_video", choices=["per_video", "synchronized"],
+                    help="per-video decisions (reference semantics, no collective) or one "
+                         "policy for the whole batch (one NCCL all-reduce per step)")
     return ap.parse_args()
 
 
@@ -323,7 +326,8 @@ def run_ours(args):
     th0 = ThresholdConfig(delta1=0.0, delta2=0.0)
     eng = QuantCacheEngine(model, sched.alpha_bar, tog_cal, th0, wbits, absmax, sign_seed=0,
                            prune_seed=0, max_videos=B, options=opts)
-    _, tr = eng.generate([1000 + rank], device_noise_seed=1000 + rank)
+    # the same calibration video on every rank: one threshold set for the job
+    _, tr = eng.generate([1000], device_noise_seed=1000)
     ds = [r.d for r in tr[0] if r.d is not None]
     vs = [r.v for r in tr[0] if r.layer == 0 and r.v is not None and r.v > 0]
     th = ThresholdConfig(delta1=float(np.percentile(ds, 33)), delta2=float(np.percentile(ds, 66)),
@@ -331,6 +335,7 @@ def run_ours(args):
     del eng
     torch.cuda.empty_cache()
     tog = Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=True)
+    opts = EngineOptions(attention="fast", noise="device", decisions=args.decisions)
     eng = QuantCacheEngine(model, sched.alpha_bar, tog, th, wbits, absmax, sign_seed=0,
                            prune_seed=0, max_videos=B, options=opts)
     gen = torch.Generator(device="cuda")
@@ -472,7 +477,10 @@ def run_ours(args):
         "config": {"workload": "C3: STDiT-XL/2 dims (28x1152, 16 heads, FFN 4608, cond 4096), "
                                "16 frames 256x256 (S=4096), DDPM T=100, full QuantCache",
                    "videos_per_gpu_per_step": B, "timesteps": T, "weight_bits": args.wbits,
-                   "parallelism": f"video-sharded x{world}", "attention": "bf16 SDPA (library)",
+                   "parallelism": f"video-sharded x{world}" + (
+                       ", synchronised decisions (1 NCCL all-reduce of 1.1 KB per step)"
+                       if args.decisions == "synchronized" else ", per-video decisions"),
+                   "decisions": args.decisions, "attention": "bf16 SDPA (library)",
                    "noise": "device Philox", "l2": "inputs > L2 (activation arena "
                    f"{eng.arena.numel() * 4 / 2**30:.1f} GiB)",
                    "thresholds": {"delta1": th.delta1, "delta2": th.delta2,

@@ -702,3 +702,58 @@ def sample(dims: ModelDims, steps: int, th: Optional[Thresholds] = None,
         else:
             x = ddpm_final(x, eps, ab)
     return x, st
+
+
+def sample_sync(dims: ModelDims, steps: int, th: Optional[Thresholds] = None,
+                toggles=(False, False, False, False), seeds: Sequence[int] = (0,),
+                prune_seed: int = 0, weight_bits=None, act_absmax=None, sign_seed: int = 0,
+                b0: float = 1e-4, b1: float = 2e-2, weights=None):
+    """Synchronised-decision mode (BASELINE north_star: "all-reduce the scalar
+    cache and prune decisions so every rank takes the same path").
+
+    The videos of the whole batch (every rank's shard) are sampled in lockstep
+    under ONE PolicyState, and the policy statistics are the reference formulas
+    applied to the CONCATENATED batch: features are stacked on a leading video
+    axis, so `divergence` (schedule.py:67-82), `similarity` (:108-116) and
+    `variation` (:128-133) sum over every video.  Blocks, quantizers (per video
+    tensor), head and the DDPM update stay per video, each video with its own
+    NumPy stream (x0, cond, then one noise draw per t > 0, sampler.py:108-131).
+    With a single seed this is exactly `sample`.
+
+    Returns (final latents f32 (B, F, T, d), PolicyState)."""
+    hlc, aw, aa, srap = toggles
+    blocks, head_w, head_b = weights if weights is not None else init_weights(dims)
+    ab = alpha_bar(steps, b0, b1)
+    q, fp, hm = block_costs(dims)
+    st = PolicyState(dims.num_blocks, steps, th or Thresholds(0.0, 0.0), hlc, aw, aa, srap,
+                     q, fp, hm, prune_seed, weight_bits if aw else {})
+    qs = QuantSites(blocks, aw, aa, weight_bits or {}, act_absmax, sign_seed) \
+        if (aw or aa) else None
+    rngs = [np.random.default_rng(s) for s in seeds]
+    shape = (dims.frames, dims.tokens_per_frame, dims.model_dim)
+    xs, conds = [], []
+    for r in rngs:
+        xs.append(r.standard_normal(shape).astype(np.float32))
+        conds.append(r.standard_normal(dims.cond_dim).astype(np.float32))
+    x = np.stack(xs)
+    B, S, D = len(rngs), dims.seq_len, dims.model_dim
+    for t in range(steps - 1, -1, -1):
+        dec = st.plan(t, x)
+        gemm = qs.hook(dec.abits) if qs is not None else None
+        h = x.reshape(B, S, D)
+        for l in range(dims.num_blocks):
+            a = dec.actions[l]
+            if a == "reuse":
+                h = st.cache[l][0]
+            elif a != "prune":
+                h = np.stack([block(h[v], conds[v], t, blocks[l], l, dims.num_heads, gemm)
+                              for v in range(B)])
+            st.observe(t, l, h, dec)
+        eps = np.stack([seq_mm(h[v], head_w) + head_b for v in range(B)]).reshape(x.shape)
+        st.finalize(t, x, dec)
+        if t > 0:
+            noise = np.stack([r.standard_normal(shape).astype(np.float32) for r in rngs])
+            x = ddpm_step(x, t, eps, ab, noise)
+        else:
+            x = ddpm_final(x, eps, ab)
+    return x, st

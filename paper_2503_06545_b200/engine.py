@@ -103,6 +103,8 @@ class EngineOptions:
     noise: str = "numpy"           # "numpy" (reference RNG stream) | "device" (Philox)
     head: str = "int8"             # "int8" (certified digit GEMMs) | "f64" (FMA chains);
                                    # both give the reference's mm bit for bit
+    decisions: str = "per_video"   # "per_video" (reference semantics) | "synchronized"
+                                   # (one policy for the whole batch, all ranks)
     record_features: bool = False
 
 
@@ -162,6 +164,10 @@ class QuantCacheEngine:
         self.phase_profile: Optional[list] = None  # set to [] to time the other phases
         self.host_profile: Optional[list] = None   # set to []: host s from plan sync to the
                                                    # end of the block loop, per step
+        if self.opts.decisions not in ("per_video", "synchronized"):
+            raise ValueError("decisions must be 'per_video' or 'synchronized'")
+        self.sync = self.opts.decisions == "synchronized"
+        self.sync_group = None    # process group of the synchronised mode (None: default)
         self._upload_weights(act_absmax or {})
         self._alloc()
 
@@ -246,6 +252,17 @@ class QuantCacheEngine:
         self.mask = torch.zeros((L, nv), dtype=torch.int32, device=dev)
         self.hist_l1 = torch.zeros((self.th.history_k + 1, nv), dtype=torch.float64, device=dev)
         self.hlc = torch.zeros((L, nv, 2), dtype=torch.float64, device=dev)
+        # synchronised mode: the packed per-step decision sums, summed over the
+        # local videos and then all-reduced over ranks:
+        # [L][2] HLC (sum|out-ref|, sum (out-prev)^2) | [L][3] SRAP (<a,b>, |a|^2,
+        # |b|^2) | [history_k + 1] V terms
+        hk1 = self.th.history_k + 1
+        self.stats = torch.zeros(5 * L + hk1, dtype=torch.float64, device=dev)
+        self.hlc_g = self.stats[:2 * L].view(L, 1, 2)
+        self.srap_g = self.stats[2 * L:5 * L].view(L, 1, 3)
+        self.l1_g = self.stats[5 * L:].view(hk1, 1)
+        self.sync_mask = torch.ones((L, nv), dtype=torch.int32, device=dev)
+        self.sync_mask[0].zero_()
         # the next step's reuse plan + SRAP similarities run on a side stream
         # while this step's FP64 noise head runs (see _early_plan)
         self.side = torch.cuda.Stream(device=dev)
@@ -458,11 +475,11 @@ class QuantCacheEngine:
         N.check(lib.qcb_policy_plan_reuse(pol, nv, L, t, self.thc, sp), "plan_reuse")
         Dv.count(1)
         if do_srap:
-            N.check(lib.qcb_policy_sim_mask(pol, nv, L, self.thc, N.ptr(self.mask), sp),
+            N.check(lib.qcb_policy_sim_mask(pol, nv, L, self.thc, N.ptr(self.mask_v), sp),
                     "sim_mask")
             Dv.count(1)
             Dv.reduce_srap(Dv.feat(self.arena, tabs[0]), Dv.feat(self.arena, tabs[1]), S, d,
-                           L * nv, self.srap.view(L * nv, 3), seg_active=self.mask.view(L * nv),
+                           L * nv, self.srap_v.view(L * nv, 3), seg_active=self.mask_v.view(L * nv),
                            stream=stream, workspace=workspace, dup_src=tabs[2])
 
     def _early_plan(self, tn: int, vids, main):
@@ -517,138 +534,228 @@ class QuantCacheEngine:
         if self.opts.noise == "device":
             gen = torch.Generator(device=self.dev)
             gen.manual_seed(int(device_noise_seed if device_noise_seed is not None else seeds[0]))
-        pol = self.pol.data_ptr()
         self._early = None
-        lib = N.lib()
-        sp = N.stream_ptr()
+        # reduction results laid out [.][nv][.] for the nv videos of this call
+        # (the layout the policy kernels index with nvid = nv)
+        hk1 = self.th.history_k + 1
+        self.hlc_v = self.hlc.view(-1)[:L * nv * 2].view(L, nv, 2)
+        self.srap_v = self.srap.view(-1)[:L * nv * 3].view(L, nv, 3)
+        self.l1_v = self.hist_l1.view(-1)[:hk1 * nv].view(hk1, nv)
+        self.mask_v = self.mask.view(-1)[:L * nv].view(L, nv)
+        if self.sync:
+            self.sync_mask_v = self.sync_mask.view(-1)[:L * nv].view(L, nv)
+            self.sync_mask_v.fill_(1)
+            self.sync_mask_v[0].zero_()
         for t in range(T - 1, -1, -1):
             self._begin_step(t)
             # ---------------- plan (device) ----------------
-            nh = len(vids[0].hist)
-            pre = []
-            for j in range(nh):
-                pre.append([self.rows(vs.x) for vs in vids])
-                pre.append([self.rows(vs.hist[j]) for vs in vids])
-            early = self._early if (self._early is not None and self._early[0] == t) else None
-            self._early = None
-            if early is None:
-                do_srap = self.tog.srap and not (vids[0].seen == 0 or t == 0)
-                if do_srap:
-                    pre += self._srap_tables(vids)
-            tabs = self._upload_idx(pre)
-            ph = self._ph("plan")
-            ph.__enter__()
-            for j in range(nh):
-                Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]), Dv.feat(self.arena, tabs[2 * j + 1]),
-                             S, d, nv, self.hist_l1[j])
-            if early is None:
-                self._plan_reuse_srap(t, nv, do_srap, tabs[2 * nh:], st)
+            if self.sync:
+                if t == T - 1:
+                    self._sync_plan(t, 0)    # later steps were planned by _sync_decide
             else:
-                st.wait_event(early[1])   # plan_reuse / SRAP of this step ran on the side stream
-            N.check(lib.qcb_policy_plan_finish(pol, nv, L, t, self.thc, N.ptr(self.srap),
-                                               N.ptr(self.hist_l1), nh,
-                                               N.ptr(self.draws[t]), 0, sp), "plan_finish")
-            Dv.count(1)
-            ph.__exit__(None, None, None)
+                self._plan_step(t, vids)
             self.pol_host.copy_(self.pol, non_blocking=True)
             st.synchronize()
-            first_launch = None
-            if self.host_profile is not None:
-                t_sync = time.perf_counter()
             raw = self.pol_host.numpy()
+            npl = 1 if self.sync else nv
             plans = [N.QcbPolicyVideo.from_buffer_copy(
-                raw[v * self.pol_size:(v + 1) * self.pol_size].tobytes()) for v in range(nv)]
+                raw[v * self.pol_size:(v + 1) * self.pol_size].tobytes()) for v in range(npl)]
+            if self.sync:
+                plans = plans * nv    # every video (and every rank) takes one path
             for vs in vids:
                 vs.seen += 1
             # plain Python copies of the decisions (ctypes field access is slow)
             act_tab = [list(p.action) for p in plans]
             abits_of = [int(p.abits) for p in plans]
-            # ---------------- execute blocks ----------------
-            cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
-            feats = [] if collect_features is not None else None
-            for l in range(L):
-                acts = [act_tab[v][l] for v in range(nv)]
-                outs = list(cur)
-                rec = []
-                for v in range(nv):
-                    a = acts[v]
-                    if a == N.ACT_REUSE:
-                        outs[v] = vids[v].pool.inc(vids[v].cache[l])
-                    elif a == N.ACT_PRUNE:
-                        outs[v] = vids[v].pool.inc(cur[v])
-                    else:
-                        outs[v] = vids[v].pool.alloc()
-                        rec.append(v)
-                if rec:
-                    # group recomputing videos by activation bits
-                    groups: Dict[int, List[int]] = {}
-                    for v in rec:
-                        groups.setdefault(abits_of[v], []).append(v)
-                    need_d = [acts[v] == N.ACT_RECOMPUTE and vids[v].prev[l] is not None
-                              for v in range(nv)]
-                    tabl = []
-                    for bits, g in groups.items():
-                        tabl += [[self.rows(cur[v]) for v in g], [self.rows(outs[v]) for v in g],
-                                 g]
-                    if any(need_d):
-                        tabl += [[self.rows(outs[v]) for v in range(nv)],
-                                 [self.rows(vids[v].cache[l] if vids[v].cache[l] is not None
-                                            else (vids[v].prev[l] or 0)) for v in range(nv)],
-                                 [self.rows(vids[v].prev[l] or 0) for v in range(nv)],
-                                 [int(x) for x in need_d]]
-                    tl = self._upload_idx(tabl)
-                    if self.host_profile is not None and first_launch is None:
-                        first_launch = time.perf_counter() - t_sync
-                    for gi, (bits, g) in enumerate(groups.items()):
-                        self._block(l, t, g, bits, tl[3 * gi], tl[3 * gi + 1], tl[3 * gi + 2])
-                    if any(need_d):
-                        base = 3 * len(groups)
-                        act = tl[base + 3].to(torch.int32)
-                        with self._ph("hlc"):
-                            Dv.reduce_hlc(Dv.feat(self.arena, tl[base]),
-                                          Dv.feat(self.arena, tl[base + 1]),
-                                          Dv.feat(self.arena, tl[base + 2]), S, d, nv,
-                                          self.hlc[l], seg_active=act)
+            self._run_step(t, vids, act_tab, abits_of, collect_features, gen)
+        out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
+        if return_device:
+            return out, vids
+        return out.cpu().numpy(), self._collect_traces(vids)
 
-                # host mirror of the cache / prev references (schedule.py:349-351)
-                for v, vs in enumerate(vids):
-                    if acts[v] == N.ACT_RECOMPUTE and t > 0:
-                        vs.pool.dec(vs.cache[l])
-                        vs.cache[l] = vs.pool.inc(outs[v])
-                    vs.pool.dec(vs.prev[l])
-                    vs.prev[l] = vs.pool.inc(outs[v])
-                    vs.pool.dec(cur[v])
-                cur = outs
-                if feats is not None:
-                    feats.append(torch.stack([self.slot_view(s) for s in cur]).cpu().numpy())
-            # observe_block for every layer of the step (schedule.py:330-351)
-            if self.host_profile is not None:
-                now = time.perf_counter() - t_sync
-                self.host_profile.append((now, first_launch if first_launch is not None else now))
-            N.check(lib.qcb_policy_observe_all(pol, nv, L, t, self.thc, N.ptr(self.hlc), sp),
+    def _plan_step(self, t: int, vids):
+        """Per-video plan of step t: V reductions, plan_reuse + SRAP (unless the
+        side stream already ran them during step t+1's head), plan_finish."""
+        nv, L, S, d = len(vids), self.L, self.S, self.d
+        st, lib, sp, pol = self.stream, N.lib(), N.stream_ptr(), self.pol.data_ptr()
+        nh = len(vids[0].hist)
+        pre = []
+        for j in range(nh):
+            pre.append([self.rows(vs.x) for vs in vids])
+            pre.append([self.rows(vs.hist[j]) for vs in vids])
+        early = self._early if (self._early is not None and self._early[0] == t) else None
+        self._early = None
+        if early is None:
+            do_srap = self.tog.srap and not (vids[0].seen == 0 or t == 0)
+            if do_srap:
+                pre += self._srap_tables(vids)
+        tabs = self._upload_idx(pre)
+        with self._ph("plan"):
+            for j in range(nh):
+                Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]),
+                             Dv.feat(self.arena, tabs[2 * j + 1]), S, d, nv, self.l1_v[j])
+            if early is None:
+                self._plan_reuse_srap(t, nv, do_srap, tabs[2 * nh:], st)
+            else:
+                st.wait_event(early[1])   # plan_reuse / SRAP of this step ran on the side stream
+            N.check(lib.qcb_policy_plan_finish(pol, nv, L, t, self.thc, N.ptr(self.srap_v),
+                                               N.ptr(self.l1_v), nh,
+                                               N.ptr(self.draws[t]), 0, sp), "plan_finish")
+            Dv.count(1)
+
+    # ------------------------------------------------------------------ synchronised mode
+    def _sync_plan(self, tn: int, nh: int):
+        """plan_step of step tn for the ONE policy state of the synchronised
+        mode, from the all-reduced sums in self.stats (schedule.py:281-328)."""
+        lib, sp, pol, L = N.lib(), N.stream_ptr(), self.pol.data_ptr(), self.L
+        N.check(lib.qcb_policy_plan_reuse(pol, 1, L, tn, self.thc, sp), "plan_reuse")
+        N.check(lib.qcb_policy_plan_finish(pol, 1, L, tn, self.thc, N.ptr(self.srap_g),
+                                           N.ptr(self.l1_g), nh, N.ptr(self.draws[tn]), 0, sp),
+                "plan_finish")
+        Dv.count(2)
+
+    def _sync_decide(self, t: int, vids):
+        """Synchronised mode, after reverse_step(t): every input of
+        the next decisions is known -- D sums of step t's recomputes
+        (schedule.py:342-350), S sums of the step-t features prev[l-1] vs prev[l]
+        (:301-305, for every layer: which ones plan(t-1) keeps depends on D) and
+        the V terms of x_{t-1} against the history (:293).  They are summed over
+        the local videos, packed into one f64 vector and all-reduced over the
+        ranks (ONE collective per step); then every rank runs the identical
+        observe + plan kernels, so all videos of all ranks take the same path.
+        Equals the reference formulas on the concatenated batch
+        (oracle.sample_sync): L1 terms, squares, dots and norms are additive."""
+        from . import dist as qdist
+        nv, L, S, d = len(vids), self.L, self.S, self.d
+        lib, sp, pol = N.lib(), N.stream_ptr(), self.pol.data_ptr()
+        nh = len(vids[0].hist)             # history after finalize_step(t)
+        do_plan = t > 0
+        do_srap = self.tog.srap and t - 1 > 0   # plan(t-1) is a boundary iff t-1 == 0
+        pre = []
+        if do_plan:
+            for j in range(nh):
+                pre.append([self.rows(vs.x) for vs in vids])
+                pre.append([self.rows(vs.hist[j]) for vs in vids])
+        if do_srap:
+            pre += self._srap_tables(vids)
+        tabs = self._upload_idx(pre)
+        with self._ph("plan"):
+            if do_plan:
+                for j in range(nh):
+                    Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]),
+                                 Dv.feat(self.arena, tabs[2 * j + 1]), S, d, nv, self.l1_v[j])
+            if do_srap:
+                Dv.reduce_srap(Dv.feat(self.arena, tabs[2 * nh]),
+                               Dv.feat(self.arena, tabs[2 * nh + 1]), S, d, L * nv,
+                               self.srap_v.view(L * nv, 3),
+                               seg_active=self.sync_mask_v.view(L * nv),
+                               workspace=self._srap_ws, dup_src=tabs[2 * nh + 2])
+            # pack the local sums (fixed video order: deterministic), then ranks
+            qdist.pack_decision_sums(self.stats, self.hlc_v, self.srap_v, self.l1_v)
+            qdist.allreduce_sum(self.stats, group=self.sync_group)
+            N.check(lib.qcb_policy_observe_all(pol, 1, L, t, self.thc, N.ptr(self.hlc_g), sp),
                     "observe_all")
             Dv.count(1)
-            if collect_features is not None:
-                x_now = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
-                collect_features.append((t, x_now, feats))
-            # ---------------- head + sampler update ----------------
+            self.pol_trace[t, :self.pol_size].copy_(self.pol[:self.pol_size], non_blocking=True)
+            if do_plan:
+                self._sync_plan(t - 1, nh)
+
+    # ------------------------------------------------------------------ one step
+    def _run_step(self, t: int, vids, act_tab, abits_of, collect_features, gen):
+        """Execute step t's plan: recomputed blocks with the HLC reductions,
+        observe, the noise head and the DDPM update (sampler.py:114-133)."""
+        nv, L, S, d = len(vids), self.L, self.S, self.d
+        F, Tk = self.cfg.frames, self.cfg.tokens_per_frame
+        st, lib, sp, pol = self.stream, N.lib(), N.stream_ptr(), self.pol.data_ptr()
+        first_launch = None
+        if self.host_profile is not None:
+            t_sync = time.perf_counter()
+        # ---------------- execute blocks ----------------
+        cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
+        feats = [] if collect_features is not None else None
+        for l in range(L):
+            acts = [act_tab[v][l] for v in range(nv)]
+            outs = list(cur)
+            rec = []
+            for v in range(nv):
+                a = acts[v]
+                if a == N.ACT_REUSE:
+                    outs[v] = vids[v].pool.inc(vids[v].cache[l])
+                elif a == N.ACT_PRUNE:
+                    outs[v] = vids[v].pool.inc(cur[v])
+                else:
+                    outs[v] = vids[v].pool.alloc()
+                    rec.append(v)
+            if rec:
+                # group recomputing videos by activation bits
+                groups: Dict[int, List[int]] = {}
+                for v in rec:
+                    groups.setdefault(abits_of[v], []).append(v)
+                need_d = [acts[v] == N.ACT_RECOMPUTE and vids[v].prev[l] is not None
+                          for v in range(nv)]
+                tabl = []
+                for bits, g in groups.items():
+                    tabl += [[self.rows(cur[v]) for v in g], [self.rows(outs[v]) for v in g], g]
+                if any(need_d):
+                    tabl += [[self.rows(outs[v]) for v in range(nv)],
+                             [self.rows(vids[v].cache[l] if vids[v].cache[l] is not None
+                                        else (vids[v].prev[l] or 0)) for v in range(nv)],
+                             [self.rows(vids[v].prev[l] or 0) for v in range(nv)],
+                             [int(x) for x in need_d]]
+                tl = self._upload_idx(tabl)
+                if self.host_profile is not None and first_launch is None:
+                    first_launch = time.perf_counter() - t_sync
+                for gi, (bits, g) in enumerate(groups.items()):
+                    self._block(l, t, g, bits, tl[3 * gi], tl[3 * gi + 1], tl[3 * gi + 2])
+                if any(need_d):
+                    base = 3 * len(groups)
+                    act = tl[base + 3].to(torch.int32)
+                    with self._ph("hlc"):
+                        Dv.reduce_hlc(Dv.feat(self.arena, tl[base]),
+                                      Dv.feat(self.arena, tl[base + 1]),
+                                      Dv.feat(self.arena, tl[base + 2]), S, d, nv,
+                                      self.hlc_v[l], seg_active=act)
+
+            # host mirror of the cache / prev references (schedule.py:349-351)
+            for v, vs in enumerate(vids):
+                if acts[v] == N.ACT_RECOMPUTE and t > 0:
+                    vs.pool.dec(vs.cache[l])
+                    vs.cache[l] = vs.pool.inc(outs[v])
+                vs.pool.dec(vs.prev[l])
+                vs.prev[l] = vs.pool.inc(outs[v])
+                vs.pool.dec(cur[v])
+            cur = outs
+            if feats is not None:
+                feats.append(torch.stack([self.slot_view(s) for s in cur]).cpu().numpy())
+        if self.host_profile is not None:
+            now = time.perf_counter() - t_sync
+            self.host_profile.append((now, first_launch if first_launch is not None else now))
+        if not self.sync:
+            # observe_block for every layer of the step (schedule.py:330-351)
+            N.check(lib.qcb_policy_observe_all(pol, nv, L, t, self.thc, N.ptr(self.hlc_v), sp),
+                    "observe_all")
+            Dv.count(1)
+        if collect_features is not None:
+            x_now = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
+            collect_features.append((t, x_now, feats))
+        # ---------------- head + sampler update ----------------
+        if not self.sync:
             self.pol_trace[t].copy_(self.pol, non_blocking=True)
             if t > 0:
                 # the next step's reuse plan depends only on the cache state just
                 # observed (schedule.py:286-309): overlap it with the head
                 self._early = self._early_plan(t - 1, vids, st)
-            tabh = self._upload_idx([[self.rows(c) for c in cur]])
-            with self._ph("head"):
-                if self.head_prep is not None:
-                    Dv.head_gemm(self.arena, self.head_prep, out=self.eps, bias=self.head_b,
-                                 seg_rows=self.Sp, seg_valid=S, nseg=nv, a_row0=tabh[0],
-                                 fallback_count=self.head_fallbacks)
-                else:
-                    Dv.gemm_f64(self.arena, self.head_w, out=self.eps, epilogue=N.EPI_BIAS,
-                                bias=self.head_b, seg_rows=self.Sp, seg_valid=S,
-                                a_row0=tabh[0], M=nv * self.Sp)
-            ph = self._ph("sampler")
-            ph.__enter__()
+        tabh = self._upload_idx([[self.rows(c) for c in cur]])
+        with self._ph("head"):
+            if self.head_prep is not None:
+                Dv.head_gemm(self.arena, self.head_prep, out=self.eps, bias=self.head_b,
+                             seg_rows=self.Sp, seg_valid=S, nseg=nv, a_row0=tabh[0],
+                             fallback_count=self.head_fallbacks)
+            else:
+                Dv.gemm_f64(self.arena, self.head_w, out=self.eps, epilogue=N.EPI_BIAS,
+                            bias=self.head_b, seg_rows=self.Sp, seg_valid=S,
+                            a_row0=tabh[0], M=nv * self.Sp)
+        with self._ph("sampler"):
             if t > 0:
                 if self.opts.noise == "numpy":
                     for v, vs in enumerate(vids):
@@ -678,11 +785,8 @@ class QuantCacheEngine:
                 if len(vs.hist) > self.th.history_k:
                     vs.pool.dec(vs.hist.pop(0))
                 vs.x = new
-            ph.__exit__(None, None, None)
-        out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
-        if return_device:
-            return out, vids
-        return out.cpu().numpy(), self._collect_traces(vids)
+        if self.sync:
+            self._sync_decide(t, vids)
 
     def traces_of(self, vids) -> List[List[TraceRecord]]:
         return self._collect_traces(vids)
@@ -694,8 +798,9 @@ class QuantCacheEngine:
         wb_of = lambda l: self.weight_bits.get(l, FP_BITS) if self.tog.aigq_weights else FP_BITS
         for t in range(self.T - 1, -1, -1):
             for v in range(nv):
+                pv = 0 if self.sync else v
                 p = N.QcbPolicyVideo.from_buffer_copy(
-                    raw[t, v * self.pol_size:(v + 1) * self.pol_size].tobytes())
+                    raw[t, pv * self.pol_size:(pv + 1) * self.pol_size].tobytes())
                 for l in range(self.L):
                     a = p.action[l]
                     wb = wb_of(l)

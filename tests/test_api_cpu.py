@@ -26,7 +26,7 @@ class TestConfig:  # test_harness.py:45-116
         cfg = harness.parse_config({"seed": 7})
         assert cfg.seeds == {"model": 7, "sampling": 7, "prune": 7}
         assert cfg.model["num_blocks"] == 8 and cfg.schedule["steps"] == 50
-        assert cfg.device == {"attention": "precise", "noise": "numpy"}
+        assert cfg.device == {"attention": "precise", "noise": "numpy", "decisions": "per_video"}
 
     @pytest.mark.parametrize("obj", [{"bogus": 1}, {"model": {"bogus": 1}},
                                      {"thresholds": {"nope": 1}}, {"device": {"x": 1}}])
@@ -39,7 +39,8 @@ class TestConfig:  # test_harness.py:45-116
         {"schedule": {"beta_start": 0.5, "beta_end": 0.1}},
         {"thresholds": {"delta1": 3.0, "delta2": 1.0}}, {"toggles": {"hlc": 1}},
         {"weight_bits": {"0": 5}}, {"weight_bits": {"0": 8}}, {"bit_budget": 3},
-        {"toggles": {"aigq_weights": True}}, {"device": {"attention": "magic"}}])
+        {"toggles": {"aigq_weights": True}}, {"device": {"attention": "magic"}},
+        {"device": {"decisions": "global"}}])
     def test_validation(self, obj):
         with pytest.raises(ConfigurationError):
             harness.parse_config(obj)

@@ -109,3 +109,64 @@ def test_repeat_runs_byte_identical(golden_dir):
     assert a.output.tobytes() == b.output.tobytes()
     assert [r.to_json_obj() for r in a.scheduler.trace] == \
         [r.to_json_obj() for r in b.scheduler.trace]
+
+
+def _sync_cfg(golden_dir, tname="full"):
+    from paper_2503_06545_b200 import harness
+    base = dict(SMALL, calibration=os.path.join(golden_dir, "calib_small.json"),
+                toggles=TOGGLES[tname], device={"decisions": "synchronized"})
+    return harness.parse_config(base)
+
+
+def test_sync_single_video_equals_per_video(golden_dir, runs):
+    """With one video the synchronised mode is the reference run."""
+    from paper_2503_06545_b200 import harness
+    cfg = _sync_cfg(golden_dir)
+    calib = harness.load_calibration(cfg.calibration)
+    res = harness.run_single(cfg, cfg.toggles_obj(), calib)
+    assert np.array_equal(res.output, runs["small_full"])
+    ref_trace = [json.loads(l) for l in
+                 open(os.path.join(golden_dir, "trace_small_full.jsonl"))]
+    got = [r.to_json_obj() for r in res.scheduler.trace]
+    for a, b in zip(ref_trace, got):
+        for k in ("t", "layer", "action", "bits", "wbits", "macs"):
+            assert a[k] == b[k], (k, a, b)
+
+
+@pytest.mark.parametrize("tname", ["full", "hlc_aigq"])
+def test_sync_mode_matches_concatenated_batch_oracle(golden_dir, tname):
+    """Synchronised decisions (north_star: one all-reduce of the decision sums
+    per step, every rank on one path) == oracle.sample_sync: the reference
+    formulas on the concatenated batch.  Bars: one shared trace, decisions
+    identical at every (step, layer), D / S / V within 1e-9 relative, latents
+    bit-identical."""
+    from dataclasses import fields
+    from paper_2503_06545_b200 import harness
+    from oracle import qc_oracle as O
+    cfg = _sync_cfg(golden_dir, tname)
+    calib = harness.load_calibration(cfg.calibration)
+    tog = cfg.toggles_obj()
+    seeds = [3, 11, 12]
+    eng, _ = harness.build_engine(cfg, tog, calib, max_videos=len(seeds))
+    outs, traces = eng.generate(seeds)
+    thr = harness.resolve_thresholds(cfg, calib, tog)
+    th = O.Thresholds(**{f.name: getattr(thr, f.name) for f in fields(O.Thresholds)})
+    wbits = harness.resolve_weight_bits(cfg, calib) if tog.aigq_weights else {}
+    want, st = O.sample_sync(O.ModelDims(3, 16, 2, 4, 2, 8, cfg.seeds["model"]), 10, th,
+                             (tog.hlc, tog.aigq_weights, tog.aigq_acts, tog.srap), seeds,
+                             prune_seed=cfg.seeds["prune"], weight_bits=wbits,
+                             act_absmax=calib.act_absmax if tog.aigq_weights else None,
+                             sign_seed=cfg.seeds["model"])
+    for v in range(len(seeds)):
+        got = [r.to_json_obj() for r in traces[v]]
+        assert got == [r.to_json_obj() for r in traces[0]]      # one path for all
+        assert len(got) == len(st.trace)
+        for a, b in zip(st.trace, got):
+            for k in ("t", "layer", "action", "bits", "wbits", "macs"):
+                assert a[k] == b[k], (k, a, b)
+            for k in ("D", "S", "V"):
+                if a[k] is not None and b[k] is not None:
+                    assert b[k] == pytest.approx(a[k], rel=1e-9, abs=1e-12), (k, a, b)
+                elif k != "V":
+                    assert a[k] is None and b[k] is None, (k, a, b)
+        assert np.array_equal(outs[v], want[v]), float(np.abs(outs[v] - want[v]).max())

@@ -152,3 +152,61 @@ class TestModelFixtures:
         assert np.array_equal(out, f[f"{name}_out"])
         gen, _ = O.sample(dims, 4, seed=2)
         assert np.array_equal(gen, f[f"{name}_gen4"])
+
+
+def _oracle_run_args(golden_dir, tog):
+    """The run_single wiring (harness.py:416-437) resolved on the host for the
+    small config with the reference's calibration, as oracle.sample arguments."""
+    from paper_2503_06545_b200 import harness
+    from dataclasses import fields
+    cfg = harness.parse_config({
+        "seed": 3, "model": {"num_blocks": 3, "model_dim": 16, "num_heads": 2,
+                             "tokens_per_frame": 4, "frames": 2, "cond_dim": 8},
+        "schedule": {"steps": 10}, "toggles": tog,
+        "calibration": os.path.join(golden_dir, "calib_small.json")})
+    calib = harness.load_calibration(cfg.calibration)
+    toggles = cfg.toggles_obj()
+    thr = harness.resolve_thresholds(cfg, calib, toggles)
+    th = O.Thresholds(**{f.name: getattr(thr, f.name) for f in fields(O.Thresholds)})
+    wbits = harness.resolve_weight_bits(cfg, calib) if toggles.aigq_weights else {}
+    dims = O.ModelDims(3, 16, 2, 4, 2, 8, cfg.seeds["model"])
+    kw = dict(th=th, toggles=(toggles.hlc, toggles.aigq_weights, toggles.aigq_acts,
+                              toggles.srap),
+              prune_seed=cfg.seeds["prune"], weight_bits=wbits,
+              act_absmax=calib.act_absmax if toggles.aigq_weights else None,
+              sign_seed=cfg.seeds["model"])
+    return dims, cfg.seeds["sampling"], kw
+
+
+class TestSampler:
+    FULL = dict(hlc=True, aigq_weights=True, aigq_acts=True, srap=True)
+
+    def test_full_stack_sample_matches_reference(self, golden_dir):
+        """oracle.sample with every toggle reproduces the reference's run_single
+        output bit for bit and its trace decision for decision."""
+        dims, seed, kw = _oracle_run_args(golden_dir, self.FULL)
+        out, st = O.sample(dims, 10, seed=seed, **kw)
+        assert np.array_equal(out, load(golden_dir, "runs.npz")["small_full"])
+        ref = [json.loads(l) for l in open(os.path.join(golden_dir, "trace_small_full.jsonl"))]
+        ref = [r for r in ref if r["layer"] != "head"]
+        got = [r for r in st.trace if r["layer"] != "head"]
+        assert len(got) == len(ref)
+        for a, b in zip(ref, got):
+            for k in ("t", "layer", "action", "bits", "wbits", "macs"):
+                assert a[k] == b[k], (k, a, b)
+
+    def test_sync_mode_single_video_is_sample(self, golden_dir):
+        dims, seed, kw = _oracle_run_args(golden_dir, self.FULL)
+        out, _ = O.sample_sync(dims, 10, seeds=[seed], **kw)
+        assert np.array_equal(out[0], load(golden_dir, "runs.npz")["small_full"])
+
+    def test_sync_mode_shares_one_path(self, golden_dir):
+        """Two videos under one concatenated-batch policy: one trace, and the
+        statistics are the reference formulas on the stacked features."""
+        dims, seed, kw = _oracle_run_args(golden_dir, self.FULL)
+        out, st = O.sample_sync(dims, 10, seeds=[seed, seed + 8], **kw)
+        assert out.shape == (2, 2, 4, 16)
+        assert len(st.trace) == 10 * (dims.num_blocks + 1)
+        solo, _ = O.sample(dims, 10, seed=seed + 8, **kw)
+        assert not np.array_equal(out[1], out[0])
+        assert np.isfinite(out).all() and np.isfinite(solo).all()
