@@ -91,6 +91,8 @@ typedef struct QcbGemm {
   int block_n;                 /* 0 = auto                                      */
   const int* seg_active;       /* nullable: per-segment flag, skip inactive     */
   long long out_rows;          /* rows of the output buffer (TMA bounds); 0 = M */
+  long long resid_rows;        /* rows of the residual buffer (TMA bounds); 0 =  */
+                               /* out_rows when resid == out, else M             */
 } QcbGemm;
 
 int qcb_gemm_u8(const QcbGemm* g, void* stream);
@@ -119,13 +121,15 @@ typedef struct QcbGemmF64 {
 int qcb_gemm_f64(const QcbGemmF64* g, void* stream);
 
 /* Noise head out = f32(mm(x, W)) + bias (model.py:228 with tensor.py:43-60) on
- * the int8 tensor cores: x rows and W columns split into base-128 digit planes,
- * one exact u8 GEMM per digit diagonal, f64 combination with an error bound;
+ * the int8 tensor cores: x rows and W columns split into 6 base-256 digit planes,
+ * one grouped exact u8 GEMM over the digit diagonals, f64 combination with an
+ * error bound;
  * elements whose bound straddles an f32 rounding boundary are recomputed with
  * the reference's ascending-k f64 FMA chain, so every output equals mm's.
  * qcb_head_prep writes W's planes / statistics into `prep` once
  * (qcb_head_prep_bytes); qcb_head_gemm runs per call with a workspace of
- * qcb_head_workspace_bytes(nseg * seg_rows, K, N).  K and N must be multiples of 4. */
+ * qcb_head_workspace_bytes(nseg * seg_rows, K, N).  K and N must be multiples of 4;
+ * K <= 5504 (6 K 255^2 < 2^31, else QCB_ERR_OVERFLOW). */
 typedef struct QcbHeadGemm {
   int nseg, seg_rows, seg_valid; /* rows = nseg * seg_rows; rows >= seg_valid of a */
   int K, N;                      /* segment are padding (not written)             */

@@ -31,7 +31,7 @@ class QcbGemm(C.Structure):
                 ("w_zero", vp), ("w_colsum", vp), ("out", vp), ("ldo", i64),
                 ("out_row0", vp), ("resid", vp), ("ldr", i64), ("resid_row0", vp),
                 ("gate", vp), ("gate_scalar", f32), ("epilogue", i32), ("block_n", i32),
-                ("seg_active", vp), ("out_rows", i64)]
+                ("seg_active", vp), ("out_rows", i64), ("resid_rows", i64)]
 
 
 class QcbGemmF64(C.Structure):

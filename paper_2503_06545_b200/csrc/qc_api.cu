@@ -31,7 +31,7 @@ extern "C" int qcb_gemm_u8(const QcbGemm* g, void* stream) {
 extern "C" int qcb_head_prep(const float* w, int K, int N, void* prep, void* stream) {
   if (!w || !prep) return QCB_ERR_VALUE;
   if (K <= 0 || N <= 0) return QCB_ERR_DIM;
-  if (7LL * K * 255LL * 255LL > 2147483647LL) return QCB_ERR_OVERFLOW;
+  if (6LL * K * 255LL * 255LL > 2147483647LL) return QCB_ERR_OVERFLOW;
   return qc::head_prep_launch(w, K, N, prep, (cudaStream_t)stream);
 }
 
@@ -42,7 +42,7 @@ extern "C" int qcb_head_gemm(const QcbHeadGemm* g, void* stream) {
     return QCB_ERR_DIM;
   if (g->K % 4 || g->N % 4 || g->ldx % 4 || (reinterpret_cast<uintptr_t>(g->x) & 15))
     return QCB_ERR_DIM;   // 16-byte row vectors (digits, outputs, exact fallback)
-  if (7LL * g->K * 255LL * 255LL > 2147483647LL) return QCB_ERR_OVERFLOW;
+  if (6LL * g->K * 255LL * 255LL > 2147483647LL) return QCB_ERR_OVERFLOW;
   if ((long long)g->nseg * g->seg_rows * g->N >= (1LL << 31)) return QCB_ERR_DIM;
   return qc::head_gemm_launch(g, (cudaStream_t)stream);
 }

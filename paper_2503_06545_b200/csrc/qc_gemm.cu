@@ -32,9 +32,8 @@ constexpr int kUmmaK = 32;    // K per tcgen05.mma kind::i8
 constexpr int kEpiWarps = 8;                    // 2 per TMEM lane quarter
 constexpr int kThreads = 128 + 32 * kEpiWarps;  // TMA, MMA, TMEM-alloc, spare + epilogue
 
-template <int BN>
+template <int BN, bool RES = false>
 struct GemmCfg {
-  static constexpr int kStages = BN >= 256 ? 3 : (BN >= 192 ? 4 : (BN >= 128 ? 5 : (BN >= 64 ? 7 : 8)));
   static constexpr int kABytes = kBlockM * kBlockK;
   static constexpr int kBBytes = BN * kBlockK;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -43,12 +42,19 @@ struct GemmCfg {
                                         : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256
                                                           : 512;
-  // epilogue: 4 warps x one 32x32 f32 staging tile (128B-swizzled, TMA store)
+  // epilogue: per warp one 32x32 f32 staging tile (128B-swizzled, TMA store)
   static constexpr int kStageOutBytes = kEpiWarps * 32 * 32 * 4;
+  // residual epilogues: per warp two 32x32 f32 residual slabs (TMA loads)
+  static constexpr int kResBytes = RES ? kEpiWarps * 2 * 32 * 32 * 4 : 0;
   // per-tile column parameters, double-buffered by accumulator stage
   static constexpr int kColBytes = 2 * BN * (8 + 4 + 4);
-  static constexpr int kSmemBytes =
-      kStages * kStageBytes + kStageOutBytes + kColBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kFixedBytes =
+      kStageOutBytes + kResBytes + kColBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kStagesWanted =
+      BN >= 256 ? 3 : (BN >= 192 ? 4 : (BN >= 128 ? 5 : (BN >= 64 ? 7 : 8)));
+  static constexpr int kStagesFit = (227 * 1024 - kFixedBytes) / kStageBytes;
+  static constexpr int kStages = kStagesWanted < kStagesFit ? kStagesWanted : kStagesFit;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kFixedBytes;
 };
 
 // one output column's epilogue parameters: a single 16-byte broadcast load
@@ -84,6 +90,7 @@ struct GemmParams {
   int mode;
   const int* seg_active;  // nullable: skip tiles of inactive segments
   int tma_store;          // 1: each 32-row warp slab maps to contiguous output rows
+  int tma_resid;          // 1: residual slabs come by TMA (same contiguity, map_res)
   // Grouped launch (0 = off): output columns [g*group_n, (g+1)*group_n) form
   // group g, reduced over K_g = (g+1)*group_k with row sums rowsum + g*rowsum_stride
   // (one launch for the head's digit diagonals, qc_head.cu).
@@ -96,8 +103,10 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_u8_tcgen05(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
-                    const __grid_constant__ CUtensorMap map_out, const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+                    const __grid_constant__ CUtensorMap map_out,
+                    const __grid_constant__ CUtensorMap map_res, const GemmParams p) {
+  constexpr bool resid_mode = (MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID);
+  using Cfg = GemmCfg<BN, resid_mode>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // Pointers are derived from the __shared__ symbol directly (no integer
   // round-trip) so the compiler keeps them in the shared window (LDS/STS).
@@ -106,12 +115,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + Cfg::kStages * Cfg::kABytes;
   uint8_t* smem_out = smem + Cfg::kStages * Cfg::kStageBytes;           // 1024-aligned
-  ColParam* col = reinterpret_cast<ColParam*>(smem_out + Cfg::kStageOutBytes);  // [2][BN]
+  uint8_t* smem_res = smem_out + Cfg::kStageOutBytes;                   // 1024-aligned
+  ColParam* col = reinterpret_cast<ColParam*>(smem_res + Cfg::kResBytes);  // [2][BN]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(col + 2 * BN);
   uint64_t* empty_bar = full_bar + Cfg::kStages;
   uint64_t* tfull_bar = empty_bar + Cfg::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* res_bar = tempty_bar + 2;   // [kEpiWarps][2] residual slab barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + 2 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -133,6 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], kEpiWarps);
     }
+    for (int r = 0; r < 2 * kEpiWarps; ++r) mbar_init(&res_bar[r], 1);
+    if (resid_mode && p.tma_resid) tma_prefetch(&map_res);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -215,7 +228,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int et = threadIdx.x - 128;        // epilogue thread id
     const int half = (warp - 4) >> 2;       // which column half of each tile this warp owns
     uint8_t* stage_out = smem_out + (warp - 4) * 4096;
-    constexpr bool resid_mode = (MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID);
+    // residual slabs: two 4 KB buffers per warp, filled by TMA one chunk ahead
+    uint8_t* res_buf = smem_res + (warp - 4) * 8192;
+    uint64_t* rbar = res_bar + 2 * (warp - 4);
+    const bool res_tma = resid_mode && p.tma_resid;
+    uint32_t res_it = 0;      // residual slabs issued by this warp (buffer = res_it & 1)
+    uint32_t res_phase = 0;   // bit b: parity of buffer b's next completion
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -248,6 +266,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg = m / p.seg_rows;
       const int mrow = m - seg * p.seg_rows;
       const bool row_ok = (m < p.M) && (mrow < p.seg_valid);
+      // a slab with no valid row (segment padding) is neither read nor written
+      const bool slab_live = __any_sync(0xffffffffu, row_ok);
       double sa = 0.0;
       int za = 0, rs = 0;
       float gate = p.gate_scalar;
@@ -264,16 +284,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // acc = raw - zw*rowsum - za*colsum + K*za*zw = raw - zw*(rowsum - K*za) - za*colsum
       const int tr = rs - k_eff * za;
-      // first output row of this warp's 32-row slab (TMA store path)
+      // first output / residual row of this warp's 32-row slab (TMA paths; a live
+      // slab's lane 0 is a valid row since padding rows sit at a segment's end)
       const long long orow_slab = __shfl_sync(0xffffffffu, orow, 0);
+      const long long rrow_slab = __shfl_sync(0xffffffffu, rrow, 0);
+      const int n_chunks = min(BN / 32, (p.N - n0 + 31) / 32);
 
-      // residual rows are independent of the MMA: the first chunk's loads are
-      // issued before waiting for the accumulator, each next chunk's during the
-      // current chunk's math (register double buffer)
-      float rv_next[32];
-      auto load_resid = [&](int c, float (&dst)[32]) {
+      // residual chunk c -> registers: TMA slab (issued one chunk ahead) or
+      // per-row vector loads
+      auto issue_res = [&](int c) {
+        if (lane == 0) {
+          uint8_t* buf = res_buf + (res_it & 1) * 4096;
+          fence_proxy_async_smem();   // prior generic reads of this buffer are done
+          mbar_arrive_expect_tx(&rbar[res_it & 1], 4096);
+          tma_load_2d(&map_res, &rbar[res_it & 1], buf, n0 + c * 32, (int)rrow_slab);
+        }
+        ++res_it;
+      };
+      auto load_resid_rows = [&](int c, float (&dst)[32]) {
         const int nb = n0 + c * 32;
-        if (!resid_mode || !row_ok || c >= BN / 32 || nb >= p.N) return;
+        if (!row_ok) return;
         const float* rp = p.resid + rrow * p.ldr + nb;
         if (nb + 32 <= p.N && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
 #pragma unroll
@@ -286,22 +316,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) dst[j] = (nb + j < p.N) ? rp[j] : 0.f;
         }
       };
-      if (resid_mode) load_resid(half, rv_next);
+      uint32_t res_first = res_it;   // buffer of this tile's first chunk
+      if (res_tma && slab_live && half < n_chunks) issue_res(half);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      for (int c = half; c < n_chunks; c += 2) {
         const int nb = n0 + c * 32;
-        if (nb >= p.N) break;
         float rv[32];
         if (resid_mode) {
+          if (res_tma) {
+            if (slab_live) {
+              if (c + 2 < n_chunks) issue_res(c + 2);   // next chunk into the other buffer
+              const uint32_t b = res_first & 1;
+              mbar_wait(&rbar[b], (res_phase >> b) & 1);
+              res_phase ^= 1u << b;
+              const uint8_t* rowp = res_buf + b * 4096 + lane * 128;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) rv[j] = rv_next[j];
-          load_resid(c + 2, rv_next);
+              for (int j = 0; j < 8; ++j) {
+                const float4 t4 =
+                    *reinterpret_cast<const float4*>(rowp + ((j ^ (lane & 7)) << 4));
+                rv[4 * j] = t4.x; rv[4 * j + 1] = t4.y; rv[4 * j + 2] = t4.z; rv[4 * j + 3] = t4.w;
+              }
+              __syncwarp();   // every lane has read buffer b before it is refilled
+              ++res_first;
+            }
+          } else {
+            load_resid_rows(c, rv);
+          }
         }
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
+        if (!slab_live) continue;
         float v[32];
         // y = f32(f64(sa*sw) * acc); int->f64 by a magic add on the FP64 pipe
         // so only the final rounding uses the conversion (XU) pipe.
@@ -314,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const double d = __hiloint2double(0x43300000, accb) - 4503601774854144.0;
             v[j] = __double2float_rn(__dmul_rn(cp.sw, d));
           }
-          if (!__all_sync(0xffffffffu, row_ok)) {   // padding rows are written as 0
+          if (!__all_sync(0xffffffffu, row_ok)) {   // padding rows: residual (or 0)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = row_ok ? v[j] : 0.0f;
           }
@@ -440,7 +487,8 @@ int num_sms() {
 
 template <int BN, int MODE>
 static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
-  using Cfg = GemmCfg<BN>;
+  constexpr bool resid_mode = (MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID);
+  using Cfg = GemmCfg<BN, resid_mode>;
   CUtensorMap ma, mb;
   int rc = make_map_u8(&ma, g->a_codes, g->M, g->K, g->lda, kBlockM);
   if (rc) return rc;
@@ -483,6 +531,19 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   if (slab_contig && (g->ldo * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->out) & 15) == 0 &&
       make_map_out(&mo, g->out, out_rows, g->N, g->ldo) == QCB_OK)
     p.tma_store = 1;
+  // TMA residual slabs under the same contiguity rule (residual rows per segment)
+  CUtensorMap mr = ma;
+  p.tma_resid = 0;
+  if (resid_mode && g->resid != nullptr) {
+    const bool rslab_contig =
+        (p.seg_rows % 32 == 0) || (nseg == 1 && g->resid_row0 == nullptr);
+    const long long resid_rows =
+        g->resid_rows > 0 ? g->resid_rows : (g->resid == g->out ? out_rows : (long long)g->M);
+    if (rslab_contig && (g->ldr * 4) % 16 == 0 &&
+        (reinterpret_cast<uintptr_t>(g->resid) & 15) == 0 &&
+        make_map_out(&mr, g->resid, resid_rows, g->N, g->ldr) == QCB_OK)
+      p.tma_resid = 1;
+  }
   static_assert(Cfg::kSmemBytes <= 227 * 1024, "GEMM smem budget exceeds 227 KB");
   static bool attr_set = false;
   if (!attr_set) {
@@ -494,7 +555,7 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   int tiles = p.num_m_tiles * p.num_n_tiles;
   int grid = tiles < num_sms() ? tiles : num_sms();
   launch_pdl(gemm_u8_tcgen05<BN, MODE>, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, st, ma, mb,
-             mo, p);
+             mo, mr, p);
   return launch_status();
 }
 

@@ -2,19 +2,29 @@
 // tensor.py:43-60: ascending-k f64 accumulation of exact f32*f32 products),
 // on the int8 tensor cores with an exactness certificate.
 //
-// Digit planes.  Each x row i is scaled by 2^-e_i (max|x_i| < 2^e_i) and split
-// into kHeadDigits balanced base-128 digits D_s in [-64, 64] of weight
-// 2^(e_i - 6 - 7 s); each W column j likewise (E_t, 2^(f_j - 6 - 7 t)).  Digits
-// are stored as u8 codes D + 64, so the existing tcgen05 u8 GEMM with zero
-// point 64 yields exact integer sums.  The products with s + t = d share the
-// weight 2^(e+f-12-7d): one GEMM per diagonal d = 0..kHeadDigits-1 with A =
-// [X_0 .. X_d] (a prefix of the row's planes) and B_d = [E_d .. E_0] per column,
-// K' = (d+1) K, accumulates them exactly in s32 (|sum| <= 7 K 64^2 < 2^31).
+// Digit planes.  Each x row i is scaled by 2^-e_i (max|x_i| < 2^e_i), r = x 2^-e
+// in (-1, 1), and split into kHeadDigits = 6 base-256 floor digits, stored as
+// u8 codes U_s in [0, 255]:
+//   r = (U_0 - 128) 2^-7 + sum_{s>=1} U_s 2^(-7-8s) + tau,   0 <= tau < 2^-47.
+// Read with zero point 128 on every plane, B_s = U_s - 128 in [-128, 127] is a
+// balanced digit (mean ~0, so the dropped digit pairs stay small) and
+//   r = rho + c + tau,  rho = sum_s B_s 2^(-7-8s),  c = 128 sum_{s=1..5} 2^(-7-8s).
+// Each W column j likewise (V_t, C_t, sigma, exponent f_j).  Then
+//   sum_k r q = sum_d 2^(-14-8d) A_d + c (sum rho + sum sigma) + c^2 K + (tau terms)
+// with the diagonal sums A_d = sum_{s+t=d} sum_k B_s C_t.  All six diagonals run
+// as ONE grouped tcgen05 u8 GEMM (zero point 128, which it removes exactly):
+// column group d has A = [U_0 .. U_d] (a prefix of the row's planes), B_d =
+// [V_d .. V_0] per column and K' = (d+1) K; |A_d| <= 6 K 128^2 and the raw code
+// sums <= 6 K 255^2 < 2^31.  Against 7 balanced base-128 planes (28 digit pairs)
+// this is 21 pairs: a quarter less tensor-core work.  The row and column offset
+// terms R_i = c sum rho_i and Q_j = c (sum sigma_j + c K) come from exact integer
+// plane sums.
 //
-// Certificate.  S^ = 2^(e+f-12) sum_d acc_d 2^-7d (f64) differs from the exact
-// sum S by at most T1 (diagonals d >= kHeadDigits dropped) + T2 (digit
-// truncation) + T3 (f64 combination rounding); the reference's sequential sum
-// differs from S by at most T4 = (K-1) 2^-53 sum|x w| <= (K-1) 2^-53 |x|_2 |w|_2.
+// Certificate.  S^ = 2^(e+f) (2^-14 sum_d A_d 2^-8d + R_i + Q_j) (f64) differs
+// from the exact sum S by at most T1 (diagonals d >= kHeadDigits dropped) + T2
+// (digit truncation) + T3 (f64 rounding of the combination and of R, Q); the
+// reference's sequential sum differs from S by at most
+// T4 = (K-1) 2^-53 sum|x w| <= (K-1) 2^-53 |x|_2 |w|_2.
 // When [S^ - E, S^ + E] (E = T1+T2+T3+T4, padded) holds no f32 rounding
 // boundary, RN32(S^) == RN32(reference); other elements are listed and
 // recomputed with the reference's ascending-k f64 FMA chain (bit-exact).
@@ -25,8 +35,11 @@
 
 namespace qc {
 
-constexpr int kHeadDigits = 7;
+constexpr int kHeadDigits = 6;
+constexpr int kZp = 128;   // code zero point of every digit plane
 constexpr int kHeadSliceWarps = 8;
+// c = sum_{s=1..5} 128 2^(-7-8s) = sum_{s=1..5} 2^-8s;  c 2^40 = 2^32 + 2^24 + 2^16 + 2^8 + 1
+constexpr double kC = 4311810305.0 * 0x1p-40;
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -34,12 +47,12 @@ static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 // ------------------------------------------------------------------ layouts
 struct HeadPrepLayout {   // one-time weight side
   size_t bstack;            // B_d codes stacked [kHeadDigits N][ldb], ldb = a16(kHeadDigits K):
-                            // row d N + n = [E_d .. E_0] of column n (zero padded)
-  size_t csum;              // s32 [kHeadDigits][N]
+                            // row d N + n = [V_d .. V_0] of column n (zero padded)
+  size_t csum;              // s32 [kHeadDigits][N]: prefix code sums of B_d's row
   size_t cstat;             // f64 [N][8]: certificate column factors (head_prep_cols)
   size_t wt;                // f32 [N][K] (W^T for the exact fallback)
-  size_t ones;              // f64 [N] = 1.0 (w_scale), s32 [N] = 64 (w_zero) after it
-  size_t zeros64;
+  size_t ones;              // f64 [kHeadDigits N] = 1.0 (w_scale)
+  size_t wzero;             // s32 [kHeadDigits N] = 128 (w_zero)
   size_t total;
 };
 
@@ -56,7 +69,7 @@ static HeadPrepLayout prep_layout(int K, int N) {
   off = a256(off + (size_t)4 * N * K);
   L.ones = off;
   off = a256(off + (size_t)8 * kHeadDigits * N);
-  L.zeros64 = off;
+  L.wzero = off;
   off = a256(off + (size_t)4 * kHeadDigits * N);
   L.total = off;
   return L;
@@ -64,12 +77,12 @@ static HeadPrepLayout prep_layout(int K, int N) {
 
 struct HeadWsLayout {     // per call
   size_t planes;  // u8 [M][ldp], ldp = a16(kHeadDigits K)
-  size_t rsum;    // s32 [kHeadDigits][M] (prefix over planes)
+  size_t rsum;    // s32 [kHeadDigits][M]: prefix code sums over planes 0..d
   size_t rstat;   // f64 [M][8]: certificate row factors (head_slice_rows)
   size_t acc;     // s32 [M][kHeadDigits N] (diagonal d at columns d N ..)
   size_t list;    // s32 [M*N] flagged elements (i*N + j)
   size_t count;   // s32
-  size_t one;     // f64 1.0, s32 64
+  size_t one;     // f64 1.0, s32 128
   size_t total;
 };
 
@@ -94,15 +107,21 @@ static HeadWsLayout ws_layout(long long M, int K, int N) {
   return L;
 }
 
-// Balanced base-128 digits of r in (-1, 1): r = sum_s D_s 2^(-6-7s) + rest,
-// |D_s| <= 64, |rest| <= 2^-(6 + 7 kHeadDigits) / 2.  Every step is exact in f64.
-QC_DEV void head_digits(double r, int (&D)[kHeadDigits]) {
-  double v = r * 64.0;
+// Codes of r in (-1, 1) (see the header).  floor() by a round-down add of a
+// magic constant on the FP64 pipe; the integer is the sum's low word (no
+// conversion-pipe instructions).  Every step is exact.
+QC_DEV void head_digits(double r, int (&U)[kHeadDigits]) {
+  constexpr double kM0 = 6755399441055744.0;   // 1.5 2^52: floor for |v| < 2^51
+  constexpr double kM1 = 4503599627370496.0;   // 2^52: floor for 0 <= v < 2^52
+  double v = r * 128.0;   // (-128, 128)
+  double t = __dadd_rd(v, kM0);
+  U[0] = __double2loint(t) + kZp;
+  v = (v - (t - kM0)) * 256.0;   // [0, 256)
 #pragma unroll
-  for (int s = 0; s < kHeadDigits; ++s) {
-    const double q = (v + 6755399441055744.0) - 6755399441055744.0;   // rint, |v| <= 64
-    D[s] = (int)q;
-    v = (v - q) * 128.0;
+  for (int s = 1; s < kHeadDigits; ++s) {
+    t = __dadd_rd(v, kM1);
+    U[s] = __double2loint(t);
+    v = (v - (t - kM1)) * 256.0;
   }
 }
 
@@ -117,6 +136,15 @@ QC_DEV int head_exponent(double amax) {
   int e;
   frexp(amax, &e);   // amax = m 2^e, m in [0.5, 1)
   return e;
+}
+
+// sum_k rho_k 2^47 = sum_s (plane sum_s - 128 K) 2^(40-8s): exact in int64
+// (|plane sum - 128 K| <= 128 K < 2^20)
+QC_DEV long long rho_sum_2p47(const long long (&ps)[kHeadDigits], int K) {
+  long long t = 0;
+#pragma unroll
+  for (int s = 0; s < kHeadDigits; ++s) t += (ps[s] - (long long)kZp * K) << (40 - 8 * s);
+  return t;
 }
 
 // ------------------------------------------------------------------ weights
@@ -142,22 +170,22 @@ __global__ void head_prep_cols(const float* __restrict__ w, int K, int N, uint8_
     l2 += __shfl_xor_sync(0xffffffffu, l2, o);
   }
   const int f = head_exponent(amax);
-  int cs[kHeadDigits] = {0, 0, 0, 0, 0, 0, 0};
-  double sq[kHeadDigits] = {0, 0, 0, 0, 0, 0, 0};
+  long long cs[kHeadDigits] = {0, 0, 0, 0, 0, 0};
+  long long sq[kHeadDigits] = {0, 0, 0, 0, 0, 0};   // sum (V - 128)^2
+  const size_t ldb = a16((size_t)kHeadDigits * K);
   for (int k = lane; k < K; k += 32) {
-    int E[kHeadDigits];
-    head_digits((double)w[(size_t)k * N + j] * pow2(-f), E);
+    int V[kHeadDigits];
+    head_digits((double)w[(size_t)k * N + j] * pow2(-f), V);
 #pragma unroll
     for (int t = 0; t < kHeadDigits; ++t) {
-      cs[t] += E[t] + 64;
-      sq[t] += (double)(E[t] * E[t]);
+      cs[t] += V[t];
+      sq[t] += (long long)((V[t] - kZp) * (V[t] - kZp));
     }
-    const size_t ldb = a16((size_t)kHeadDigits * K);
 #pragma unroll
     for (int d = 0; d < kHeadDigits; ++d) {
       uint8_t* bd = base + L.bstack + ((size_t)d * N + j) * ldb;
 #pragma unroll
-      for (int t = 0; t <= d; ++t) bd[(size_t)(d - t) * K + k] = (uint8_t)(E[t] + 64);
+      for (int t = 0; t <= d; ++t) bd[(size_t)(d - t) * K + k] = (uint8_t)V[t];
     }
   }
 #pragma unroll
@@ -166,27 +194,28 @@ __global__ void head_prep_cols(const float* __restrict__ w, int K, int N, uint8_
       cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], o);
       sq[t] += __shfl_xor_sync(0xffffffffu, sq[t], o);
     }
-  double rho = 0.0;   // max over digit planes t >= 1 of |E_t|_2 (exact integer sums)
+  long long rho = 0;   // max over digit planes t >= 1 of |C_t|_2^2
 #pragma unroll
-  for (int t = 1; t < kHeadDigits; ++t) rho = fmax(rho, sq[t]);
+  for (int t = 1; t < kHeadDigits; ++t) rho = sq[t] > rho ? sq[t] : rho;
   if (lane == 0) {
     int* csum = reinterpret_cast<int*>(base + L.csum);
-    int pre = 0;
+    long long pre = 0;
     for (int d = 0; d < kHeadDigits; ++d) {
-      pre += cs[d];   // B_d holds E_0..E_d
-      csum[(size_t)d * N + j] = pre;
+      pre += cs[d];   // B_d holds V_0..V_d
+      csum[(size_t)d * N + j] = (int)pre;
     }
-    // certificate column factors (see head_combine): 2^f, |E|_2 2^f, |w|_1, 2^(f-49), |w|_2
+    // certificate column factors (see head_combine)
     double* cst = reinterpret_cast<double*>(base + L.cstat) + (size_t)j * 8;
     cst[0] = pow2(f);
-    cst[1] = up(sqrt(rho)) * pow2(f);
+    cst[1] = up(sqrt((double)rho)) * pow2(f);
     cst[2] = up(l1);
-    cst[3] = pow2(f - 49);
+    cst[3] = pow2(f - 47);
     cst[4] = up(sqrt(l2));
-    cst[5] = cst[6] = cst[7] = 0.0;
+    cst[5] = kC * ((double)rho_sum_2p47(cs, K) * 0x1p-47 + kC * (double)K);   // Q_j
+    cst[6] = cst[7] = 0.0;
     for (int d = 0; d < kHeadDigits; ++d) {
       reinterpret_cast<double*>(base + L.ones)[(size_t)d * N + j] = 1.0;
-      reinterpret_cast<int*>(base + L.zeros64)[(size_t)d * N + j] = 64;
+      reinterpret_cast<int*>(base + L.wzero)[(size_t)d * N + j] = kZp;
     }
   }
 }
@@ -200,7 +229,7 @@ struct HeadRows {
   long long M;
 };
 
-// One warp per output row i: statistics, digits, planes, prefix rowsums.
+// One warp per output row i: statistics, digit codes, planes, prefix code sums.
 __global__ void __launch_bounds__(32 * kHeadSliceWarps)
     head_slice_rows(const HeadRows h, uint8_t* ws, HeadWsLayout L) {
   pdl_wait();
@@ -214,21 +243,23 @@ __global__ void __launch_bounds__(32 * kHeadSliceWarps)
   int* rsum = reinterpret_cast<int*>(ws + L.rsum);
   double* rst = reinterpret_cast<double*>(ws + L.rstat) + (size_t)i * 8;
   const int seg = (int)(i / h.seg_rows), r = (int)(i - (long long)seg * h.seg_rows);
-  if (r >= h.seg_valid) {   // padding row: zero digits
-    for (int k = lane; k < kHeadDigits * K; k += 32) prow[k] = 64;
+  if (r >= h.seg_valid) {   // padding row (never combined): the codes of 0
+    for (int k = lane; k < kHeadDigits * K; k += 32) prow[k] = k < K ? kZp : 0;
     if (lane == 0) {
-      for (int d = 0; d < kHeadDigits; ++d) rsum[(size_t)d * h.M + i] = 64 * (d + 1) * K;
+      for (int d = 0; d < kHeadDigits; ++d) rsum[(size_t)d * h.M + i] = kZp * K;
       for (int u = 0; u < 8; ++u) rst[u] = 0.0;
     }
     return;
   }
   const float* xr = h.x + ((h.x_row0 ? h.x_row0[seg] : (long long)seg * h.seg_rows) + r) * h.ldx;
   double amax = 0.0, l1 = 0.0, l2 = 0.0;
-  for (int k = lane; k < K; k += 32) {
-    const double a = fabs((double)xr[k]);
-    amax = fmax(amax, a);
-    l1 += a;
-    l2 += a * a;
+  for (int k = 4 * lane; k < K; k += 128) {
+    const float4 x4 = *reinterpret_cast<const float4*>(xr + k);
+    const double a0 = fabs((double)x4.x), a1 = fabs((double)x4.y);
+    const double a2 = fabs((double)x4.z), a3 = fabs((double)x4.w);
+    amax = fmax(amax, fmax(fmax(a0, a1), fmax(a2, a3)));
+    l1 += (a0 + a1) + (a2 + a3);
+    l2 += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
   }
   for (int o = 16; o > 0; o >>= 1) {
     amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -236,23 +267,23 @@ __global__ void __launch_bounds__(32 * kHeadSliceWarps)
     l2 += __shfl_xor_sync(0xffffffffu, l2, o);
   }
   const int e = head_exponent(amax);
-  int cs[kHeadDigits] = {0, 0, 0, 0, 0, 0, 0};
-  int sq[kHeadDigits] = {0, 0, 0, 0, 0, 0, 0};   // per-lane sum D^2 <= 36 * 4096: fits
+  int cs[kHeadDigits] = {0, 0, 0, 0, 0, 0};
+  int sq[kHeadDigits] = {0, 0, 0, 0, 0, 0};   // sum (U - 128)^2 <= 128^2 K < 2^31
   const double sc = pow2(-e);
   // 4 consecutive k per lane -> one 32-bit store per plane (K % 4 == 0)
   for (int k0 = 4 * lane; k0 < K; k0 += 128) {
-    uint32_t pk[kHeadDigits] = {0, 0, 0, 0, 0, 0, 0};
+    uint32_t pk[kHeadDigits] = {0, 0, 0, 0, 0, 0};
     const float4 x4 = *reinterpret_cast<const float4*>(xr + k0);
     const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      int D[kHeadDigits];
-      head_digits((double)xv[u] * sc, D);
+      int U[kHeadDigits];
+      head_digits((double)xv[u] * sc, U);
 #pragma unroll
       for (int s = 0; s < kHeadDigits; ++s) {
-        pk[s] |= (uint32_t)(D[s] + 64) << (8 * u);
-        cs[s] += D[s] + 64;
-        sq[s] += D[s] * D[s];
+        pk[s] |= (uint32_t)U[s] << (8 * u);
+        cs[s] += U[s];
+        sq[s] += (U[s] - kZp) * (U[s] - kZp);
       }
     }
 #pragma unroll
@@ -265,24 +296,26 @@ __global__ void __launch_bounds__(32 * kHeadSliceWarps)
       cs[s] += __shfl_xor_sync(0xffffffffu, cs[s], o);
       sq[s] += __shfl_xor_sync(0xffffffffu, sq[s], o);
     }
-  int rho = 0;   // max over digit planes s >= 1 of |D_s|_2^2 (<= 4096 K)
+  int rho = 0;   // max over digit planes s >= 1 of |B_s|_2^2
 #pragma unroll
   for (int s = 1; s < kHeadDigits; ++s) rho = max(rho, sq[s]);
   if (lane == 0) {
-    int pre = 0;
+    long long ps[kHeadDigits], pre = 0;
     for (int d = 0; d < kHeadDigits; ++d) {
+      ps[d] = cs[d];
       pre += cs[d];
-      rsum[(size_t)d * h.M + i] = pre;
+      rsum[(size_t)d * h.M + i] = (int)pre;   // A = planes 0..d for diagonal d
     }
     // certificate row factors (see head_combine)
     const double Kd = (double)K;
-    rst[0] = pow2(e - 12);
-    rst[1] = 6.04 * up(sqrt((double)rho)) * pow2(e - 61);
-    rst[2] = pow2(e - 49);
-    rst[3] = up(l1) + Kd * pow2(e - 49);
-    rst[4] = (double)kHeadDigits * pow2(e - 65);
+    rst[0] = pow2(e);
+    rst[1] = 5.03 * up(sqrt((double)rho)) * pow2(e - 62);
+    rst[2] = pow2(e - 47);
+    rst[3] = up(l1) + Kd * pow2(e - 47);
+    rst[4] = pow2(e - 64);
     rst[5] = (Kd - 1.0) * 0x1p-53 * up(sqrt(l2));
-    rst[6] = rst[7] = 0.0;
+    rst[6] = kC * ((double)rho_sum_2p47(ps, K) * 0x1p-47);   // R_i
+    rst[7] = pow2(e - 50);
   }
 }
 
@@ -291,7 +324,7 @@ struct HeadCombine {
   int N, K, seg_rows, seg_valid;
   const double* rstat;
   const double* cstat;
-  const int* acc;   // [kHeadDigits][M][N]
+  const int* acc;    // [M][kHeadDigits N] diagonal sums A_d (zero points removed)
   const float* bias;
   float* out;
   long long ldo;
@@ -300,13 +333,26 @@ struct HeadCombine {
   int* count;
 };
 
+// int32 -> f64 on the FP64 pipe: the word under exponent 2^52, biased by 2^31
+QC_DEV double i2d_magic(int v) {
+  return __hiloint2double(0x43300000, v ^ (int)0x80000000) - 4503601774854144.0;
+}
+
 // 4 consecutive columns per thread over kCombineRows rows.  With the per-row
 // (r*) and per-column (c*) factors prepared by the slicing kernels:
-//   S^ = s r0 c0 with s = sum_d acc_d 2^-7d             (r0 c0 = 2^(e+f-12), exact)
-//   T1 = r1 c1      dropped pairs: 6.04 |D|_2 |E|_2 2^(e+f-61)  (Cauchy-Schwarz)
-//   T2 = r2 c2 + r3 c3    truncation: 2^(e-49) |w|_1 + 2^(f-49) (|x|_1 + K 2^(e-49))
-//   T3 = r4 c0 (|acc_0| + 65 K)    combination: 7 2^(e+f-65) sum_d |acc_d| 2^-7d
+//   S^ = ((2^-14 s + R_i) + Q_j) r0 c0,  s = sum_d A_d 2^-8d,  r0 c0 = 2^(e+f)
+//   T1 = r1 c1      dropped pairs (s, t >= 1, s + t >= 6; 5 + 4 2^-8 + ... <= 5.03 of
+//                   weight 2^-62): 5.03 |B|_2 |C|_2 2^(e+f-62)   (Cauchy-Schwarz)
+//   T2 = r2 c2 + r3 c3    truncation: 2^(e-47) |w|_1 + 2^(f-47) (|x|_1 + K 2^(e-47))
+//   T3 = c0 (r4 (|A_0| + 130 K) + r7 (|R_i| + |Q_j|))    combination: six FMA
+//                   roundings of at most 2^-53 sum_d |A_d| 2^-8d (sum_{d>=1} <= 16384 K
+//                   (2 2^-8 + 3 2^-16 + ...) < 129 K), two more adds, and R, Q
+//                   (each within 2^-51 relative): <= 2^(e+f) (2^-64 (|A_0| + 130 K)
+//                   + 2^-50 (|R| + |Q|))
 //   T4 = r5 c4      the reference's rounding: (K-1) 2^-53 |x|_2 |w|_2
+// The nearest f32 rounding boundary of S^ is the midpoint T of its f32 bracket
+// (bits: low 29 cleared, bit 28 set) as long as E < 2^-26 |S^| (the next
+// boundary is >= 2^27 ulp64 away): accept when |S^ - T| > E (exact subtraction).
 constexpr int kCombineRows = 16;   // rows per thread (column factors stay in registers)
 
 __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
@@ -315,7 +361,7 @@ __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= c.N) return;
   // the thread's 4 columns: certificate factors once
-  double c0[4], c1[4], c2[4], c3[4], c4[4];
+  double c0[4], c1[4], c2[4], c3[4], c4[4], qj[4];
   float bj[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -325,10 +371,11 @@ __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
     c2[u] = cf[2];
     c3[u] = cf[3];
     c4[u] = cf[4];
+    qj[u] = cf[5];
     bj[u] = c.bias ? c.bias[j0 + u] : 0.0f;
   }
   const size_t ldacc = (size_t)kHeadDigits * c.N;
-  const double k65 = 65.0 * (double)c.K;
+  const double k130 = 130.0 * (double)c.K;
   const long long i_end = min((long long)(blockIdx.y + 1) * kCombineRows, c.M);
   for (long long i = (long long)blockIdx.y * kCombineRows; i < i_end; ++i) {
     const int seg = (int)(i / c.seg_rows), r = (int)(i - (long long)seg * c.seg_rows);
@@ -340,6 +387,7 @@ __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
       a4[d] = __ldcs(reinterpret_cast<const int4*>(c.acc + base + (size_t)d * c.N));
     const double* rf = c.rstat + i * 8;
     const double r0 = rf[0], r1 = rf[1], r2 = rf[2], r3 = rf[3], r4 = rf[4], r5 = rf[5];
+    const double ri = rf[6], r7 = rf[7];
     const long long orow = c.out_row0 ? c.out_row0[seg] + r : i;
     float res[4];
     bool all_ok = true;
@@ -349,25 +397,19 @@ __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
 #pragma unroll
       for (int d = kHeadDigits - 1; d >= 0; --d) {   // small terms first
         const int av = u == 0 ? a4[d].x : u == 1 ? a4[d].y : u == 2 ? a4[d].z : a4[d].w;
-        s = fma(i2d_alu(av), pow2(-7 * d), s);   // exact products, rounded sums (T3)
+        s = fma(i2d_magic(av), pow2(-8 * d), s);   // exact products, rounded sums (T3)
       }
       const int a0 = u == 0 ? a4[0].x : u == 1 ? a4[0].y : u == 2 ? a4[0].z : a4[0].w;
-      const double S = (s * r0) * c0[u];
-      const double E = (r1 * c1[u] + r2 * c2[u] + r3 * c3[u] +
-                        r4 * c0[u] * (fabs(i2d_alu(a0)) + k65) + r5 * c4[u]) * (1.0 + 0x1p-20);
+      const double S = ((fma(s, 0x1p-14, ri) + qj[u]) * r0) * c0[u];
+      const double E = (r1 * c1[u] + r2 * c2[u] + r3 * c3[u] + r5 * c4[u] +
+                        c0[u] * (r4 * (fabs(i2d_magic(a0)) + k130) +
+                                 r7 * (fabs(ri) + fabs(qj[u])))) * (1.0 + 0x1p-20);
       const double aS = fabs(S);
-      bool ok = aS < 0x1p126 && aS > 0x1p-125;
-      float y = 0.0f;
+      const long long sb = __double_as_longlong(S);
+      const double T = __longlong_as_double((sb & ~0x1FFFFFFFLL) | 0x10000000LL);
+      const bool ok = aS < 0x1p126 && aS > 0x1p-125 && E < aS * 0x1p-26 && fabs(S - T) > E;
       if (ok) {
-        y = __double2float_rn(S);
-        const uint32_t yb = __float_as_uint(y);
-        const float dn = __uint_as_float(y > 0.0f ? yb - 1u : yb + 1u);   // toward -inf
-        const float upn = __uint_as_float(y > 0.0f ? yb + 1u : yb - 1u);  // toward +inf
-        const double lo = 0.5 * ((double)y + (double)dn);
-        const double hi = 0.5 * ((double)y + (double)upn);
-        ok = (S - E > lo) && (S + E < hi);
-      }
-      if (ok) {
+        const float y = __double2float_rn(S);
         res[u] = c.bias ? __fadd_rn(y, bj[u]) : y;
       } else {
         all_ok = false;
@@ -486,11 +528,11 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
   const HeadWsLayout W = ws_layout(M, K, N);
   uint8_t* prep = reinterpret_cast<uint8_t*>(const_cast<void*>(g->prep));
   uint8_t* ws = reinterpret_cast<uint8_t*>(g->workspace);
-  // constants: a_scale = 1.0, a_zero = 64
+  // constants: a_scale = 1.0, a_zero = 128
   static const double kOne = 1.0;
-  static const int k64 = 64;
+  static const int kZpHost = kZp;
   cudaMemcpyAsync(ws + W.one, &kOne, 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(ws + W.one + 8, &k64, 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(ws + W.one + 8, &kZpHost, 4, cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(ws + W.count, 0, 4, st);
   HeadRows hr{g->x, g->ldx, g->x_row0, g->seg_rows, g->seg_valid, K, M};
   head_slice_rows<<<(unsigned)((M + kHeadSliceWarps - 1) / kHeadSliceWarps), 32 * kHeadSliceWarps,
@@ -512,7 +554,7 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
     q.w_codes = prep + P.bstack;
     q.ldw = (long long)a16((size_t)kHeadDigits * K);
     q.w_scale = reinterpret_cast<const double*>(prep + P.ones);
-    q.w_zero = reinterpret_cast<const int*>(prep + P.zeros64);
+    q.w_zero = reinterpret_cast<const int*>(prep + P.wzero);
     q.w_colsum = reinterpret_cast<const int*>(prep + P.csum);
     q.out = reinterpret_cast<float*>(ws + W.acc);
     q.ldo = (long long)kHeadDigits * N;
@@ -530,7 +572,7 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
         qd.a_rowsum = reinterpret_cast<const int*>(ws + W.rsum) + (size_t)d * M;
         qd.w_codes = prep + P.bstack + (size_t)d * N * ldb;
         qd.w_scale = reinterpret_cast<const double*>(prep + P.ones) + (size_t)d * N;
-        qd.w_zero = reinterpret_cast<const int*>(prep + P.zeros64) + (size_t)d * N;
+        qd.w_zero = reinterpret_cast<const int*>(prep + P.wzero) + (size_t)d * N;
         qd.w_colsum = reinterpret_cast<const int*>(prep + P.csum) + (size_t)d * N;
         qd.out = reinterpret_cast<float*>(ws + W.acc) + (size_t)d * N;
         rc = gemm_u8_launch(&qd, st);

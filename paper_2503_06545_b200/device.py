@@ -217,6 +217,7 @@ def gemm_u8(a: ActCodes, w: PackedWeight, M: Optional[int] = None, out=None,
     g.gate, g.gate_scalar = N.ptr(gate_vec), float(gate)
     g.epilogue, g.block_n, g.seg_active = epilogue, block_n, N.ptr(seg_active)
     g.out_rows = out.shape[0]
+    g.resid_rows = resid.shape[0] if resid is not None else 0
     N.check(N.lib().qcb_gemm_u8(C.byref(g), N.stream_ptr(stream)), "gemm_u8")
     count(1)
     return out
