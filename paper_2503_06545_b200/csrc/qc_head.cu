@@ -338,7 +338,7 @@ QC_DEV double i2d_magic(int v) {
   return __hiloint2double(0x43300000, v ^ (int)0x80000000) - 4503601774854144.0;
 }
 
-// 4 consecutive columns per thread over kCombineRows rows.  With the per-row
+// kCombineCols consecutive columns per thread over kCombineRows rows.  With the per-row
 // (r*) and per-column (c*) factors prepared by the slicing kernels:
 //   S^ = ((2^-14 s + R_i) + Q_j) r0 c0,  s = sum_d A_d 2^-8d,  r0 c0 = 2^(e+f)
 //   T1 = r1 c1      dropped pairs (s, t >= 1, s + t >= 6; 5 + 4 2^-8 + ... <= 5.03 of
@@ -354,17 +354,19 @@ QC_DEV double i2d_magic(int v) {
 // (bits: low 29 cleared, bit 28 set) as long as E < 2^-26 |S^| (the next
 // boundary is >= 2^27 ulp64 away): accept when |S^ - T| > E (exact subtraction).
 constexpr int kCombineRows = 16;   // rows per thread (column factors stay in registers)
+constexpr int kCombineCols = 2;    // consecutive columns per thread (int2 loads)
 
-__global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
+__global__ void __launch_bounds__(256) head_combine(const HeadCombine c) {
   pdl_wait();
   pdl_trigger();
-  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * kCombineCols;
   if (j0 >= c.N) return;
-  // the thread's 4 columns: certificate factors once
-  double c0[4], c1[4], c2[4], c3[4], c4[4], qj[4];
-  float bj[4];
+  // the thread's columns: certificate factors once
+  double c0[kCombineCols], c1[kCombineCols], c2[kCombineCols], c3[kCombineCols],
+      c4[kCombineCols], qj[kCombineCols];
+  float bj[kCombineCols];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kCombineCols; ++u) {
     const double* cf = c.cstat + (size_t)(j0 + u) * 8;
     c0[u] = cf[0];
     c1[u] = cf[1];
@@ -376,30 +378,39 @@ __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
   }
   const size_t ldacc = (size_t)kHeadDigits * c.N;
   const double k130 = 130.0 * (double)c.K;
-  const long long i_end = min((long long)(blockIdx.y + 1) * kCombineRows, c.M);
-  for (long long i = (long long)blockIdx.y * kCombineRows; i < i_end; ++i) {
-    const int seg = (int)(i / c.seg_rows), r = (int)(i - (long long)seg * c.seg_rows);
-    if (r >= c.seg_valid) continue;
+  const long long i0 = (long long)blockIdx.y * kCombineRows;
+  const long long i_end = min(i0 + kCombineRows, c.M);
+  // the next row's six diagonal sums are in flight while this row is combined
+  int2 nx[kHeadDigits];
+  auto load_row = [&](long long i, int2 (&dst)[kHeadDigits]) {
     const size_t base = (size_t)i * ldacc + j0;
-    int4 a4[kHeadDigits];
 #pragma unroll
     for (int d = 0; d < kHeadDigits; ++d)
-      a4[d] = __ldcs(reinterpret_cast<const int4*>(c.acc + base + (size_t)d * c.N));
+      dst[d] = __ldcs(reinterpret_cast<const int2*>(c.acc + base + (size_t)d * c.N));
+  };
+  if (i0 < i_end) load_row(i0, nx);
+  for (long long i = i0; i < i_end; ++i) {
+    int2 a2[kHeadDigits];
+#pragma unroll
+    for (int d = 0; d < kHeadDigits; ++d) a2[d] = nx[d];
+    if (i + 1 < i_end) load_row(i + 1, nx);
+    const int seg = (int)(i / c.seg_rows), r = (int)(i - (long long)seg * c.seg_rows);
+    if (r >= c.seg_valid) continue;
     const double* rf = c.rstat + i * 8;
     const double r0 = rf[0], r1 = rf[1], r2 = rf[2], r3 = rf[3], r4 = rf[4], r5 = rf[5];
     const double ri = rf[6], r7 = rf[7];
     const long long orow = c.out_row0 ? c.out_row0[seg] + r : i;
-    float res[4];
+    float res[kCombineCols];
     bool all_ok = true;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kCombineCols; ++u) {
       double s = 0.0;
 #pragma unroll
       for (int d = kHeadDigits - 1; d >= 0; --d) {   // small terms first
-        const int av = u == 0 ? a4[d].x : u == 1 ? a4[d].y : u == 2 ? a4[d].z : a4[d].w;
+        const int av = u == 0 ? a2[d].x : a2[d].y;
         s = fma(i2d_magic(av), pow2(-8 * d), s);   // exact products, rounded sums (T3)
       }
-      const int a0 = u == 0 ? a4[0].x : u == 1 ? a4[0].y : u == 2 ? a4[0].z : a4[0].w;
+      const int a0 = u == 0 ? a2[0].x : a2[0].y;
       const double S = ((fma(s, 0x1p-14, ri) + qj[u]) * r0) * c0[u];
       const double E = (r1 * c1[u] + r2 * c2[u] + r3 * c3[u] + r5 * c4[u] +
                         c0[u] * (r4 * (fabs(i2d_magic(a0)) + k130) +
@@ -419,11 +430,11 @@ __global__ void __launch_bounds__(128) head_combine(const HeadCombine c) {
       }
     }
     float* op = c.out + orow * c.ldo + j0;
-    if (all_ok && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
-      *reinterpret_cast<float4*>(op) = make_float4(res[0], res[1], res[2], res[3]);
+    if (all_ok && ((reinterpret_cast<uintptr_t>(op) & 7) == 0)) {
+      *reinterpret_cast<float2*>(op) = make_float2(res[0], res[1]);
     } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) op[u] = res[u];   // flagged ones are rewritten by the fallback
+      for (int u = 0; u < kCombineCols; ++u) op[u] = res[u];   // flagged: rewritten by the fallback
     }
   }
 }
@@ -443,72 +454,97 @@ struct HeadFallback {
   int* total;   // nullable running total of exact recomputations
 };
 
-// The reference's ascending-k f64 FMA chain for the listed elements.
-__global__ void __launch_bounds__(256) head_fallback(const HeadFallback h) {
+// The reference's ascending-k f64 FMA chain for the listed elements.  A warp
+// takes 32 listed elements (one chain per lane).  Their x / W^T row segments of
+// kFbChunk k are staged into shared memory by cp.async (one coalesced
+// 128-byte row segment per 8 lanes and instruction, double-buffered), and
+// each lane then runs its chain from its own staged rows (LDS.128,
+// bank-conflict free with the padded stride).  Per-lane streaming of private
+// rows instead costs one L1 wavefront per lane and instruction.
+constexpr int kFbWarps = 8;
+constexpr int kFbChunk = 32;                 // k per stage
+constexpr int kFbStride = kFbChunk + 4;      // floats per staged row
+
+struct FbSmem {
+  float buf[kFbWarps][2][2][32][kFbStride];  // [warp][stage][x | w][element][k]
+  const float* ptr[kFbWarps][2][32];         // [warp][x | w][element] row pointers
+};
+
+QC_DEV void cp_async16(void* dst, const void* src, bool full) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(full ? 16 : 0)
+               : "memory");
+}
+QC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+QC_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__global__ void __launch_bounds__(32 * kFbWarps) head_fallback(const HeadFallback h) {
+  extern __shared__ __align__(16) uint8_t fb_smem[];
+  FbSmem& sm = *reinterpret_cast<FbSmem*>(fb_smem);
   pdl_wait();
   pdl_trigger();
   const int n = *h.count;
   if (h.total && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(h.total, n);
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    const long long idx = h.list[t];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = h.K;
+  const int nchunks = (K + kFbChunk - 1) / kFbChunk;
+  for (int base = (blockIdx.x * kFbWarps + warp) * 32; base < n;
+       base += gridDim.x * kFbWarps * 32) {
+    const int t = base + lane;
+    const bool act = t < n;
+    const long long idx = h.list[act ? t : base];
     const long long i = idx / h.N;
     const int j = (int)(idx - i * h.N);
     const int seg = (int)(i / h.seg_rows), r = (int)(i - (long long)seg * h.seg_rows);
-    const float* xr = h.x + ((h.x_row0 ? h.x_row0[seg] : (long long)seg * h.seg_rows) + r) * h.ldx;
-    const float* wr = h.wt + (size_t)j * h.K;
+    __syncwarp();   // the previous group's staged rows are consumed
+    sm.ptr[warp][0][lane] =
+        h.x + ((h.x_row0 ? h.x_row0[seg] : (long long)seg * h.seg_rows) + r) * h.ldx;
+    sm.ptr[warp][1][lane] = h.wt + (size_t)j * K;
+    __syncwarp();
+    // stage chunk c: lane group g = lane / 8 copies row segments of elements
+    // g, g + 4, ...
+    auto stage = [&](int c) {
+      const int k0 = c * kFbChunk;
+      const int kk = 4 * (lane & 7);
+      const bool ok = k0 + kk < K;
+      for (int e = lane >> 3; e < 32; e += 4) {
+        const float* px = sm.ptr[warp][0][e];
+        const float* pw = sm.ptr[warp][1][e];
+        cp_async16(&sm.buf[warp][c & 1][0][e][kk], ok ? px + k0 + kk : px, ok);
+        cp_async16(&sm.buf[warp][c & 1][1][e][kk], ok ? pw + k0 + kk : pw, ok);
+      }
+      cp_async_commit();
+    };
+    stage(0);
     double s = 0.0;
-    // ascending k in batches of 16 through a register ring of kFbDepth batches:
-    // each batch's 16-byte loads are issued kFbDepth batches ahead of its FMAs
-    // (K % 4 == 0, rows 16-byte aligned)
-    constexpr int kFbDepth = 4;
-    float4 xq[kFbDepth][4], wq[kFbDepth][4];
+    for (int c = 0; c < nchunks; ++c) {
+      if (c + 1 < nchunks) stage(c + 1);
+      else cp_async_commit();   // an empty group keeps wait_group(1) uniform
+      cp_async_wait1();
+      __syncwarp();             // every lane's copies of chunk c have landed
+      const float* xs = sm.buf[warp][c & 1][0][lane];
+      const float* ws = sm.buf[warp][c & 1][1][lane];
+      const int kn = min(kFbChunk, K - c * kFbChunk);
+      if (kn == kFbChunk) {
 #pragma unroll
-    for (int b = 0; b < kFbDepth; ++b)
-      if (16 * b + 16 <= h.K) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          xq[b][u] = __ldg(reinterpret_cast<const float4*>(xr + 16 * b) + u);
-          wq[b][u] = __ldg(reinterpret_cast<const float4*>(wr + 16 * b) + u);
+        for (int kk = 0; kk < kFbChunk; kk += 4) {
+          const float4 a4 = *reinterpret_cast<const float4*>(xs + kk);
+          const float4 b4 = *reinterpret_cast<const float4*>(ws + kk);
+          s = fma((double)a4.x, (double)b4.x, s);
+          s = fma((double)a4.y, (double)b4.y, s);
+          s = fma((double)a4.z, (double)b4.z, s);
+          s = fma((double)a4.w, (double)b4.w, s);
         }
+      } else {
+        for (int kk = 0; kk < kn; ++kk) s = fma((double)xs[kk], (double)ws[kk], s);
       }
-    int k = 0;
-    for (; k + 16 * kFbDepth <= h.K; k += 16 * kFbDepth) {
-#pragma unroll
-      for (int b = 0; b < kFbDepth; ++b) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          s = fma((double)xq[b][u].x, (double)wq[b][u].x, s);
-          s = fma((double)xq[b][u].y, (double)wq[b][u].y, s);
-          s = fma((double)xq[b][u].z, (double)wq[b][u].z, s);
-          s = fma((double)xq[b][u].w, (double)wq[b][u].w, s);
-        }
-        const int kn = k + 16 * (b + kFbDepth);
-        if (kn + 16 <= h.K) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            xq[b][u] = __ldg(reinterpret_cast<const float4*>(xr + kn) + u);
-            wq[b][u] = __ldg(reinterpret_cast<const float4*>(wr + kn) + u);
-          }
-        }
-      }
+      __syncwarp();             // buffer c & 1 is refilled by stage(c + 2)
     }
-    // full batches left in the ring, then the scalar tail
-#pragma unroll
-    for (int b = 0; b < kFbDepth; ++b)
-      if (k + 16 <= h.K) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          s = fma((double)xq[b][u].x, (double)wq[b][u].x, s);
-          s = fma((double)xq[b][u].y, (double)wq[b][u].y, s);
-          s = fma((double)xq[b][u].z, (double)wq[b][u].z, s);
-          s = fma((double)xq[b][u].w, (double)wq[b][u].w, s);
-        }
-        k += 16;
-      }
-    for (; k < h.K; ++k) s = fma((double)xr[k], (double)wr[k], s);
-    const float y = __double2float_rn(s);
-    const long long orow = h.out_row0 ? h.out_row0[seg] + r : i;
-    h.out[orow * h.ldo + j] = h.bias ? __fadd_rn(y, h.bias[j]) : y;
+    if (act) {
+      const float y = __double2float_rn(s);
+      const long long orow = h.out_row0 ? h.out_row0[seg] + r : i;
+      h.out[orow * h.ldo + j] = h.bias ? __fadd_rn(y, h.bias[j]) : y;
+    }
   }
 }
 
@@ -585,15 +621,31 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
                 reinterpret_cast<const double*>(prep + P.cstat),
                 reinterpret_cast<const int*>(ws + W.acc), g->bias, g->out, g->ldo, g->out_row0,
                 reinterpret_cast<int*>(ws + W.list), reinterpret_cast<int*>(ws + W.count)};
-  head_combine<<<dim3((unsigned)((N / 4 + 127) / 128),
-                     (unsigned)((M + kCombineRows - 1) / kCombineRows)), 128, 0, st>>>(c);
+  // threads per block: a multiple of 32 dividing the column groups when one
+  // exists (no idle tail block), else 128
+  const int quads = N / kCombineCols;
+  int cb = 128;
+  for (int t = 256; t >= 64; t -= 32)
+    if (quads % t == 0) {
+      cb = t;
+      break;
+    }
+  head_combine<<<dim3((unsigned)((quads + cb - 1) / cb),
+                     (unsigned)((M + kCombineRows - 1) / kCombineRows)), cb, 0, st>>>(c);
   rc = launch_status();
   if (rc) return rc;
   HeadFallback fb{g->x, g->ldx, g->x_row0, g->seg_rows, N, K,
                   reinterpret_cast<const float*>(prep + P.wt), g->bias, g->out, g->ldo,
                   g->out_row0, reinterpret_cast<const int*>(ws + W.list),
                   reinterpret_cast<const int*>(ws + W.count), g->fallback_count};
-  head_fallback<<<num_sms() * 4, 256, 0, st>>>(fb);
+  static bool fb_attr = false;
+  if (!fb_attr) {
+    if (cudaFuncSetAttribute(head_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(FbSmem)) != cudaSuccess)
+      return QCB_ERR_CUDA;
+    fb_attr = true;
+  }
+  head_fallback<<<num_sms(), 32 * kFbWarps, sizeof(FbSmem), st>>>(fb);
   rc = launch_status();
   if (rc) return rc;
   return launch_status();
