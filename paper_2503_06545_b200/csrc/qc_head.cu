@@ -53,6 +53,7 @@ struct HeadPrepLayout {   // one-time weight side
   size_t wt;                // f32 [N][K] (W^T for the exact fallback)
   size_t ones;              // f64 [kHeadDigits N] = 1.0 (w_scale)
   size_t wzero;             // s32 [kHeadDigits N] = 128 (w_zero)
+  size_t one;               // f64 1.0 (a_scale), s32 128 (a_zero)
   size_t total;
 };
 
@@ -71,6 +72,8 @@ static HeadPrepLayout prep_layout(int K, int N) {
   off = a256(off + (size_t)8 * kHeadDigits * N);
   L.wzero = off;
   off = a256(off + (size_t)4 * kHeadDigits * N);
+  L.one = off;
+  off = a256(off + 16);
   L.total = off;
   return L;
 }
@@ -82,7 +85,6 @@ struct HeadWsLayout {     // per call
   size_t acc;     // s32 [M][kHeadDigits N] (diagonal d at columns d N ..)
   size_t list;    // s32 [M*N] flagged elements (i*N + j)
   size_t count;   // s32
-  size_t one;     // f64 1.0, s32 128
   size_t total;
 };
 
@@ -101,8 +103,6 @@ static HeadWsLayout ws_layout(long long M, int K, int N) {
   off = a256(off + (size_t)4 * M * N);
   L.count = off;
   off = a256(off + 4);
-  L.one = off;
-  off = a256(off + 16);
   L.total = off;
   return L;
 }
@@ -216,6 +216,10 @@ __global__ void head_prep_cols(const float* __restrict__ w, int K, int N, uint8_
     for (int d = 0; d < kHeadDigits; ++d) {
       reinterpret_cast<double*>(base + L.ones)[(size_t)d * N + j] = 1.0;
       reinterpret_cast<int*>(base + L.wzero)[(size_t)d * N + j] = kZp;
+    }
+    if (j == 0) {   // the activation side's scale / zero point (one segment)
+      *reinterpret_cast<double*>(base + L.one) = 1.0;
+      *reinterpret_cast<int*>(base + L.one + 8) = kZp;
     }
   }
 }
@@ -564,11 +568,6 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
   const HeadWsLayout W = ws_layout(M, K, N);
   uint8_t* prep = reinterpret_cast<uint8_t*>(const_cast<void*>(g->prep));
   uint8_t* ws = reinterpret_cast<uint8_t*>(g->workspace);
-  // constants: a_scale = 1.0, a_zero = 128
-  static const double kOne = 1.0;
-  static const int kZpHost = kZp;
-  cudaMemcpyAsync(ws + W.one, &kOne, 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(ws + W.one + 8, &kZpHost, 4, cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(ws + W.count, 0, 4, st);
   HeadRows hr{g->x, g->ldx, g->x_row0, g->seg_rows, g->seg_valid, K, M};
   head_slice_rows<<<(unsigned)((M + kHeadSliceWarps - 1) / kHeadSliceWarps), 32 * kHeadSliceWarps,
@@ -584,8 +583,8 @@ int head_gemm_launch(const QcbHeadGemm* g, cudaStream_t st) {
     q.seg_valid = (int)M;
     q.a_codes = ws + W.planes;
     q.lda = (long long)a16((size_t)kHeadDigits * K);
-    q.a_scale = reinterpret_cast<const double*>(ws + W.one);
-    q.a_zero = reinterpret_cast<const int*>(ws + W.one + 8);
+    q.a_scale = reinterpret_cast<const double*>(prep + P.one);
+    q.a_zero = reinterpret_cast<const int*>(prep + P.one + 8);
     q.a_rowsum = reinterpret_cast<const int*>(ws + W.rsum);
     q.w_codes = prep + P.bstack;
     q.ldw = (long long)a16((size_t)kHeadDigits * K);

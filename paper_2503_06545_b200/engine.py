@@ -243,6 +243,8 @@ class QuantCacheEngine:
         self.noise_dev = torch.zeros((nv, self.S, d), dtype=torch.float32, device=dev)
         self.noise_host = torch.zeros((nv, self.S, d), dtype=torch.float32).pin_memory()
         self.pol_size = C.sizeof(N.QcbPolicyVideo)
+        self._act_off = N.QcbPolicyVideo.action.offset // 4
+        self._abits_off = N.QcbPolicyVideo.abits.offset // 4
         self.pol = torch.zeros(nv * self.pol_size, dtype=torch.uint8, device=dev)
         self.pol_host = torch.zeros(nv * self.pol_size, dtype=torch.uint8).pin_memory()
         self.pol_trace = torch.zeros((self.T, nv * self.pol_size), dtype=torch.uint8, device=dev)
@@ -280,8 +282,9 @@ class QuantCacheEngine:
         self._idx_end = self._idx_base + half
         self._idx_cur = self._idx_base
 
-    def _upload_idx(self, arrays: Sequence[Sequence[int]]) -> List[torch.Tensor]:
-        """Pack small int64 row tables into a pinned region, one H2D copy."""
+    def _upload_idx(self, arrays: Sequence[Sequence[int]], stream=None) -> List[torch.Tensor]:
+        """Pack small int64 row tables into a pinned region, one H2D copy (on
+        `stream`, default the current one: the stream whose kernels read them)."""
         sizes = [len(a) for a in arrays]
         total = sum(sizes)
         lo = self._idx_cur
@@ -290,7 +293,12 @@ class QuantCacheEngine:
         if total:
             flat = np.concatenate([np.asarray(a, np.int64) for a in arrays])
             self.idx_host[lo:lo + total].numpy()[:] = flat
-            self.idx_dev[lo:lo + total].copy_(self.idx_host[lo:lo + total], non_blocking=True)
+            if stream is None:
+                self.idx_dev[lo:lo + total].copy_(self.idx_host[lo:lo + total], non_blocking=True)
+            else:
+                with torch.cuda.stream(stream):
+                    self.idx_dev[lo:lo + total].copy_(self.idx_host[lo:lo + total],
+                                                      non_blocking=True)
         self._idx_cur = lo + total
         out, off = [], lo
         for n in sizes:
@@ -499,13 +507,14 @@ class QuantCacheEngine:
                            L * nv, self.srap_v.view(L * nv, 3), seg_active=self.mask_v.view(L * nv),
                            stream=stream, workspace=workspace, dup_src=tabs[2])
 
-    def _early_plan(self, tn: int, vids, main):
-        """Launch step tn's plan_reuse + SRAP on the side stream (after everything
-        queued on `main` so far); returns (tn, completion event)."""
+    def _early_plan(self, tn: int, vids, ready):
+        """Launch step tn's plan_reuse + SRAP on the side stream once `ready` (an
+        event recorded on the main stream after the observe kernel) has fired;
+        returns (tn, completion event)."""
         do_srap = self.tog.srap and tn != 0   # seen >= 1 here: boundary iff tn == 0
-        tabs = self._upload_idx(self._srap_tables(vids)) if do_srap else []
-        ready = torch.cuda.Event()
-        ready.record(main)
+        # the tables travel on the side stream itself: main is already running
+        # the head, queued after `ready`
+        tabs = self._upload_idx(self._srap_tables(vids), stream=self.side) if do_srap else []
         self.side.wait_event(ready)
         self._plan_reuse_srap(tn, len(vids), do_srap, tabs, self.side, self._srap_ws)
         done = torch.cuda.Event()
@@ -577,17 +586,16 @@ class QuantCacheEngine:
                 self._plan_step(t, vids)
             self.pol_host.copy_(self.pol, non_blocking=True)
             st.synchronize()
-            raw = self.pol_host.numpy()
+            # the decisions straight from the pinned copy (QcbPolicyVideo.action /
+            # .abits as int32 words; ctypes parsing costs ~10 us per video)
             npl = 1 if self.sync else nv
-            plans = [N.QcbPolicyVideo.from_buffer_copy(
-                raw[v * self.pol_size:(v + 1) * self.pol_size].tobytes()) for v in range(npl)]
-            if self.sync:
-                plans = plans * nv    # every video (and every rank) takes one path
+            r32 = self.pol_host.numpy()[:npl * self.pol_size].view(np.int32).reshape(npl, -1)
+            act_tab = r32[:, self._act_off:self._act_off + L].tolist()
+            abits_of = r32[:, self._abits_off].tolist()
+            if self.sync:   # every video (and every rank) takes one path
+                act_tab, abits_of = act_tab * nv, abits_of * nv
             for vs in vids:
                 vs.seen += 1
-            # plain Python copies of the decisions (ctypes field access is slow)
-            act_tab = [list(p.action) for p in plans]
-            abits_of = [int(p.abits) for p in plans]
             self._run_step(t, vids, act_tab, abits_of, collect_features, gen)
         out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
         if return_device:
@@ -692,9 +700,23 @@ class QuantCacheEngine:
         if self.host_profile is not None:
             t_sync = time.perf_counter()
         # ---------------- execute blocks ----------------
-        cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
+        fast = collect_features is None and not any(
+            a == N.ACT_RECOMPUTE for row in act_tab for a in row)
+        if fast:
+            # nothing recomputes: the head reads each video's last reused cache
+            # entry (or x_t); the prev bookkeeping runs after the head launch
+            cur = []
+            for v, vs in enumerate(vids):
+                c = vs.x
+                for l, a in enumerate(act_tab[v]):
+                    if a == N.ACT_REUSE:
+                        c = vs.cache[l]
+                cur.append(vs.pool.inc(c))
+            x_in = [vs.x for vs in vids]
+        else:
+            cur = [vs.pool.inc(vs.x) for vs in vids]     # block input slot per video
         feats = [] if collect_features is not None else None
-        for l in range(L):
+        for l in range(0 if fast else L):
             acts = [act_tab[v][l] for v in range(nv)]
             outs = list(cur)
             rec = []
@@ -751,21 +773,20 @@ class QuantCacheEngine:
         if self.host_profile is not None:
             now = time.perf_counter() - t_sync
             self.host_profile.append((now, first_launch if first_launch is not None else now))
+        ready = None
         if not self.sync:
             # observe_block for every layer of the step (schedule.py:330-351)
             N.check(lib.qcb_policy_observe_all(pol, nv, L, t, self.thc, N.ptr(self.hlc_v), sp),
                     "observe_all")
             Dv.count(1)
+            self.pol_trace[t].copy_(self.pol, non_blocking=True)
+            if t > 0:
+                ready = torch.cuda.Event()
+                ready.record(st)
         if collect_features is not None:
             x_now = torch.stack([self.slot_view(vs.x) for vs in vids]).cpu().numpy()
             collect_features.append((t, x_now, feats))
         # ---------------- head + sampler update ----------------
-        if not self.sync:
-            self.pol_trace[t].copy_(self.pol, non_blocking=True)
-            if t > 0:
-                # the next step's reuse plan depends only on the cache state just
-                # observed (schedule.py:286-309): overlap it with the head
-                self._early = self._early_plan(t - 1, vids, st)
         tabh = self._upload_idx([[self.rows(c) for c in cur]])
         with self._ph("head"):
             if self.head_prep is not None:
@@ -806,6 +827,21 @@ class QuantCacheEngine:
                 if len(vs.hist) > self.th.history_k:
                     vs.pool.dec(vs.hist.pop(0))
                 vs.x = new
+        if fast:
+            # prev references of the step (schedule.py:349-351): a reused layer's
+            # output is its cache entry, a pruned layer passes its input through
+            for v, vs in enumerate(vids):
+                c = x_in[v]
+                for l, a in enumerate(act_tab[v]):
+                    if a == N.ACT_REUSE:
+                        c = vs.cache[l]
+                    vs.pool.dec(vs.prev[l])
+                    vs.prev[l] = vs.pool.inc(c)
+        if ready is not None:
+            # the next step's reuse plan depends only on the cache state just
+            # observed (schedule.py:286-309): it runs on the side stream while
+            # the head (launched above) runs
+            self._early = self._early_plan(t - 1, vids, ready)
         if self.sync:
             self._sync_decide(t, vids)
 
