@@ -1281,6 +1281,143 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2(const ActQuantParams p, 
   }
 }
 
+// Pass 2, common case (codes only, K % 4 == 0, n_out * nseg <= kP2Pairs): the
+// (output, segment) -> (s, z) table is built once per block in shared memory
+// while the warp's first row segment is already in flight, and each warp then
+// streams its rows as a sequence of (row, output, batch) items with the next
+// item's loads issued before the current one is coded.  A persistent grid
+// (resident blocks only) lets every warp serve several rows.
+constexpr int kP2Pairs = 128;
+constexpr int kP2HBatch = 4;   // float4 per lane per item
+
+__global__ void __launch_bounds__(kV2Threads) aq2_pass2_hot(const ActQuantParams p, const AQ2 a) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float t_inv[kP2Pairs], t_z[kP2Pairs];
+  __shared__ double t_s[kP2Pairs];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.K, n_out = p.n_out;
+  const float topf = (float)((1 << p.bits) - 1);
+  const int nb = (K + 128 * kP2HBatch - 1) / (128 * kP2HBatch);   // items per (row, output)
+  const int per_row = nb * n_out;
+  const long long W = (long long)gridDim.x * (kV2Threads / 32);
+  const long long w = (long long)blockIdx.x * (kV2Threads / 32) + warp;
+  // item u of this warp -> stash pointer of its first float4 (nullptr: no item)
+  auto item_src = [&](long long u, const float*& src, int& jbase, long long& orow, int& o,
+                      int& b, int& seg) -> bool {
+    const long long k = u / per_row;
+    const int rem = (int)(u - k * per_row);
+    o = rem / nb;
+    b = rem - o * nb;
+    const long long gr = w + k * W;
+    if (gr >= a.total_rows) return false;
+    seg = (int)(gr / p.seg_valid);
+    const int mrow = (int)(gr - (long long)seg * p.seg_valid);
+    orow = (long long)seg * p.seg_rows + mrow;
+    jbase = lane * 4 + b * 128 * kP2HBatch;
+    src = a.stash[o] + orow * a.ld_stash;
+    return true;
+  };
+  auto load_item = [&](const float* src, int jbase, float4 (&v)[kP2HBatch]) {
+#pragma unroll
+    for (int i = 0; i < kP2HBatch; ++i) {
+      const int j = jbase + 128 * i;
+      if (j < K) v[i] = __ldcs(reinterpret_cast<const float4*>(src + j));
+    }
+  };
+  float4 cur[kP2HBatch], nxt[kP2HBatch];
+  const float* src;
+  int jb, o, b, seg;
+  long long orow;
+  bool have = item_src(0, src, jb, orow, o, b, seg);
+  if (have) load_item(src, jb, cur);
+  // (s, z) per (output, segment): quantize's minmax parameters (quant.py:83-123)
+  const double top = (double)((1 << p.bits) - 1);
+  for (int t = threadIdx.x; t < n_out * p.nseg; t += blockDim.x) {
+    const int to = t / p.nseg, ts = t - to * p.nseg;
+    const uint32_t* kk = p.keys + ((size_t)to * p.nseg + ts) * 2;
+    const double lo = (double)key2f(kk[0]), hi = (double)key2f(kk[1]);
+    const double span = hi - lo;
+    double sc, z;
+    if (span <= 0.0) {
+      sc = 1.0;
+      z = 0.0;
+    } else {
+      sc = scale_up16(__ddiv_rn(span, top));
+      z = fmin(fmax(rha(__ddiv_rn(-lo, sc)), 0.0), top);
+    }
+    t_inv[t] = (float)(1.0 / sc);
+    t_z[t] = (float)z;
+    t_s[t] = sc;
+    if (blockIdx.x == 0) {
+      p.scale[to][ts] = sc;
+      p.zero[to][ts] = (int)z;
+    }
+  }
+  __syncthreads();
+  const float2 mg = make_float2(12582912.0f, 12582912.0f);
+  const float2 nmg = make_float2(-12582912.0f, -12582912.0f);
+  const float2 m1 = make_float2(-1.0f, -1.0f);
+  const float2 b23 = make_float2(8388608.0f, 8388608.0f);
+  int rs = 0;
+  for (long long u = 0; have; ++u) {
+    const float* nsrc;
+    int njb, no, nbb, nseg_;
+    long long norow;
+    const bool nhave = item_src(u + 1, nsrc, njb, norow, no, nbb, nseg_);
+    if (nhave) load_item(nsrc, njb, nxt);
+    const int t = o * p.nseg + seg;
+    const float inv_sf = t_inv[t], zf = t_z[t];
+    const float2 inv2 = make_float2(inv_sf, inv_sf), z2 = make_float2(zf, zf);
+    uint8_t* cr = p.codes[o] + orow * p.ldc;
+    if (b == 0) rs = 0;
+#pragma unroll
+    for (int i = 0; i < kP2HBatch; ++i) {
+      const int j = jb + 128 * i;
+      if (j >= K) break;
+      // packed f32x2 estimate of clip(rha(xe/s) + z), one near-tie test per float4
+      float dmax = 0.0f;
+      auto codes2 = [&](float2 x) -> uint32_t {
+        const float2 q = __fmul2_rn(x, inv2);
+        const float2 n = __fadd2_rn(__fadd2_rn(q, mg), nmg);   // rint(q), |q| < 2^22
+        const float2 d = __ffma2_rn(n, m1, q);                  // q - n, exact
+        dmax = fmaxf(dmax, fmaxf(fabsf(d.x), fabsf(d.y)));
+        float2 v = __fadd2_rn(n, z2);
+        v.x = fminf(fmaxf(v.x, 0.0f), topf);
+        v.y = fminf(fmaxf(v.y, 0.0f), topf);
+        const float2 kq = __fadd2_rn(v, b23);                   // code in the low byte
+        return __byte_perm(__float_as_uint(kq.x), __float_as_uint(kq.y), 0x0040);
+      };
+      const uint32_t lo2 = codes2(make_float2(cur[i].x, cur[i].y));
+      const uint32_t hi2 = codes2(make_float2(cur[i].z, cur[i].w));
+      uint32_t packed = __byte_perm(lo2, hi2, 0x5410);
+      if (dmax > 0.5f - 0x1p-12f) {   // near a .5 tie: the reference's f64 sequence
+        const float e4[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
+        const double sc = t_s[t];
+        packed = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          packed |= (uint32_t)code_of(e4[e], inv_sf, sc, zf, topf) << (8 * e);
+      }
+      rs = __dp4a(packed, 0x01010101u, (unsigned)rs);
+      *reinterpret_cast<uint32_t*>(cr + j) = packed;
+    }
+    if (b == nb - 1) {
+      const int tot = warp_sum(rs);
+      if (lane == 0) p.rowsum[o][orow] = tot;
+    }
+#pragma unroll
+    for (int i = 0; i < kP2HBatch; ++i) cur[i] = nxt[i];
+    have = nhave;
+    src = nsrc;
+    jb = njb;
+    orow = norow;
+    o = no;
+    b = nbb;
+    seg = nseg_;
+  }
+}
+
 // reciprocal table 1/c; with `signs`, the rotation signs of the first b
 // columns are folded in (s_j / c_j), which is what the v4 kernel consumes
 __global__ void recip_k(const double* c, const float* signs, int b, double* rc, int K) {
@@ -1291,6 +1428,28 @@ __global__ void recip_k(const double* c, const float* signs, int b, double* rc, 
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// pass 2 launch: the streaming kernel for codes-only calls, else the general one
+static void launch_pass2(const qc::ActQuantParams& p, const qc::AQ2& a, cudaStream_t st) {
+  bool hot = (p.K & 3) == 0 && (p.ldc & 3) == 0 && p.n_out * p.nseg <= qc::kP2Pairs &&
+             a.ld_stash % 4 == 0;
+  for (int o = 0; o < p.n_out; ++o)
+    if (!p.codes[o] || p.deq_out[o] || (reinterpret_cast<uintptr_t>(p.codes[o]) & 3)) hot = false;
+  if (hot) {
+    static int resident = 0;
+    if (!resident) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, qc::aq2_pass2_hot, qc::kV2Threads, 0);
+      if (resident < 1) resident = 1;
+    }
+    int b2 = (a.total_rows + 3) / 4;
+    if (b2 > num_sms() * resident) b2 = num_sms() * resident;
+    launch_pdl(qc::aq2_pass2_hot, dim3(b2), dim3(qc::kV2Threads), 0, st, p, a);
+  } else {
+    int b2 = (a.total_rows + 3) / 4;
+    if (b2 > num_sms() * 16) b2 = num_sms() * 16;
+    launch_pdl(qc::aq2_pass2, dim3(b2), dim3(qc::kV2Threads), 0, st, p, a);
+  }
+}
 
 }  // namespace qc
 
@@ -1415,9 +1574,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
         aq3_pass1<4096, true><<<b1, kV3Threads, sizeof(V3Smem<4096>), st>>>(p, a);
         break;
     }
-    int b2 = (a.total_rows + 3) / 4;
-    if (b2 > num_sms() * 16) b2 = num_sms() * 16;
-    launch_pdl(aq2_pass2, dim3(b2), dim3(kV2Threads), 0, st, p, a);
+    launch_pass2(p, a, st);
     if (q->xe_out[0] && q->ldxe != q->K) return QCB_ERR_DIM;  // debug copy layout unsupported
     return launch_status();
   }

@@ -19,7 +19,7 @@ ap.add_argument("--shapes", default="1152x1152,1152x4608,4608x1152")
 ap.add_argument("--epi", default="store")
 ap.add_argument("--bn", type=int, default=0)
 args = ap.parse_args()
-epi = {"store": N.EPI_STORE, "gelu": N.EPI_GELU, "gate": N.EPI_GATE_RESID}[args.epi]
+epi = {"store": N.EPI_STORE, "gelu": N.EPI_GELU, "gate": N.EPI_GATE_RESID, "acc": N.EPI_ACC}[args.epi]
 torch.manual_seed(0)
 for shp in args.shapes.split(","):
     K, Nn = map(int, shp.split("x"))
