@@ -259,6 +259,13 @@ int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nseg,
 int qcb_reduce_l1(QcbFeat x, QcbFeat h, int rows, int cols, int nseg, double* res,
                   void* workspace, void* stream);
 
+/* cumulative_variation terms for all history entries in one pass
+ * (schedule.py:128-133): res[j*nseg + seg] = sum|x - hist[j]| per segment, x read
+ * once; 1 <= nh <= 8, every operand's segment rows contiguous (ld == cols),
+ * cols % 4 == 0.  Replaces nh qcb_reduce_l1 calls. */
+int qcb_reduce_l1_hist(QcbFeat x, const QcbFeat* hist, int nh, int rows, int cols, int nseg,
+                       double* res, void* workspace, void* stream);
+
 size_t qcb_reduce_workspace_bytes(int nseg);
 
 /* ---------------------------------------------------------------- policy */

@@ -184,7 +184,7 @@ using namespace qc;
 constexpr int kMaxSegs = 4096;
 
 extern "C" size_t qcb_reduce_workspace_bytes(int nseg) {
-  return (size_t)kMaxSegs * sizeof(int) + (size_t)nseg * kMaxChunks * 3 * sizeof(double) +
+  return (size_t)kMaxSegs * sizeof(int) + (size_t)nseg * kMaxChunks * 8 * sizeof(double) +
          (size_t)nseg * sizeof(int) + 256;
 }
 
@@ -210,6 +210,99 @@ __global__ void srap_copy_k(const int* seg_active, const long long* dup, int nse
   const int d = (int)dup[s];
   if (d != s && (!seg_active || seg_active[s]))
     for (int i = 0; i < 3; ++i) res[(size_t)s * 3 + i] = res[(size_t)d * 3 + i];
+}
+}  // namespace qc
+
+namespace qc {
+// cumulative_variation terms for every history entry in one pass
+// (schedule.py:128-133): res[j][seg] = sum|x - h_j| over the segment, x read
+// once.  Each segment's rows must be contiguous (ld == cols), so a CTA streams a
+// flat float4 range with kL1Unroll loads per operand in flight per thread.
+// Same deterministic two-stage fixed-order sum as seg_reduce.
+constexpr int kL1MaxHist = 8;
+constexpr int kL1Unroll = 2;
+
+struct FeatHist {
+  FeatP h[kL1MaxHist];
+};
+
+template <int NH>
+__global__ void __launch_bounds__(kRThreads)
+    l1_hist_k(FeatP fx, FeatHist fh, int rows, int cols, double* partials, int* tickets,
+              double* res, int chunks, int nseg) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double scratch[NH * 8];
+  __shared__ bool last;
+  const int seg = blockIdx.y, chunk = blockIdx.x;
+  const long long n4 = (long long)rows * cols / 4;
+  const long long e0 = n4 * chunk / chunks, e1 = n4 * (chunk + 1) / chunks;
+  const float4* x = reinterpret_cast<const float4*>(feat_row(fx, seg, rows, 0));
+  const float4* h[NH];
+#pragma unroll
+  for (int j = 0; j < NH; ++j) h[j] = reinterpret_cast<const float4*>(feat_row(fh.h[j], seg, rows, 0));
+  double acc[NH];
+#pragma unroll
+  for (int j = 0; j < NH; ++j) acc[j] = 0.0;
+  auto add = [&](const float4 a, const float4 b, double& s) {
+    const double ax = a.x, ay = a.y, az = a.z, aw = a.w;
+    s += (fabs(ax - (double)b.x) + fabs(ay - (double)b.y)) +
+         (fabs(az - (double)b.z) + fabs(aw - (double)b.w));
+  };
+  long long i = e0 + threadIdx.x;
+  for (; i + (long long)(kL1Unroll - 1) * kRThreads < e1; i += (long long)kL1Unroll * kRThreads) {
+    float4 xv[kL1Unroll], hv[NH][kL1Unroll];
+#pragma unroll
+    for (int u = 0; u < kL1Unroll; ++u) xv[u] = __ldg(x + i + u * kRThreads);
+#pragma unroll
+    for (int j = 0; j < NH; ++j)
+#pragma unroll
+      for (int u = 0; u < kL1Unroll; ++u) hv[j][u] = __ldcs(h[j] + i + u * kRThreads);
+#pragma unroll
+    for (int j = 0; j < NH; ++j)
+#pragma unroll
+      for (int u = 0; u < kL1Unroll; ++u) add(xv[u], hv[j][u], acc[j]);
+  }
+  for (; i < e1; i += kRThreads) {
+    const float4 xv = __ldg(x + i);
+#pragma unroll
+    for (int j = 0; j < NH; ++j) add(xv, __ldcs(h[j] + i), acc[j]);
+  }
+  block_sum_vec<NH>(acc, scratch);
+  if (threadIdx.x == 0) {
+    double* pp = partials + ((size_t)seg * kMaxChunks + chunk) * kL1MaxHist;
+#pragma unroll
+    for (int j = 0; j < NH; ++j) pp[j] = acc[j];
+    __threadfence();
+    last = (atomicAdd(&tickets[seg], 1) == chunks - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double tot[NH];
+#pragma unroll
+    for (int j = 0; j < NH; ++j) tot[j] = 0.0;
+    for (int ch = threadIdx.x; ch < chunks; ch += kRThreads) {
+      const double* pp = partials + ((size_t)seg * kMaxChunks + ch) * kL1MaxHist;
+#pragma unroll
+      for (int j = 0; j < NH; ++j) tot[j] += __ldcg(pp + j);
+    }
+    __syncthreads();
+    block_sum_vec<NH>(tot, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int j = 0; j < NH; ++j) res[(size_t)j * nseg + seg] = tot[j];
+      tickets[seg] = 0;
+    }
+  }
+}
+
+template <int NH>
+static void launch_l1_hist(const FeatP& fx, const FeatHist& fh, int rows, int cols, int nseg,
+                           double* partials, int* tickets, double* res, int ch,
+                           cudaStream_t st) {
+  launch_pdl(l1_hist_k<NH>, dim3(ch, nseg), dim3(kRThreads), 0, st, fx, fh, rows, cols,
+             partials, tickets, res, ch, nseg);
 }
 }  // namespace qc
 
@@ -239,7 +332,7 @@ extern "C" int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nse
   if (nseg <= 0 || nseg > kMaxSegs) return QCB_ERR_DIM;
   cudaStream_t st = (cudaStream_t)stream;
   int* need = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + kMaxSegs * sizeof(int) +
-                                     (size_t)nseg * kMaxChunks * 3 * sizeof(double));
+                                     (size_t)nseg * kMaxChunks * 8 * sizeof(double));
   launch_pdl(srap_need_k, dim3(1), dim3(1024), 0, st, seg_active, dup_src, nseg, need);
   int rc = launch_reduce<1, 3>(a, b, a, rows, cols, nseg, need, res, ws, stream);
   if (rc) return rc;
@@ -251,6 +344,40 @@ extern "C" int qcb_reduce_srap(QcbFeat a, QcbFeat b, int rows, int cols, int nse
 extern "C" int qcb_reduce_l1(QcbFeat x, QcbFeat h, int rows, int cols, int nseg, double* res,
                              void* ws, void* stream) {
   return launch_reduce<2, 1>(x, h, x, rows, cols, nseg, nullptr, res, ws, stream);
+}
+
+extern "C" int qcb_reduce_l1_hist(QcbFeat x, const QcbFeat* hist, int nh, int rows, int cols,
+                                  int nseg, double* res, void* ws, void* stream) {
+  if (nh <= 0 || nh > kL1MaxHist || !hist || !res || !ws) return nh == 0 ? QCB_OK : QCB_ERR_VALUE;
+  if (rows <= 0 || cols <= 0 || nseg <= 0 || nseg > kMaxSegs || cols % 4) return QCB_ERR_DIM;
+  if (x.ld != cols) return QCB_ERR_DIM;
+  FeatHist fh{};
+  for (int j = 0; j < nh; ++j) {
+    if (hist[j].ld != cols) return QCB_ERR_DIM;
+    fh.h[j] = fp(hist[j]);
+  }
+  int* tickets = reinterpret_cast<int*>(ws);
+  double* partials = reinterpret_cast<double*>(tickets + kMaxSegs);
+  // ~2K float4 (8 per thread) per CTA, at most ~8 CTAs per SM in flight
+  long long n4 = (long long)rows * cols / 4;
+  int ch = (int)((n4 + 2047) / 2048);
+  const int cap = (8 * num_sms() + nseg - 1) / nseg;
+  if (ch > cap) ch = cap;
+  if (ch > kMaxChunks) ch = kMaxChunks;
+  if (ch < 1) ch = 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  const FeatP fx = fp(x);
+  switch (nh) {
+    case 1: launch_l1_hist<1>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+    case 2: launch_l1_hist<2>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+    case 3: launch_l1_hist<3>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+    case 4: launch_l1_hist<4>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+    case 5: launch_l1_hist<5>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+    case 6: launch_l1_hist<6>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+    case 7: launch_l1_hist<7>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+    default: launch_l1_hist<8>(fx, fh, rows, cols, nseg, partials, tickets, res, ch, st); break;
+  }
+  return launch_status();
 }
 
 // ------------------------------------------------------------------ policy

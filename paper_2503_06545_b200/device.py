@@ -385,6 +385,16 @@ def reduce_l1(x: N.QcbFeat, h: N.QcbFeat, rows: int, cols: int, nseg: int,
     return res
 
 
+def reduce_l1_hist(x: N.QcbFeat, hist: Sequence[N.QcbFeat], rows: int, cols: int, nseg: int,
+                   res: torch.Tensor, stream=None):
+    """res[j][seg] = sum|x - hist[j]| for every history entry, x read once."""
+    arr = (N.QcbFeat * len(hist))(*hist)
+    N.check(N.lib().qcb_reduce_l1_hist(x, arr, len(hist), rows, cols, nseg, N.ptr(res),
+                                       _rws(nseg), N.stream_ptr(stream)), "reduce_l1_hist")
+    count(1)
+    return res
+
+
 def thresholds_struct(th, toggles) -> N.QcbThresholds:
     return N.QcbThresholds(
         float(th.delta1), float(th.delta2), int(th.tau_max), int(th.tau_mid), int(th.tau_min),

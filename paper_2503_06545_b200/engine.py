@@ -608,10 +608,7 @@ class QuantCacheEngine:
         nv, L, S, d = len(vids), self.L, self.S, self.d
         st, lib, sp, pol = self.stream, N.lib(), N.stream_ptr(), self.pol.data_ptr()
         nh = len(vids[0].hist)
-        pre = []
-        for j in range(nh):
-            pre.append([self.rows(vs.x) for vs in vids])
-            pre.append([self.rows(vs.hist[j]) for vs in vids])
+        pre = self._l1_tables(vids)
         early = self._early if (self._early is not None and self._early[0] == t) else None
         self._early = None
         if early is None:
@@ -620,17 +617,32 @@ class QuantCacheEngine:
                 pre += self._srap_tables(vids)
         tabs = self._upload_idx(pre)
         with self._ph("plan"):
-            for j in range(nh):
-                Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]),
-                             Dv.feat(self.arena, tabs[2 * j + 1]), S, d, nv, self.l1_v[j])
+            self._reduce_l1(tabs, nh, nv)
             if early is None:
-                self._plan_reuse_srap(t, nv, do_srap, tabs[2 * nh:], st)
-            else:
+                self._plan_reuse_srap(t, nv, do_srap, tabs[-3:] if do_srap else [], st)
+        with self._ph("plan_srap_wait"):
+            if early is not None:
                 st.wait_event(early[1])   # plan_reuse / SRAP of this step ran on the side stream
             N.check(lib.qcb_policy_plan_finish(pol, nv, L, t, self.thc, N.ptr(self.srap_v),
                                                N.ptr(self.l1_v), nh,
                                                N.ptr(self.draws[t]), 0, sp), "plan_finish")
             Dv.count(1)
+
+    def _l1_tables(self, vids) -> List[List[int]]:
+        """Row tables of x_t and its history entries (cumulative_variation)."""
+        nh = len(vids[0].hist)
+        if nh == 0:
+            return []
+        return [[self.rows(vs.x) for vs in vids]] + \
+            [[self.rows(vs.hist[j]) for vs in vids] for j in range(nh)]
+
+    def _reduce_l1(self, tabs, nh: int, nv: int):
+        """V terms sum|x - h_j| of every history entry in one pass over x
+        (schedule.py:128-133) into l1_v[j][video]."""
+        if nh:
+            Dv.reduce_l1_hist(Dv.feat(self.arena, tabs[0]),
+                              [Dv.feat(self.arena, tabs[1 + j]) for j in range(nh)],
+                              self.S, self.d, nv, self.l1_v)
 
     # ------------------------------------------------------------------ synchronised mode
     def _sync_plan(self, tn: int, nh: int):
@@ -660,25 +672,20 @@ class QuantCacheEngine:
         nh = len(vids[0].hist)             # history after finalize_step(t)
         do_plan = t > 0
         do_srap = self.tog.srap and t - 1 > 0   # plan(t-1) is a boundary iff t-1 == 0
-        pre = []
-        if do_plan:
-            for j in range(nh):
-                pre.append([self.rows(vs.x) for vs in vids])
-                pre.append([self.rows(vs.hist[j]) for vs in vids])
+        pre = self._l1_tables(vids) if do_plan else []
+        n_l1 = len(pre)
         if do_srap:
             pre += self._srap_tables(vids)
         tabs = self._upload_idx(pre)
         with self._ph("plan"):
             if do_plan:
-                for j in range(nh):
-                    Dv.reduce_l1(Dv.feat(self.arena, tabs[2 * j]),
-                                 Dv.feat(self.arena, tabs[2 * j + 1]), S, d, nv, self.l1_v[j])
+                self._reduce_l1(tabs, nh, nv)
             if do_srap:
-                Dv.reduce_srap(Dv.feat(self.arena, tabs[2 * nh]),
-                               Dv.feat(self.arena, tabs[2 * nh + 1]), S, d, L * nv,
+                Dv.reduce_srap(Dv.feat(self.arena, tabs[n_l1]),
+                               Dv.feat(self.arena, tabs[n_l1 + 1]), S, d, L * nv,
                                self.srap_v.view(L * nv, 3),
                                seg_active=self.sync_mask_v.view(L * nv),
-                               workspace=self._srap_ws, dup_src=tabs[2 * nh + 2])
+                               workspace=self._srap_ws, dup_src=tabs[n_l1 + 2])
             # pack the local sums (fixed video order: deterministic), then ranks
             qdist.pack_decision_sums(self.stats, self.hlc_v, self.srap_v, self.l1_v)
             qdist.allreduce_sum(self.stats, group=self.sync_group)

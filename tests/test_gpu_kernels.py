@@ -463,6 +463,36 @@ class TestReductions:
             sl = slice(v * S, (v + 1) * S)
             assert r[v] == pytest.approx(O.variation([b[sl]], a[sl]), rel=1e-12)
 
+    @pytest.mark.parametrize("nh", [1, 4, 5])
+    def test_l1_hist_fused(self, D, nh):
+        """cumulative_variation terms of every history entry in one pass
+        (schedule.py:128-133) == the per-entry reduction, incl. row tables that
+        place each video's slot anywhere in an arena and an odd row count."""
+        rng = np.random.default_rng(20 + nh)
+        S, d, nseg, slots = 1003, 1152, 2, 12
+        arena = rng.standard_normal((slots * 1024, d)).astype(np.float32)
+        ta = t(arena)
+        pick = rng.permutation(slots)[:(nh + 1) * nseg].reshape(nh + 1, nseg)
+        tabs = [torch.tensor(pick[j] * 1024, dtype=torch.int64, device="cuda")
+                for j in range(nh + 1)]
+        res = torch.zeros((nh, nseg), dtype=torch.float64, device="cuda")
+        D.reduce_l1_hist(D.feat(ta, tabs[0]), [D.feat(ta, tabs[1 + j]) for j in range(nh)],
+                         S, d, nseg, res)
+        got = res.cpu().numpy()
+        one = torch.zeros(nseg, dtype=torch.float64, device="cuda")
+        for j in range(nh):
+            D.reduce_l1(D.feat(ta, tabs[0]), D.feat(ta, tabs[1 + j]), S, d, nseg, one)
+            ref = one.cpu().numpy()
+            for v in range(nseg):
+                x = arena[pick[0, v] * 1024: pick[0, v] * 1024 + S]
+                h = arena[pick[1 + j, v] * 1024: pick[1 + j, v] * 1024 + S]
+                assert got[j, v] == pytest.approx(O.variation([h], x), rel=1e-12)
+                assert got[j, v] == pytest.approx(ref[v], rel=1e-13)
+        again = torch.zeros_like(res)
+        D.reduce_l1_hist(D.feat(ta, tabs[0]), [D.feat(ta, tabs[1 + j]) for j in range(nh)],
+                         S, d, nseg, again)
+        assert torch.equal(again, res)   # deterministic (fixed-order sums)
+
     def test_srap_dedup_equals_full(self, D):
         """SRAP over (layer, video) segments with repeated slot pairs: reducing
         only the representatives (dup_src) gives the full results bit for bit,
