@@ -229,6 +229,11 @@ typedef struct QcbDdpm {
   const float* x; const float* eps; const float* noise; float* out;
   long long n;
   double c1, c2, c3;
+  double rc2;                /* RN(1 / c2) (host IEEE division) or 0: the quotient by */
+                             /* c2 then comes from one FMA correction, else a divide  */
+  unsigned long long noise_seed;   /* gen_noise: N(0,1) from Philox4x32-10 in-kernel  */
+  unsigned long long noise_offset; /* (key = seed, counter = offset + i / 4) instead  */
+  int gen_noise;                   /* of reading `noise` (the device-noise mode)      */
 } QcbDdpm;
 
 int qcb_ddpm_step(const QcbDdpm* d, void* stream);

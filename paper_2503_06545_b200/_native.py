@@ -22,6 +22,7 @@ MAX_LAYERS = 64
 
 vp = C.c_void_p
 i32, i64, f32, f64 = C.c_int, C.c_longlong, C.c_float, C.c_double
+u64 = C.c_ulonglong
 
 
 class QcbGemm(C.Structure):
@@ -80,7 +81,8 @@ class QcbAttention(C.Structure):
 
 class QcbDdpm(C.Structure):
     _fields_ = [("x", vp), ("eps", vp), ("noise", vp), ("out", vp), ("n", i64),
-                ("c1", f64), ("c2", f64), ("c3", f64)]
+                ("c1", f64), ("c2", f64), ("c3", f64), ("rc2", f64), ("noise_seed", u64),
+                ("noise_offset", u64), ("gen_noise", i32)]
 
 
 class QcbFeat(C.Structure):

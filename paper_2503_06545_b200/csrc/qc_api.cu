@@ -96,6 +96,8 @@ extern "C" int qcb_attention_f64(const QcbAttention* a, void* stream) {
 extern "C" int qcb_ddpm_step(const QcbDdpm* d, void* stream) {
   if (!d || !d->x || !d->eps || !d->out) return QCB_ERR_VALUE;
   if (d->n <= 0) return QCB_ERR_DIM;
+  if (d->rc2 != 0.0 && d->rc2 * d->c2 != 1.0 && fabs(d->rc2 * d->c2 - 1.0) > 1e-15)
+    return QCB_ERR_VALUE;   // rc2 must be RN(1 / c2)
   return ddpm_launch(d, (cudaStream_t)stream);
 }
 

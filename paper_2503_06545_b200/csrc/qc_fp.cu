@@ -748,19 +748,86 @@ int gelu_launch(float* x, long long ld, int rows, int cols, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ ddpm
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, one call -> 4 uniforms.
+QC_DEV uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// four N(0,1) samples (Box-Muller on two uniform pairs in (0, 1])
+QC_DEV float4 normal4(unsigned long long seed, unsigned long long ctr) {
+  const uint4 r = philox4x32_10(make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), 0u, 0u),
+                                make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const float k = 2.3283064365386963e-10f;   // 2^-32
+  const float u0 = ((float)r.x + 1.0f) * k, u1 = (float)r.y * k;
+  const float u2 = ((float)r.z + 1.0f) * k, u3 = (float)r.w * k;
+  const float m0 = sqrtf(-2.0f * logf(fminf(u0, 1.0f))), m1 = sqrtf(-2.0f * logf(fminf(u2, 1.0f)));
+  float s0, c0, s1, c1;
+  sincospif(2.0f * u1, &s0, &c0);
+  sincospif(2.0f * u3, &s1, &c1);
+  return make_float4(m0 * c0, m0 * s0, m1 * c1, m1 * s1);
+}
+
+// mean = (x - c1 eps) / c2 (+ c3 noise), every operation rounded like the
+// reference's f64 expression (sampler.py:59-88).  With rc2 = RN(1/c2) the
+// quotient is q = RN(m rc2) corrected once, RN(q + (m - q c2) rc2) (exact
+// residual by FMA): the correctly rounded m / c2 (Markstein).
+QC_DEV float ddpm_elem(const QcbDdpm& d, float x, float e, float nz, bool has_noise) {
+  const double m = __dsub_rn((double)x, __dmul_rn(d.c1, (double)e));
+  double q;
+  if (d.rc2 != 0.0) {
+    const double q0 = __dmul_rn(m, d.rc2);
+    q = __fma_rn(__fma_rn(-q0, d.c2, m), d.rc2, q0);
+  } else {
+    q = __ddiv_rn(m, d.c2);
+  }
+  if (has_noise) q = __dadd_rn(q, __dmul_rn(d.c3, (double)nz));
+  return __double2float_rn(q);
+}
+
+// four elements per thread (float4 when the buffers are 16-byte aligned)
 __global__ void ddpm_k(const QcbDdpm d) {
   pdl_wait();
   pdl_trigger();
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = i4 * 4;
   if (i >= d.n) return;
-  double m = __ddiv_rn(__dsub_rn((double)d.x[i], __dmul_rn(d.c1, (double)d.eps[i])), d.c2);
-  if (d.noise) m = __dadd_rn(m, __dmul_rn(d.c3, (double)d.noise[i]));
-  d.out[i] = __double2float_rn(m);
+  const bool has_noise = d.noise != nullptr || d.gen_noise;
+  float4 nz = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (d.gen_noise) nz = normal4(d.noise_seed, d.noise_offset + (unsigned long long)i4);
+  const bool vec = i + 3 < d.n &&
+                   ((reinterpret_cast<uintptr_t>(d.x) | reinterpret_cast<uintptr_t>(d.eps) |
+                     reinterpret_cast<uintptr_t>(d.out) |
+                     (d.noise ? reinterpret_cast<uintptr_t>(d.noise) : 0)) & 15) == 0;
+  if (vec) {
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(d.x + i));
+    const float4 e = __ldcs(reinterpret_cast<const float4*>(d.eps + i));
+    if (d.noise) nz = __ldcs(reinterpret_cast<const float4*>(d.noise + i));
+    float4 o;
+    o.x = ddpm_elem(d, x.x, e.x, nz.x, has_noise);
+    o.y = ddpm_elem(d, x.y, e.y, nz.y, has_noise);
+    o.z = ddpm_elem(d, x.z, e.z, nz.z, has_noise);
+    o.w = ddpm_elem(d, x.w, e.w, nz.w, has_noise);
+    *reinterpret_cast<float4*>(d.out + i) = o;
+  } else {
+    const float nzv[4] = {nz.x, nz.y, nz.z, nz.w};
+    for (int u = 0; u < 4 && i + u < d.n; ++u)
+      d.out[i + u] = ddpm_elem(d, d.x[i + u], d.eps[i + u],
+                               d.noise ? d.noise[i + u] : nzv[u], has_noise);
+  }
 }
 
 int ddpm_launch(const QcbDdpm* d, cudaStream_t st) {
   const int th = 256;
-  launch_pdl(ddpm_k, dim3((unsigned)((d->n + th - 1) / th)), dim3(th), 0, st, *d);
+  const long long n4 = (d->n + 3) / 4;
+  launch_pdl(ddpm_k, dim3((unsigned)((n4 + th - 1) / th)), dim3(th), 0, st, *d);
   return launch_status();
 }
 

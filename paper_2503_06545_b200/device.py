@@ -325,10 +325,15 @@ def attention_f64(q, k, v, heads: int, out=None, nseg: int = 1, S=None, Skv=None
     return out
 
 
-def ddpm(x, eps, c1: float, c2: float, noise=None, c3: float = 0.0, out=None, stream=None):
+def ddpm(x, eps, c1: float, c2: float, noise=None, c3: float = 0.0, out=None, stream=None,
+         noise_gen=None):
+    """reverse_step / final_step (sampler.py:59-88).  noise: a tensor, or
+    noise_gen = (seed, offset) for in-kernel Philox N(0,1) noise."""
     if out is None:
         out = torch.empty_like(x)
-    d = N.QcbDdpm(N.ptr(x), N.ptr(eps), N.ptr(noise), N.ptr(out), x.numel(), c1, c2, c3)
+    seed, off = noise_gen if noise_gen is not None else (0, 0)
+    d = N.QcbDdpm(N.ptr(x), N.ptr(eps), N.ptr(noise), N.ptr(out), x.numel(), c1, c2, c3,
+                  1.0 / float(c2), int(seed), int(off), 1 if noise_gen is not None else 0)
     N.check(N.lib().qcb_ddpm_step(C.byref(d), N.stream_ptr(stream)), "ddpm_step")
     count(1)
     return out

@@ -556,10 +556,10 @@ class QuantCacheEngine:
                 self.slot_view(vs.x).copy_(torch.from_numpy(x0.reshape(S, d)))
                 self.cond[v].copy_(torch.from_numpy(cond))
             vids.append(vs)
-        gen = None
-        if self.opts.noise == "device":
-            gen = torch.Generator(device=self.dev)
-            gen.manual_seed(int(device_noise_seed if device_noise_seed is not None else seeds[0]))
+        # device-noise mode: N(0,1) drawn inside the DDPM kernel (Philox4x32-10 keyed
+        # by this seed, one counter range per (step, video))
+        gen = int(device_noise_seed if device_noise_seed is not None else seeds[0]) \
+            if self.opts.noise == "device" else None
         self._early = None
         # cross-attention K/V of the cond tokens, per (layer, bits), for this call
         self._kv_cache: Dict[tuple, tuple] = {}
@@ -805,14 +805,12 @@ class QuantCacheEngine:
                             bias=self.head_b, seg_rows=self.Sp, seg_valid=S,
                             a_row0=tabh[0], M=nv * self.Sp)
         with self._ph("sampler"):
-            if t > 0:
-                if self.opts.noise == "numpy":
-                    for v, vs in enumerate(vids):
-                        self.noise_host[v].numpy()[:] = vs.rng.standard_normal(
-                            (F, Tk, d)).astype(np.float32).reshape(S, d)
-                    self.noise_dev[:nv].copy_(self.noise_host[:nv], non_blocking=True)
-                else:
-                    self.noise_dev[:nv].normal_(generator=gen)
+            if t > 0 and self.opts.noise == "numpy":
+                for v, vs in enumerate(vids):
+                    self.noise_host[v].numpy()[:] = vs.rng.standard_normal(
+                        (F, Tk, d)).astype(np.float32).reshape(S, d)
+                self.noise_dev[:nv].copy_(self.noise_host[:nv], non_blocking=True)
+            quads = (S * d + 3) // 4
             a_t = self.ab[t]
             for v, vs in enumerate(vids):
                 new = vs.pool.alloc()
@@ -822,9 +820,12 @@ class QuantCacheEngine:
                     alpha = a_t / a_p
                     beta = 1.0 - alpha
                     c3 = float(np.sqrt((1.0 - a_p) / (1.0 - a_t) * beta)) if t > 1 else 0.0
+                    dev_noise = gen is not None and t > 1
                     Dv.ddpm(self.slot_view(vs.x), eps_v, float(beta / np.sqrt(1.0 - a_t)),
-                            float(np.sqrt(alpha)), self.noise_dev[v] if t > 1 else None, c3,
-                            out=self.slot_view(new))
+                            float(np.sqrt(alpha)),
+                            self.noise_dev[v] if (t > 1 and not dev_noise) else None, c3,
+                            out=self.slot_view(new),
+                            noise_gen=(gen, (t * self.nv + v) * quads) if dev_noise else None)
                 else:
                     Dv.ddpm(self.slot_view(vs.x), eps_v, float(np.sqrt(1.0 - self.ab[0])),
                             float(np.sqrt(self.ab[0])), out=self.slot_view(new))

@@ -438,6 +438,38 @@ class TestFp:
         assert np.array_equal(got, O.ddpm_final(x, e, ab))
 
 
+class TestDdpm:
+    def test_markstein_quotient_exact(self, D):
+        """(x - c1 eps) / c2 via RN(1/c2) and one FMA correction == numpy's f64
+        expression (sampler.py:59-80), over many coefficient sets."""
+        rng = np.random.default_rng(31)
+        n = 1 << 20
+        for trial in range(24):
+            x = (rng.standard_normal(n) * 10.0 ** rng.uniform(-3, 3)).astype(np.float32)
+            e = rng.standard_normal(n).astype(np.float32)
+            nz = rng.standard_normal(n).astype(np.float32)
+            c1, c2, c3 = (float(v) for v in rng.uniform(1e-4, 2.0, 3))
+            if trial % 3 == 0:
+                c2 = float(np.sqrt(1.0 - rng.uniform(1e-4, 0.05)))   # sqrt(alpha) as sampled
+            got = D.ddpm(t(x), t(e), c1, c2, t(nz), c3).cpu().numpy()
+            want = ((x.astype(np.float64) - c1 * e.astype(np.float64)) / c2
+                    + c3 * nz.astype(np.float64)).astype(np.float32)
+            assert np.array_equal(got.view(np.int32), want.view(np.int32)), trial
+
+    def test_device_noise_deterministic_normal(self, D):
+        """noise_gen: seeded in-kernel N(0,1) (Philox4x32-10), reproducible and
+        offset-addressed (the device-noise mode of the engine)."""
+        n = 1 << 22
+        z = torch.zeros(n, device="cuda")
+        a = D.ddpm(z, z, 0.0, 1.0, None, 1.0, noise_gen=(7, 0)).cpu().numpy()
+        b = D.ddpm(z, z, 0.0, 1.0, None, 1.0, noise_gen=(7, 0)).cpu().numpy()
+        c = D.ddpm(z, z, 0.0, 1.0, None, 1.0, noise_gen=(7, n // 4)).cpu().numpy()
+        assert np.array_equal(a, b) and not np.array_equal(a, c)
+        assert abs(a.mean()) < 5e-3 and abs(a.std() - 1.0) < 5e-3
+        assert abs(np.mean(a ** 4) - 3.0) < 0.05          # Gaussian kurtosis
+        assert abs(np.corrcoef(a[:-1], a[1:])[0, 1]) < 5e-3
+
+
 class TestReductions:
     def test_hlc_srap_l1(self, D):
         rng = np.random.default_rng(9)
