@@ -46,10 +46,36 @@ QC_DEV void block_sum_vec(double (&v)[NV], double* scratch /*[NV][8]*/) {
 }
 
 // kind 0: hlc (2 sums), 1: srap (3 sums), 2: l1 (1 sum).
+// one float4 of each operand into the kind's sums
+template <int KIND, int NV>
+QC_DEV void reduce4(const float4 x, const float4 y, const float4 z, bool alias, double (&acc)[NV]) {
+  const float xa[4] = {x.x, x.y, x.z, x.w}, ya[4] = {y.x, y.y, y.z, y.w};
+  const float za[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const double xd = xa[e], yd = ya[e];
+    if (KIND == 0) {
+      acc[0] += fabs(xd - yd);
+      const double d = xd - (double)za[e];
+      acc[1] += d * d;
+    } else if (KIND == 1) {
+      if (alias) {
+        acc[0] += xd * xd;
+      } else {
+        acc[0] += xd * yd;
+        acc[1] += xd * xd;
+        acc[2 % NV] += yd * yd;
+      }
+    } else {
+      acc[0] += fabs(xd - yd);
+    }
+  }
+}
+
 template <int KIND, int NV>
 __global__ void __launch_bounds__(kRThreads)
     seg_reduce(FeatP f0, FeatP f1, FeatP f2, int rows, int cols, const int* seg_active,
-               double* partials, int* tickets, double* res, int chunks) {
+               double* partials, int* tickets, double* res, int chunks, int flat) {
   pdl_wait();
   pdl_trigger();
   __shared__ double scratch[NV * 8];
@@ -67,7 +93,31 @@ __global__ void __launch_bounds__(kRThreads)
   // SRAP on a pruned chain compares a slot with itself: read it once.
   const bool alias = (KIND == 1) && (f0.base == f1.base) && (f0.ld == f1.ld) &&
                      (f0.row0 ? (f1.row0 && f0.row0[seg] == f1.row0[seg]) : !f1.row0);
-  for (int r = r0; r < r1; ++r) {
+  if (flat) {
+    // every operand's segment is one contiguous block (ld == cols): stream a flat
+    // float4 range with two loads per operand in flight per thread
+    const long long n4 = (long long)rows * cols / 4;
+    const long long e0 = n4 * chunk / chunks, e1 = n4 * (chunk + 1) / chunks;
+    const float4* a = reinterpret_cast<const float4*>(feat_row(f0, seg, rows, 0));
+    const float4* b = reinterpret_cast<const float4*>(feat_row(f1, seg, rows, 0));
+    const float4* c = KIND == 0 ? reinterpret_cast<const float4*>(feat_row(f2, seg, rows, 0))
+                                : nullptr;
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    long long i = e0 + threadIdx.x;
+    for (; i + kRThreads < e1; i += 2 * kRThreads) {
+      const float4 x0 = __ldg(a + i), x1 = __ldg(a + i + kRThreads);
+      const float4 y0 = alias ? zero4 : __ldg(b + i);
+      const float4 y1 = alias ? zero4 : __ldg(b + i + kRThreads);
+      const float4 z0 = KIND == 0 ? __ldg(c + i) : zero4;
+      const float4 z1 = KIND == 0 ? __ldg(c + i + kRThreads) : zero4;
+      reduce4<KIND, NV>(x0, y0, z0, alias, acc);
+      reduce4<KIND, NV>(x1, y1, z1, alias, acc);
+    }
+    for (; i < e1; i += kRThreads)
+      reduce4<KIND, NV>(__ldg(a + i), alias ? zero4 : __ldg(b + i),
+                        KIND == 0 ? __ldg(c + i) : zero4, alias, acc);
+  }
+  for (int r = flat ? r1 : r0; r < r1; ++r) {
     const float* a = feat_row(f0, seg, rows, r);
     const float* b = feat_row(f1, seg, rows, r);
     const float* c = KIND == 0 ? feat_row(f2, seg, rows, r) : nullptr;
@@ -312,9 +362,21 @@ static int launch_reduce(QcbFeat a, QcbFeat b, QcbFeat c, int rows, int cols, in
   if (rows <= 0 || cols <= 0 || nseg <= 0 || nseg > kMaxSegs) return QCB_ERR_DIM;
   int* tickets = reinterpret_cast<int*>(ws);
   double* partials = reinterpret_cast<double*>(tickets + kMaxSegs);
-  const int ch = chunks_for(rows, cols, nseg);
+  // contiguous segments (ld == cols): flat streaming with ~2K float4 per CTA,
+  // sized for the segment alone (masked-out segments' CTAs exit at once)
+  const bool flat = cols % 4 == 0 && a.ld == cols && b.ld == cols && (KIND != 0 || c.ld == cols);
+  int ch;
+  if (flat) {
+    const long long n4 = (long long)rows * cols / 4;
+    ch = (int)((n4 + 2047) / 2048);
+    if (ch > kMaxChunks) ch = kMaxChunks;
+    if (ch < 1) ch = 1;
+  } else {
+    ch = chunks_for(rows, cols, nseg);
+  }
   launch_pdl(seg_reduce<KIND, NV>, dim3(ch, nseg), dim3(kRThreads), 0, (cudaStream_t)stream,
-             fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch);
+             fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch,
+             flat ? 1 : 0);
   return launch_status();
 }
 

@@ -71,8 +71,9 @@ def main():
     q = rows(qrep)
     g = rows(grep_)
     qcall = [d for d in q if any(k in d["kernel"] for k in ("aq4_pass1", "aq2_pass2", "init_keys"))]
+    n_calls = max(1, sum(1 for d in qcall if "aq4_pass1" in d["kernel"]))
     q_traffic = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
-                    for d in qcall)
+                    for d in qcall) / n_calls   # per quantizer call
     gemm = [d for d in g if "gemm_u8" in d["kernel"]]
     g_traffic = (sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
                      for d in gemm) / len(gemm)) if gemm else None
