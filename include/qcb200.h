@@ -273,6 +273,11 @@ int qcb_reduce_l1_hist(QcbFeat x, const QcbFeat* hist, int nh, int rows, int col
 
 size_t qcb_reduce_workspace_bytes(int nseg);
 
+/* Stream-ordered copy of `bytes` (cudaMemcpyAsync, kind inferred from the
+ * pointers): the engine's per-step table uploads and decision read-back without
+ * a framework dispatch per copy. */
+int qcb_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+
 /* ---------------------------------------------------------------- policy */
 typedef struct QcbThresholds {  /* schedule.py:22-42 */
   double delta1, delta2;

@@ -115,3 +115,11 @@ extern "C" const char* qcb_version(void) { return "qcb200 0.1.0 sm_100a"; }
 cudaError_t qc::g_last_err = cudaSuccess;
 
 extern "C" const char* qcb_last_error(void) { return cudaGetErrorString(qc::g_last_err); }
+
+extern "C" int qcb_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return QCB_OK;
+  if (!dst || !src) return QCB_ERR_VALUE;
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream) == cudaSuccess
+             ? QCB_OK
+             : QCB_ERR_CUDA;
+}

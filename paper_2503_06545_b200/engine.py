@@ -58,6 +58,25 @@ def balance_scales(w: np.ndarray, act_absmax: np.ndarray) -> np.ndarray:
     return c
 
 
+class DevRows:
+    """An uploaded int64 row table: its device address (all the kernels need)
+    and, on demand, the torch view of it."""
+    __slots__ = ("ptr", "n", "_src", "_off")
+
+    def __init__(self, ptr: int, n: int, src: torch.Tensor, off: int):
+        self.ptr, self.n, self._src, self._off = ptr, n, src, off
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def __len__(self) -> int:
+        return self.n
+
+    @property
+    def t(self) -> torch.Tensor:
+        return self._src[self._off:self._off + self.n]
+
+
 class SlotPool:
     """Refcounted residual-stream slots of one video."""
 
@@ -270,6 +289,9 @@ class QuantCacheEngine:
         n_idx = 2 * max(1 << 15, 16 * L * (nv + 4) + 64)
         self.idx_host = torch.zeros(n_idx, dtype=torch.int64).pin_memory()
         self.idx_dev = torch.zeros(n_idx, dtype=torch.int64, device=dev)
+        self._idx_np = self.idx_host.numpy()
+        self._idx_hptr = self.idx_host.data_ptr()
+        self._idx_dptr = self.idx_dev.data_ptr()
         self._begin_step(0)
 
     # ------------------------------------------------------------------ index tables
@@ -282,28 +304,23 @@ class QuantCacheEngine:
         self._idx_end = self._idx_base + half
         self._idx_cur = self._idx_base
 
-    def _upload_idx(self, arrays: Sequence[Sequence[int]], stream=None) -> List[torch.Tensor]:
+    def _upload_idx(self, arrays: Sequence[Sequence[int]], stream=None) -> List[DevRows]:
         """Pack small int64 row tables into a pinned region, one H2D copy (on
         `stream`, default the current one: the stream whose kernels read them)."""
-        sizes = [len(a) for a in arrays]
-        total = sum(sizes)
-        lo = self._idx_cur
-        if lo + total > self._idx_end:
-            raise RuntimeError("index table staging overflow")
-        if total:
-            flat = np.concatenate([np.asarray(a, np.int64) for a in arrays])
-            self.idx_host[lo:lo + total].numpy()[:] = flat
-            if stream is None:
-                self.idx_dev[lo:lo + total].copy_(self.idx_host[lo:lo + total], non_blocking=True)
-            else:
-                with torch.cuda.stream(stream):
-                    self.idx_dev[lo:lo + total].copy_(self.idx_host[lo:lo + total],
-                                                      non_blocking=True)
-        self._idx_cur = lo + total
-        out, off = [], lo
-        for n in sizes:
-            out.append(self.idx_dev[off:off + n])
+        lo = off = self._idx_cur
+        buf = self._idx_np
+        out = []
+        for a in arrays:
+            n = len(a)
+            if off + n > self._idx_end:
+                raise RuntimeError("index table staging overflow")
+            buf[off:off + n] = a
+            out.append(DevRows(self._idx_dptr + 8 * off, n, self.idx_dev, off))
             off += n
+        if off > lo:
+            N.check(N.lib().qcb_copy_async(self._idx_dptr + 8 * lo, self._idx_hptr + 8 * lo,
+                                           8 * (off - lo), N.stream_ptr(stream)), "copy_async")
+        self._idx_cur = off
         return out
 
     def rows(self, slot: int) -> int:
@@ -475,7 +492,7 @@ class QuantCacheEngine:
             self._kv_cache[key] = kv
         if list(vids) == list(range(nv)):
             return kv
-        return kv[0].index_select(0, cond_row0), kv[1].index_select(0, cond_row0)
+        return kv[0].index_select(0, cond_row0.t), kv[1].index_select(0, cond_row0.t)
 
     # ------------------------------------------------------------------ plan
     def _srap_tables(self, vids) -> List[List[int]]:
@@ -584,7 +601,8 @@ class QuantCacheEngine:
                     self._sync_plan(t, 0)    # later steps were planned by _sync_decide
             else:
                 self._plan_step(t, vids)
-            self.pol_host.copy_(self.pol, non_blocking=True)
+            N.check(N.lib().qcb_copy_async(self.pol_host.data_ptr(), self.pol.data_ptr(),
+                                           self.pol.numel(), N.stream_ptr()), "copy_async")
             st.synchronize()
             # the decisions straight from the pinned copy (QcbPolicyVideo.action /
             # .abits as int32 words; ctypes parsing costs ~10 us per video)
@@ -759,7 +777,7 @@ class QuantCacheEngine:
                     self._block(l, t, g, bits, tl[3 * gi], tl[3 * gi + 1], tl[3 * gi + 2])
                 if any(need_d):
                     base = 3 * len(groups)
-                    act = tl[base + 3].to(torch.int32)
+                    act = tl[base + 3].t.to(torch.int32)
                     with self._ph("hlc"):
                         Dv.reduce_hlc(Dv.feat(self.arena, tl[base]),
                                       Dv.feat(self.arena, tl[base + 1]),
@@ -786,7 +804,8 @@ class QuantCacheEngine:
             N.check(lib.qcb_policy_observe_all(pol, nv, L, t, self.thc, N.ptr(self.hlc_v), sp),
                     "observe_all")
             Dv.count(1)
-            self.pol_trace[t].copy_(self.pol, non_blocking=True)
+            N.check(lib.qcb_copy_async(self.pol_trace.data_ptr() + t * self.pol.numel(), pol,
+                                       self.pol.numel(), sp), "copy_async")
             if t > 0:
                 ready = torch.cuda.Event()
                 ready.record(st)
