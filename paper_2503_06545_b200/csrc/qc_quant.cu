@@ -315,12 +315,16 @@ QC_DEV double v2_row_sum(double v, double* red_slot, int rowslot, int part) {
 // the reference's (xm / sd) * g: w's f32 rounding is certain unless w lies
 // within 64 (1 + |u| / |w|) ulp64(w) of an f32 tie (covers cancellation
 // without a separate test; w == 0 and the f32 range edges always qualify).
+// Integer-only and conservative: |u| / |w| < 2^(e_u - e_w + 1) from the binary
+// exponents, so the window is below 2^(7 + max(0, e_u - e_w + 1)) ulp64.
 QC_DEV bool ln_near_tie(double w, double u) {
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(w);
-  const int ex = (int)((bits >> 52) & 0x7FF) - 1023;
-  if (ex < -125 || ex > 126) return true;
-  const int d = (int)((unsigned)bits & 0x1FFFFFFFu) - (1 << 28);
-  return fabs(i2d_alu(d)) * fabs(w) < 64.0 * (fabs(w) + fabs(u));
+  const uint32_t hw = (uint32_t)__double2hiint(w), lw = (uint32_t)__double2loint(w);
+  const int ew = (int)((hw >> 20) & 0x7FFu);
+  const int eu = (int)(((uint32_t)__double2hiint(u) >> 20) & 0x7FFu);
+  const bool range = (uint32_t)(ew - (1023 - 125)) > 251u;   // outside [-125, 126] (w == 0 too)
+  const int sh = 7 + max(0, eu - ew + 1);
+  const uint32_t d = (uint32_t)abs((int)(lw & 0x1FFFFFFFu) - (1 << 28));
+  return range || sh >= 29 || d < (1u << sh);
 }
 
 // rare exact paths, kept out of line so they cost no registers in the hot loops
