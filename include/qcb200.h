@@ -273,6 +273,12 @@ int qcb_reduce_l1_hist(QcbFeat x, const QcbFeat* hist, int nh, int rows, int col
 
 size_t qcb_reduce_workspace_bytes(int nseg);
 
+/* Calibration statistics (harness.py:305-311): out[k] = max(out[k], max |x[r][k]|)
+ * over the seg_valid rows of each of nseg segments (rows via x_row0, nullable);
+ * out is f32 [K], initialised by the caller (0 for a fresh record). */
+int qcb_col_absmax(const float* x, long long ldx, const long long* x_row0, int seg_rows,
+                   int seg_valid, int nseg, int K, float* out, void* stream);
+
 /* Stream-ordered copy of `bytes` (cudaMemcpyAsync, kind inferred from the
  * pointers): the engine's per-step table uploads and decision read-back without
  * a framework dispatch per copy. */

@@ -36,7 +36,7 @@ def __getattr__(name):
         "parse_config": "harness", "load_config": "harness", "run_single": "harness",
         "run_benchmark": "harness", "compare_outputs": "harness", "export_trace": "harness",
         "import_trace": "harness", "replay_check": "harness", "load_calibration": "harness",
-        "save_calibration": "harness", "calibrate": "calibration",
+        "save_calibration": "harness", "calibrate": "harness", "measure_sensitivity": "harness",
     }
     if name in lazy:
         mod = importlib.import_module(f".{lazy[name]}", __name__)

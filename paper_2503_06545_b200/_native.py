@@ -141,6 +141,7 @@ def lib():
         "qcb_reduce_l1": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp],
         "qcb_reduce_l1_hist": [QcbFeat, C.POINTER(QcbFeat), i32, i32, i32, i32, vp, vp, vp],
         "qcb_copy_async": [vp, vp, C.c_size_t, vp],
+        "qcb_col_absmax": [vp, i64, vp, i32, i32, i32, i32, vp, vp],
         "qcb_policy_plan_reuse": [vp, i32, i32, i32, QcbThresholds, vp],
         "qcb_policy_sim_mask": [vp, i32, i32, QcbThresholds, vp, vp],
         "qcb_policy_plan_finish": [vp, i32, i32, i32, QcbThresholds, vp, vp, i32, vp, i64, vp],
@@ -169,7 +170,7 @@ def lib():
 EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_head_gemm", "qcb_head_prep",
             "qcb_head_prep_bytes", "qcb_head_workspace_bytes", "qcb_act_quant", "qcb_act_quant_workspace_bytes", "qcb_weight_prep", "qcb_ln_mod",
             "qcb_attention_f64", "qcb_ddpm_step", "qcb_gelu_inplace", "qcb_reduce_hlc", "qcb_reduce_srap",
-            "qcb_reduce_l1", "qcb_reduce_l1_hist", "qcb_reduce_workspace_bytes", "qcb_copy_async", "qcb_policy_plan_reuse",
+            "qcb_reduce_l1", "qcb_reduce_l1_hist", "qcb_reduce_workspace_bytes", "qcb_copy_async", "qcb_col_absmax", "qcb_policy_plan_reuse",
             "qcb_policy_sim_mask", "qcb_policy_plan_finish", "qcb_policy_observe",
             "qcb_policy_observe_all",
             "qcb_device_sm_count", "qcb_version", "qcb_last_error")

@@ -442,6 +442,48 @@ extern "C" int qcb_reduce_l1_hist(QcbFeat x, const QcbFeat* hist, int nh, int ro
   return launch_status();
 }
 
+namespace qc {
+// Per-channel max |x| over the valid rows of every segment (calibration's
+// activation statistics, harness.py:305-311): a CTA takes a column range and a
+// row chunk; the running max of non-negative floats is merged with an integer
+// atomicMax on the IEEE bits (order-independent, exact).
+__global__ void __launch_bounds__(kRThreads)
+    col_absmax_k(const float* x, long long ldx, const long long* x_row0, int seg_rows,
+                 int seg_valid, int nseg, int K, int rows_per_chunk, float* out) {
+  pdl_wait();
+  pdl_trigger();
+  const int col = blockIdx.x * kRThreads + threadIdx.x;
+  if (col >= K) return;
+  const long long total = (long long)nseg * seg_valid;
+  const long long r0 = (long long)blockIdx.y * rows_per_chunk;
+  const long long r1 = min(r0 + rows_per_chunk, total);
+  float m = 0.0f;
+  for (long long r = r0; r < r1; ++r) {
+    const int seg = (int)(r / seg_valid), mr = (int)(r - (long long)seg * seg_valid);
+    const long long row = (x_row0 ? x_row0[seg] : (long long)seg * seg_rows) + mr;
+    m = fmaxf(m, fabsf(x[row * ldx + col]));
+  }
+  atomicMax(reinterpret_cast<unsigned int*>(out) + col, __float_as_uint(m));
+}
+}  // namespace qc
+
+extern "C" int qcb_col_absmax(const float* x, long long ldx, const long long* x_row0,
+                              int seg_rows, int seg_valid, int nseg, int K, float* out,
+                              void* stream) {
+  if (!x || !out) return QCB_ERR_VALUE;
+  if (K <= 0 || nseg <= 0 || seg_rows <= 0 || seg_valid <= 0 || seg_valid > seg_rows ||
+      ldx < K)
+    return QCB_ERR_DIM;
+  const long long total = (long long)nseg * seg_valid;
+  const int rpc = 64;
+  const long long chunks = (total + rpc - 1) / rpc;
+  if (chunks > 65535) return QCB_ERR_DIM;
+  launch_pdl(col_absmax_k, dim3((K + kRThreads - 1) / kRThreads, (unsigned)chunks),
+             dim3(kRThreads), 0, (cudaStream_t)stream, x, ldx, x_row0, seg_rows, seg_valid,
+             nseg, K, rpc, out);
+  return launch_status();
+}
+
 // ------------------------------------------------------------------ policy
 
 namespace qc {

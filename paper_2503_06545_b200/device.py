@@ -400,6 +400,18 @@ def reduce_l1_hist(x: N.QcbFeat, hist: Sequence[N.QcbFeat], rows: int, cols: int
     return res
 
 
+def col_absmax(x: torch.Tensor, K: int, out: torch.Tensor, nseg: int = 1,
+               seg_rows: Optional[int] = None, seg_valid: Optional[int] = None, x_row0=None,
+               stream=None) -> torch.Tensor:
+    """out[k] = max(out[k], max over the valid rows of |x[:, k]|) (f32, in place)."""
+    seg_rows = seg_rows or (x.shape[0] // nseg)
+    seg_valid = seg_valid or seg_rows
+    N.check(N.lib().qcb_col_absmax(N.ptr(x), x.stride(0), N.ptr(x_row0), seg_rows, seg_valid,
+                                   nseg, K, N.ptr(out), N.stream_ptr(stream)), "col_absmax")
+    count(1)
+    return out
+
+
 def thresholds_struct(th, toggles) -> N.QcbThresholds:
     return N.QcbThresholds(
         float(th.delta1), float(th.delta2), int(th.tau_max), int(th.tau_mid), int(th.tau_min),

@@ -183,6 +183,9 @@ class QuantCacheEngine:
         self.phase_profile: Optional[list] = None  # set to [] to time the other phases
         self.host_profile: Optional[list] = None   # set to []: host s from plan sync to the
                                                    # end of the block loop, per step
+        # set to {} to record, per (layer, site), the channel max |x| of every
+        # full-precision GEMM input (calibration, harness.py:305-311)
+        self.absmax_rec: Optional[Dict[tuple, torch.Tensor]] = None
         if self.opts.decisions not in ("per_video", "synchronized"):
             raise ValueError("decisions must be 'per_video' or 'synchronized'")
         self.sync = self.opts.decisions == "synchronized"
@@ -410,6 +413,13 @@ class QuantCacheEngine:
                 w = self.fpw[l][s]
                 a, a_row0 = self._prologue(x, ln, mod, nseg, seg_rows, seg_valid, x_row0,
                                            w.shape[0])
+            if self.absmax_rec is not None:
+                rec = self.absmax_rec.get((l, s))
+                if rec is None:
+                    rec = torch.zeros(w.shape[0], dtype=torch.float32, device=self.dev)
+                    self.absmax_rec[(l, s)] = rec
+                Dv.col_absmax(a, w.shape[0], rec, nseg=nseg, seg_rows=seg_rows,
+                              seg_valid=seg_valid, x_row0=a_row0)
             Dv.gemm_f64(a, w, out=target, epilogue=epi, resid=resid, gate=gate,
                         seg_rows=seg_rows, seg_valid=seg_valid, a_row0=a_row0,
                         out_row0=out_row0, resid_row0=resid_row0, M=M)

@@ -170,3 +170,28 @@ def test_sync_mode_matches_concatenated_batch_oracle(golden_dir, tname):
                 elif k != "V":
                     assert a[k] is None and b[k] is None, (k, a, b)
         assert np.array_equal(outs[v], want[v]), float(np.abs(outs[v] - want[v]).max())
+
+
+@pytest.mark.parametrize("cname", ["small", "default"])
+def test_device_calibration_matches_reference(golden_dir, cname):
+    """harness.calibrate on the device == the reference's calibrate
+    (harness.py:298-351, fixtures calib_{small,default}.json): activation
+    channel max |x| per (layer, site) exact, delta / variation percentiles and
+    per-layer sensitivities within 1e-9 relative (f64 sums in another order)."""
+    from paper_2503_06545_b200 import harness
+    base = dict(SMALL) if cname == "small" else {"seed": 7}
+    cfg = harness.parse_config(base)
+    got = harness.calibrate(cfg)
+    ref = harness.load_calibration(os.path.join(golden_dir, f"calib_{cname}.json"))
+    assert sorted(got.act_absmax) == sorted(ref.act_absmax)
+    for l, sites in ref.act_absmax.items():
+        assert sorted(got.act_absmax[l]) == sorted(sites)
+        for site, arr in sites.items():
+            assert np.array_equal(got.act_absmax[l][site], arr), (l, site)
+    for a, b in ((got.delta_p33, ref.delta_p33), (got.delta_p66, ref.delta_p66),
+                 (got.v_p25, ref.v_p25), (got.v_p75, ref.v_p75)):
+        assert a == pytest.approx(b, rel=1e-9)
+    assert sorted(got.sensitivities) == sorted(ref.sensitivities)
+    for l, v in ref.sensitivities.items():
+        assert got.sensitivities[l] == pytest.approx(v, rel=1e-9), l
+    assert got.meta == ref.meta
