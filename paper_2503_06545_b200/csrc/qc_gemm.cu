@@ -29,13 +29,25 @@ namespace qc {
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 128;  // bytes == u8 elements
 constexpr int kUmmaK = 32;    // K per tcgen05.mma kind::i8
-constexpr int kEpiWarps = 8;                    // 2 per TMEM lane quarter
-constexpr int kThreads = 128 + 32 * kEpiWarps;  // TMA, MMA, TMEM-alloc, spare + epilogue
+// Epilogue warps per CTA: 3 per TMEM lane quarter (the column chunks of a tile
+// split three ways), 2 in the residual modes (their smem holds residual slabs).
+template <int MODE>
+constexpr int epi_warps() {
+  return (MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID) ? 8 : 12;
+}
+template <int MODE>
+constexpr int gemm_threads() {
+  return 128 + 32 * epi_warps<MODE>();   // TMA, MMA, TMEM-alloc, spare + epilogue
+}
+constexpr int kMaxEpiWarps = 12;
 
-template <int BN, bool RES = false>
+// PAIR: a (2,1,1) cluster computes M = 256 tiles with tcgen05 cta_group::2 --
+// each CTA stages its own 128 rows of A and half of the tile's B columns.
+template <int BN, bool RES = false, bool PAIR = false>
 struct GemmCfg {
+  static constexpr int kEpiWarps = RES ? 8 : 12;
   static constexpr int kABytes = kBlockM * kBlockK;
-  static constexpr int kBBytes = BN * kBlockK;
+  static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * kBlockK;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32
                                         : (2 * BN <= 64) ? 64
@@ -51,7 +63,7 @@ struct GemmCfg {
   static constexpr int kFixedBytes =
       kStageOutBytes + kResBytes + kColBytes + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int kStagesWanted =
-      BN >= 256 ? 3 : (BN >= 192 ? 4 : (BN >= 128 ? 5 : (BN >= 64 ? 7 : 8)));
+      PAIR ? 8 : (BN >= 256 ? 3 : (BN >= 192 ? 4 : (BN >= 128 ? 5 : (BN >= 64 ? 7 : 8))));
   static constexpr int kStagesFit = (227 * 1024 - kFixedBytes) / kStageBytes;
   static constexpr int kStages = kStagesWanted < kStagesFit ? kStagesWanted : kStagesFit;
   static constexpr int kSmemBytes = kStages * kStageBytes + kFixedBytes;
@@ -99,14 +111,16 @@ struct GemmParams {
 };
 
 
-template <int BN, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int MODE, bool PAIR>
+__global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
     gemm_u8_tcgen05(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_out,
                     const __grid_constant__ CUtensorMap map_res, const GemmParams p) {
   constexpr bool resid_mode = (MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID);
-  using Cfg = GemmCfg<BN, resid_mode>;
+  using Cfg = GemmCfg<BN, resid_mode, PAIR>;
+  constexpr int kEpiWarps = Cfg::kEpiWarps;
+  constexpr int kSplit = kEpiWarps / 4;   // warps per TMEM lane quarter
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // Pointers are derived from the __shared__ symbol directly (no integer
   // round-trip) so the compiler keeps them in the shared window (LDS/STS).
@@ -121,12 +135,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + Cfg::kStages;
   uint64_t* tfull_bar = empty_bar + Cfg::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* res_bar = tempty_bar + 2;   // [kEpiWarps][2] residual slab barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + 2 * kEpiWarps);
+  uint64_t* res_bar = tempty_bar + 2;   // [kMaxEpiWarps][2] residual slab barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + 2 * kMaxEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  // PAIR: tiles are M = 256 and shared by the two CTAs of a cluster
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int tile_start = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tile_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  constexpr int kTileM = PAIR ? 2 * kBlockM : kBlockM;
+  auto tile_m0 = [&](int tile) -> int {   // first row of THIS CTA's 128 rows
+    return (tile / p.num_n_tiles) * kTileM + (int)rank * kBlockM;
+  };
   // k-blocks of a tile (grouped launches: per column group)
   auto tile_kb = [&](int n0) -> int {
     const int k = p.group_n ? (n0 / p.group_n + 1) * p.group_k : p.K;
@@ -142,15 +164,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], kEpiWarps);
+      mbar_init(&tempty_bar[a], PAIR ? 2 * kEpiWarps : kEpiWarps);   // both CTAs' epilogues
     }
     for (int r = 0; r < 2 * kEpiWarps; ++r) mbar_init(&res_bar[r], 1);
     if (resid_mode && p.tma_resid) tma_prefetch(&map_res);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if (PAIR) tmem_alloc2<Cfg::kTmemCols>(tmem_slot);
+    else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();   // barriers of both CTAs initialised before any remote use
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // setup above overlaps the previous kernel's tail (PDL); operands come after
@@ -168,16 +194,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tile_start; tile < num_tiles; tile += tile_step) {
         if (!tile_active(tile)) continue;
-        const int m0 = (tile / p.num_n_tiles) * kBlockM;
+        const int m0 = tile_m0(tile);
         const int n0 = (tile % p.num_n_tiles) * BN;
         const int num_kb = tile_kb(n0);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
-          tma_load_2d(&map_a, &full_bar[stage], smem_a + stage * Cfg::kABytes, kb * kBlockK, m0);
-          tma_load_2d(&map_b, &full_bar[stage], smem_b + stage * Cfg::kBBytes, kb * kBlockK, n0);
+          if (PAIR) {
+            // both CTAs' halves land on the leader's full barrier
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+            const uint32_t bar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+            tma_load_2d_pair(&map_a, bar, smem_a + stage * Cfg::kABytes, kb * kBlockK, m0);
+            tma_load_2d_pair(&map_b, bar, smem_b + stage * Cfg::kBBytes, kb * kBlockK,
+                             n0 + (int)rank * (BN / 2));
+          } else {
+            mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+            tma_load_2d(&map_a, &full_bar[stage], smem_a + stage * Cfg::kABytes, kb * kBlockK,
+                        m0);
+            tma_load_2d(&map_b, &full_bar[stage], smem_b + stage * Cfg::kBBytes, kb * kBlockK,
+                        n0);
+          }
           if (++stage == Cfg::kStages) {
             stage = 0;
             phase ^= 1;
@@ -187,13 +224,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_u8(kBlockM, BN);
+    if (lane == 0 && rank == 0) {   // PAIR: the leader issues for both CTAs
+      constexpr uint32_t idesc = idesc_u8(kTileM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tile_start; tile < num_tiles; tile += tile_step) {
         if (!tile_active(tile)) continue;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -206,16 +243,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
 #pragma unroll
           for (int k = 0; k < kBlockK / kUmmaK; ++k) {
-            umma_u8(d_tmem, smem_desc_sw128(a_addr + k * kUmmaK),
-                    smem_desc_sw128(b_addr + k * kUmmaK), idesc, (kb | k) != 0);
+            if (PAIR)
+              umma_u8_pair(d_tmem, smem_desc_sw128(a_addr + k * kUmmaK),
+                           smem_desc_sw128(b_addr + k * kUmmaK), idesc, (kb | k) != 0);
+            else
+              umma_u8(d_tmem, smem_desc_sw128(a_addr + k * kUmmaK),
+                      smem_desc_sw128(b_addr + k * kUmmaK), idesc, (kb | k) != 0);
           }
-          umma_commit(&empty_bar[stage]);
+          if (PAIR) umma_commit_pair(&empty_bar[stage]);
+          else umma_commit(&empty_bar[stage]);
           if (++stage == Cfg::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[acc]);
+        if (PAIR) umma_commit_pair(&tfull_bar[acc]);
+        else umma_commit(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -226,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ epilogue (TMEM -> regs -> global)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = threadIdx.x - 128;        // epilogue thread id
-    const int half = (warp - 4) >> 2;       // which column half of each tile this warp owns
+    const int half = (warp - 4) >> 2;       // which column third / half of each tile this warp owns
     uint8_t* stage_out = smem_out + (warp - 4) * 4096;
     // residual slabs: two 4 KB buffers per warp, filled by TMA one chunk ahead
     uint8_t* res_buf = smem_res + (warp - 4) * 8192;
@@ -236,9 +279,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t res_phase = 0;   // bit b: parity of buffer b's next completion
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = tile_start; tile < num_tiles; tile += tile_step) {
       if (!tile_active(tile)) continue;
-      const int m0 = (tile / p.num_n_tiles) * kBlockM;
+      const int m0 = tile_m0(tile);
       const int n0 = (tile % p.num_n_tiles) * BN;
       // per-tile column parameters -> smem (buffer `acc`; see the barrier note)
       ColParam* t_col = col + acc * BN;
@@ -317,17 +360,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       uint32_t res_first = res_it;   // buffer of this tile's first chunk
-      if (res_tma && slab_live && half < n_chunks) issue_res(half);
+      if (res_tma && slab_live && half < n_chunks) issue_res(half);   // (res: kSplit == 2)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half; c < n_chunks; c += 2) {
+      for (int c = half; c < n_chunks; c += kSplit) {
         const int nb = n0 + c * 32;
         float rv[32];
         if (resid_mode) {
           if (res_tma) {
             if (slab_live) {
-              if (c + 2 < n_chunks) issue_res(c + 2);   // next chunk into the other buffer
+              if (c + kSplit < n_chunks) issue_res(c + kSplit);   // next chunk, other buffer
               const uint32_t b = res_first & 1;
               mbar_wait(&rbar[b], (res_phase >> b) & 1);
               res_phase ^= 1u << b;
@@ -414,7 +457,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {   // PAIR: the leader's barrier counts both CTAs' epilogue warps
+        if (PAIR && rank != 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -423,10 +469,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) bulk_wait0();
   }
 
+  tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();   // the peer's smem / TMEM stay until the pair is done
   if (warp == 2) {
     tc_fence_after();
-    tmem_free<Cfg::kTmemCols>(tmem_base);
+    if (PAIR) tmem_free2<Cfg::kTmemCols>(tmem_base);
+    else tmem_free<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -485,14 +534,14 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool PAIR>
 static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   constexpr bool resid_mode = (MODE == QCB_EPI_GATE_RESID || MODE == QCB_EPI_RESID);
-  using Cfg = GemmCfg<BN, resid_mode>;
+  using Cfg = GemmCfg<BN, resid_mode, PAIR>;
   CUtensorMap ma, mb;
   int rc = make_map_u8(&ma, g->a_codes, g->M, g->K, g->lda, kBlockM);
   if (rc) return rc;
-  rc = make_map_u8(&mb, g->w_codes, g->N, g->K, g->ldw, BN);
+  rc = make_map_u8(&mb, g->w_codes, g->N, g->K, g->ldw, PAIR ? BN / 2 : BN);
   if (rc) return rc;
   GemmParams p{};
   p.M = g->M;
@@ -500,7 +549,7 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   p.K = g->K;
   p.seg_rows = g->seg_rows > 0 ? g->seg_rows : g->M;
   p.seg_valid = g->seg_valid > 0 ? g->seg_valid : p.seg_rows;
-  p.num_m_tiles = (g->M + kBlockM - 1) / kBlockM;
+  p.num_m_tiles = (g->M + (PAIR ? 2 : 1) * kBlockM - 1) / ((PAIR ? 2 : 1) * kBlockM);
   p.num_n_tiles = (g->N + BN - 1) / BN;
   p.sa = g->a_scale;
   p.za = g->a_zero;
@@ -547,15 +596,23 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   static_assert(Cfg::kSmemBytes <= 227 * 1024, "GEMM smem budget exceeds 227 KB");
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_u8_tcgen05<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_u8_tcgen05<BN, MODE, PAIR>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmemBytes) != cudaSuccess)
       return QCB_ERR_CUDA;
     attr_set = true;
   }
   int tiles = p.num_m_tiles * p.num_n_tiles;
-  int grid = tiles < num_sms() ? tiles : num_sms();
-  launch_pdl(gemm_u8_tcgen05<BN, MODE>, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, st, ma, mb,
-             mo, mr, p);
+  if (PAIR) {   // one CTA pair per TPC-worth of SMs, persistent over pair tiles
+    const int pairs = num_sms() / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    launch_pdl_pair(gemm_u8_tcgen05<BN, MODE, true>, dim3(grid), dim3(gemm_threads<MODE>()),
+                    Cfg::kSmemBytes, st, ma, mb, mo, mr, p);
+  } else {
+    int grid = tiles < num_sms() ? tiles : num_sms();
+    launch_pdl(gemm_u8_tcgen05<BN, MODE, false>, dim3(grid), dim3(gemm_threads<MODE>()),
+               Cfg::kSmemBytes, st, ma, mb, mo, mr, p);
+  }
   return launch_status();
 }
 
@@ -576,16 +633,33 @@ int pick_block_n(int N) {
   return best;
 }
 
-template <int BN>
-static int launch_mode(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
+template <int BN, bool PAIR>
+static int launch_mode2(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   switch (g->epilogue) {
-    case QCB_EPI_STORE: return launch_bn<BN, QCB_EPI_STORE>(g, st, grp);
-    case QCB_EPI_GELU: return launch_bn<BN, QCB_EPI_GELU>(g, st, grp);
-    case QCB_EPI_GATE_RESID: return launch_bn<BN, QCB_EPI_GATE_RESID>(g, st, grp);
-    case QCB_EPI_RESID: return launch_bn<BN, QCB_EPI_RESID>(g, st, grp);
-    case QCB_EPI_ACC: return launch_bn<BN, QCB_EPI_ACC>(g, st, grp);
+    case QCB_EPI_STORE: return launch_bn<BN, QCB_EPI_STORE, PAIR>(g, st, grp);
+    case QCB_EPI_GELU: return launch_bn<BN, QCB_EPI_GELU, PAIR>(g, st, grp);
+    case QCB_EPI_GATE_RESID: return launch_bn<BN, QCB_EPI_GATE_RESID, PAIR>(g, st, grp);
+    case QCB_EPI_RESID: return launch_bn<BN, QCB_EPI_RESID, PAIR>(g, st, grp);
+    case QCB_EPI_ACC: return launch_bn<BN, QCB_EPI_ACC, PAIR>(g, st, grp);
     default: return QCB_ERR_CONFIG;
   }
+}
+
+// CTA-pair tiles when the problem has at least one M = 256 tile per pair row
+// and no per-segment tile skipping (QCB_GEMM_PAIR=0 forces single-CTA tiles).
+static bool use_pair(const QcbGemm* g, int bn) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("QCB_GEMM_PAIR");
+    env = e ? atoi(e) : 0;
+  }
+  return env != 0 && g->seg_active == nullptr && g->M >= 2 * kBlockM && bn >= 64;
+}
+
+template <int BN>
+static int launch_mode(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
+  if (use_pair(g, BN)) return launch_mode2<BN, true>(g, st, grp);
+  return launch_mode2<BN, false>(g, st, grp);
 }
 
 // ---------------------------------------------------------------- small M

@@ -400,6 +400,18 @@ class TestFp:
         bad = np.flatnonzero(got.view(np.int32) != want.view(np.int32))
         assert bad.size == 0, (bad.size, x[bad[:5]], got[bad[:5]], want[bad[:5]])
 
+    def test_gemm_cta_pair_exact(self, D):
+        """The opt-in CTA-pair GEMM (tcgen05 cta_group::2, QCB_GEMM_PAIR=1) gives
+        the exact integer accumulators (run in a subprocess: the switch is read
+        once per process)."""
+        import subprocess, sys
+        env = dict(os.environ, QCB_GEMM_PAIR="1")
+        out = subprocess.run([sys.executable, "tools/gemm_pair_check.py"], capture_output=True,
+                             text=True, timeout=300, env=env,
+                             cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        res = json.loads(out.stdout.strip().splitlines()[-1])
+        assert all(v == 0 for v in res["mismatches"].values()), res
+
     def test_gelu_exhaustive_vs_replica(self, D):
         """Every f32 in [-14, 6] (2.18e9 values): the certified fast GELU paths
         equal the exact cephes replica (f64 GEMM GELU epilogue on a K=1 identity
