@@ -15,6 +15,7 @@
 // min/max params, u8 codes stored K-major [N][K] for the UMMA B operand, and
 // column sums for the zero-point correction.
 #include "qc_common.cuh"
+#include "qc_gelu.cuh"
 #include "qc_api_internal.h"
 
 namespace qc {
@@ -848,7 +849,9 @@ QC_DEV double flip_sign(double x, uint32_t bit) {
   return __longlong_as_double(__double_as_longlong(x) ^ ((long long)bit << 63));
 }
 
-template <int B, bool kPow2Scale, int kMinCtas>
+// kPro: the prologue compiled in (0 none, 1 LN + modulation, 2 GELU), so each
+// variant gets its own register allocation.
+template <int B, bool kPow2Scale, int kMinCtas, int kPro>
 __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuantParams p, const AQ2 a) {
   pdl_wait();   // x rows / keys come from the preceding kernels
   pdl_trigger();
@@ -873,7 +876,7 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
   // LN affine parameters as f64, once per CTA (dynamic tail of the smem block)
   double* const ln_g64 = reinterpret_cast<double*>(v4_smem + sizeof(V4Smem<B>));
   double* const ln_b64 = ln_g64 + K;
-  if (p.prologue == QCB_PRO_LN_MOD) {
+  if (kPro == 1) {
     for (int i = tid; i < K; i += kV4Threads) {
       ln_g64[i] = p.ln_g ? (double)p.ln_g[i] : 1.0;
       ln_b64[i] = p.ln_b ? (double)p.ln_b[i] : 0.0;
@@ -958,7 +961,7 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
       const int t = lt + TPR * i;
       ht[i] = (t < T) ? xs[B + t] : 0.f;
     }
-    if (p.prologue == QCB_PRO_LN_MOD) {
+    if (kPro == 1) {
       double s0 = 0.0, s1 = 0.0;   // two chains
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -1015,11 +1018,38 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
         if (t < T)
           ht[i] = ln_elem(ht[i], mean, sd, rsd, ln_g64[B + t], ln_b64[B + t], p.scale1, p.shift);
       }
-    } else if (p.prologue == QCB_PRO_GELU) {
+    } else if (kPro == 2) {
+      // f32(gelu_f64(x)) (model.py:197): the branch-free certified phase A on
+      // 8-element groups; the exact-erfc phase B, then the cephes replica, only
+      // for what phase A cannot certify (qc_gelu.cuh)
+      uint32_t hard = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) h[j] = gelu_f32_ref(h[j]);
+      for (int g = 0; g < 2; ++g) {
+        float a8[8], y8[8];
 #pragma unroll
-      for (int i = 0; i < kV4Tail; ++i) ht[i] = gelu_f32_ref(ht[i]);
+        for (int j = 0; j < 8; ++j) a8[j] = h[8 * g + j];
+        const uint32_t hg = gelu_phase_a8(a8, y8, 0xFFu);
+        hard |= hg << (8 * g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h[8 * g + j] = ((hg >> j) & 1u) ? a8[j] : y8[j];
+      }
+      if (hard) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if ((hard >> j) & 1u) {
+            float yv;
+            if (!gelu_fast_b(h[j], yv)) yv = gelu_f32_ref(h[j]);
+            h[j] = yv;
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < kV4Tail; ++i) {
+        if (lt + TPR * i < T) {
+          float yv;
+          if (!gelu_fast_a(ht[i], yv) && !gelu_fast_b(ht[i], yv)) yv = gelu_f32_ref(ht[i]);
+          ht[i] = yv;
+        }
+      }
     }
     // every thread of the slot has read the smem row: refill it with row k+2
     row_sync();
@@ -1547,21 +1577,26 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
       // the LN prologue's f64 affine tables take 16 K bytes of smem: 2 CTAs per
       // SM there (128 registers), 3 CTAs per SM otherwise (80 registers)
       const bool ln = q->prologue == QCB_PRO_LN_MOD;
+      const int pro = ln ? 1 : (q->prologue == QCB_PRO_GELU ? 2 : 0);
       const size_t ln_bytes = ln ? (size_t)16 * q->K : 0;
-      const int cap = num_sms() * (ln ? 2 : 3);
+      const int cap = num_sms() * (pro ? 2 : 3);
       if (b1 > cap) b1 = cap;
-      switch (b * 2 + (ln ? 1 : 0)) {
-#define QC_AQ4(BB, P2, MC, FLAG)                                                            \
-  allow_max_smem(aq4_pass1<BB, P2, MC>, FLAG);                                              \
-  launch_pdl(aq4_pass1<BB, P2, MC>, dim3(b1), dim3(kV4Threads), sizeof(V4Smem<BB>) + ln_bytes, \
-             st, p, a);                                                                    \
+      static bool a41g = false, a42g = false, a44g = false;
+      switch (b * 4 + pro) {
+#define QC_AQ4(BB, P2, MC, PRO, FLAG)                                                          \
+  allow_max_smem(aq4_pass1<BB, P2, MC, PRO>, FLAG);                                            \
+  launch_pdl(aq4_pass1<BB, P2, MC, PRO>, dim3(b1), dim3(kV4Threads),                           \
+             sizeof(V4Smem<BB>) + ln_bytes, st, p, a);                                         \
   break;
-        case 2048: QC_AQ4(1024, true, 3, a41)
-        case 2049: QC_AQ4(1024, true, 2, a41l)
-        case 4096: QC_AQ4(2048, false, 3, a42)
-        case 4097: QC_AQ4(2048, false, 2, a42l)
-        case 8192: QC_AQ4(4096, true, 3, a44)
-        default: QC_AQ4(4096, true, 2, a44l)
+        case 4096: QC_AQ4(1024, true, 3, 0, a41)
+        case 4097: QC_AQ4(1024, true, 2, 1, a41l)
+        case 4098: QC_AQ4(1024, true, 2, 2, a41g)
+        case 8192: QC_AQ4(2048, false, 3, 0, a42)
+        case 8193: QC_AQ4(2048, false, 2, 1, a42l)
+        case 8194: QC_AQ4(2048, false, 2, 2, a42g)
+        case 16384: QC_AQ4(4096, true, 3, 0, a44)
+        case 16385: QC_AQ4(4096, true, 2, 1, a44l)
+        default: QC_AQ4(4096, true, 2, 2, a44g)
 #undef QC_AQ4
       }
     } else switch (b) {

@@ -474,7 +474,9 @@ class QuantCacheEngine:
                    resid=A, resid_row0=out_row0)
         # FFN.  On the integer path GELU (model.py:197) runs as its own in-place
         # kernel between ffn1 and the ffn2 quantizer: same f32(gelu_f64(y)) per
-        # element, with divergent exact evaluations compacted per warp.
+        # element, with divergent exact evaluations compacted per warp.  (As the
+        # ffn2 quantizer's prologue it measured slower: the exact-erfc path
+        # diverges per thread there and the variant runs at 2 CTAs per SM.)
         int_path = self.tog.aigq_weights and self.tog.aigq_acts and bits < FP_BITS
         self._site(l, "ffn1", bits, A, n, x_row0=out_row0, ln=(ln3g, ln3b), mod=(sc3, sh3),
                    epi=N.EPI_STORE if int_path else N.EPI_GELU, out=self.hid)
