@@ -55,7 +55,9 @@ enum {
   QCB_EPI_GATE_RESID = 2, /* out = resid + gate * y (f32)    (sta_o, ffn2)        */
   QCB_EPI_RESID = 3,      /* out = resid + y (f32)           (ca_o)               */
   QCB_EPI_ACC = 4,        /* out = exact s32 accumulator (debug / parity)         */
-  QCB_EPI_BIAS = 5        /* out = y + bias[n] (f32)         (head, gemm_f64 only) */
+  QCB_EPI_BIAS = 5,       /* out = y + bias[n] (f32)         (head, gemm_f64 only) */
+  QCB_EPI_STORE_BF16 = 6  /* out = bf16(f32 y), out as uint16 [M][ldo] (q, k, v for */
+                          /* the bf16 attention path; gemm_u8 only)               */
 };
 
 /* Activation prologues. */

@@ -22,7 +22,9 @@ extern "C" int qcb_gemm_u8(const QcbGemm* g, void* stream) {
   if ((long long)g->K * 255LL * 255LL > 2147483647LL) return QCB_ERR_OVERFLOW;
   if ((g->epilogue == QCB_EPI_GATE_RESID || g->epilogue == QCB_EPI_RESID) && !g->resid)
     return QCB_ERR_VALUE;
-  if (g->epilogue < QCB_EPI_STORE || g->epilogue > QCB_EPI_ACC) return QCB_ERR_CONFIG;
+  if (g->epilogue < QCB_EPI_STORE || g->epilogue > QCB_EPI_STORE_BF16 ||
+      g->epilogue == QCB_EPI_BIAS)
+    return QCB_ERR_CONFIG;
   if (reinterpret_cast<uintptr_t>(g->a_codes) % 16 || reinterpret_cast<uintptr_t>(g->w_codes) % 16)
     return QCB_ERR_DIM;
   return gemm_u8_launch(g, (cudaStream_t)stream);

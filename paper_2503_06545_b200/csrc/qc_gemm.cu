@@ -19,6 +19,7 @@
 // Fused epilogues (model.py:187-198): plain store (q/k/v, ca_*), exact-erf GELU
 // in f64 (ffn1), x + gate*y (sta_o, ffn2) and x + y (ca_o), with the f32
 // roundings of the reference (no FMA contraction).
+#include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 #include "qc_common.cuh"
@@ -432,7 +433,30 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
             }
           }
         }
-        if (p.tma_store) {
+        if (MODE == QCB_EPI_STORE_BF16) {
+          // 32x32 bf16 slab (64-byte rows) -> 64B-swizzled smem (16-byte chunk c of
+          // row r at c ^ ((r >> 1) & 3)) -> one TMA bulk tensor store
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          uint8_t* rowp = stage_out + lane * 64;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+              w4[e] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            *reinterpret_cast<uint4*>(rowp + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                make_uint4(w4[0], w4[1], w4[2], w4[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_out, stage_out, nb, (int)orow_slab);
+            bulk_commit();
+          }
+        } else if (p.tma_store) {
           // 32x32 f32 slab -> 128B-swizzled smem -> one TMA bulk tensor store.
           if (lane == 0) bulk_wait_read0();  // previous store finished reading
           __syncwarp();
@@ -524,6 +548,21 @@ static int make_map_out(CUtensorMap* map, const void* base, long long rows, int 
   return r == CUDA_SUCCESS ? QCB_OK : QCB_ERR_CUDA;
 }
 
+// 2-D bf16 output [rows][ld] (N valid columns), box 32 x 32, 64-byte swizzle.
+static int make_map_out_bf16(CUtensorMap* map, const void* base, long long rows, int N,
+                             long long ld) {
+  auto enc = get_encode_fn();
+  if (!enc) return QCB_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? QCB_OK : QCB_ERR_CUDA;
+}
+
 static int g_num_sms = 0;
 int num_sms() {
   if (!g_num_sms) {
@@ -577,9 +616,16 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   const long long out_rows = g->out_rows > 0 ? g->out_rows : (long long)g->M;
   CUtensorMap mo = ma;
   p.tma_store = 0;
-  if (slab_contig && (g->ldo * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->out) & 15) == 0 &&
-      make_map_out(&mo, g->out, out_rows, g->N, g->ldo) == QCB_OK)
+  if (MODE == QCB_EPI_STORE_BF16) {   // bf16 output: TMA store only (no per-row path)
+    if (!slab_contig || (g->ldo * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(g->out) & 15) ||
+        g->N % 8 != 0 || make_map_out_bf16(&mo, g->out, out_rows, g->N, g->ldo) != QCB_OK)
+      return QCB_ERR_DIM;
     p.tma_store = 1;
+  } else if (slab_contig && (g->ldo * 4) % 16 == 0 &&
+             (reinterpret_cast<uintptr_t>(g->out) & 15) == 0 &&
+             make_map_out(&mo, g->out, out_rows, g->N, g->ldo) == QCB_OK) {
+    p.tma_store = 1;
+  }
   // TMA residual slabs under the same contiguity rule (residual rows per segment)
   CUtensorMap mr = ma;
   p.tma_resid = 0;
@@ -641,6 +687,7 @@ static int launch_mode2(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp)
     case QCB_EPI_GATE_RESID: return launch_bn<BN, QCB_EPI_GATE_RESID, PAIR>(g, st, grp);
     case QCB_EPI_RESID: return launch_bn<BN, QCB_EPI_RESID, PAIR>(g, st, grp);
     case QCB_EPI_ACC: return launch_bn<BN, QCB_EPI_ACC, PAIR>(g, st, grp);
+    case QCB_EPI_STORE_BF16: return launch_bn<BN, QCB_EPI_STORE_BF16, PAIR>(g, st, grp);
     default: return QCB_ERR_CONFIG;
   }
 }
@@ -761,7 +808,8 @@ __global__ void __launch_bounds__(32 * kSmallWarps) gemm_u8_small_m(const QcbGem
 }
 
 int gemm_u8_launch(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
-  if (!grp && g->M <= kSmallM && g->block_n <= 0 && g->epilogue != QCB_EPI_BIAS) {
+  if (!grp && g->M <= kSmallM && g->block_n <= 0 && g->epilogue != QCB_EPI_BIAS &&
+      g->epilogue != QCB_EPI_STORE_BF16) {
     const size_t smem = (size_t)g->M * ((g->K + 15) & ~15);
     if (smem <= 200 * 1024) {
       static bool attr = false;

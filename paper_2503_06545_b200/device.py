@@ -202,7 +202,8 @@ def gemm_u8(a: ActCodes, w: PackedWeight, M: Optional[int] = None, out=None,
         raise DimensionError(f"matmul shapes (M,{a.K}) x ({w.K},{w.N})")
     M = M if M is not None else a.codes.shape[0]
     if out is None:
-        dt = torch.int32 if epilogue == N.EPI_ACC else torch.float32
+        dt = {N.EPI_ACC: torch.int32, N.EPI_STORE_BF16: torch.bfloat16}.get(epilogue,
+                                                                          torch.float32)
         out = torch.empty((M, w.N), dtype=dt, device=dev)
     g = N.QcbGemm()
     g.M, g.N, g.K = M, w.N, w.K

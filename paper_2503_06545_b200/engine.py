@@ -256,6 +256,9 @@ class QuantCacheEngine:
         self.hid = torch.zeros((rows, K4), dtype=torch.float32, device=dev)
         self.eps = torch.zeros((rows, d), dtype=torch.float32, device=dev)
         self.q2 = torch.zeros_like(self.q)
+        # bf16 q/k/v written by the integer GEMMs' epilogue for the bf16 attention
+        self.qkv16 = [torch.zeros((rows, d), dtype=torch.bfloat16, device=dev) for _ in range(3)] \
+            if self.opts.attention == "fast" else None
         self.cond = torch.zeros((nv, self.c), dtype=torch.float32, device=dev)
         self.ac = [Dv.ActCodes(self.codes[o][:, :Dv.round16(d)],
                                torch.zeros(rows, dtype=torch.int32, device=dev),
@@ -439,8 +442,10 @@ class QuantCacheEngine:
             qq = q[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].permute(0, 2, 1, 3)
             kk = k[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].permute(0, 2, 1, 3)
             vv = v[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].permute(0, 2, 1, 3)
+            bf = torch.bfloat16
             o = torch.nn.functional.scaled_dot_product_attention(
-                qq.to(torch.bfloat16), kk.to(torch.bfloat16), vv.to(torch.bfloat16))
+                qq if qq.dtype == bf else qq.to(bf), kk if kk.dtype == bf else kk.to(bf),
+                vv if vv.dtype == bf else vv.to(bf))
             out[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].copy_(o.permute(0, 2, 1, 3))
             return
         a = N.QcbAttention(N.ptr(q), q.stride(0), N.ptr(k), k.stride(0), N.ptr(v), v.stride(0),
@@ -458,11 +463,15 @@ class QuantCacheEngine:
         sh3, sc3, g3 = m[3], one + m[4], m[5]
         ln1g, ln1b, ln2g, ln2b, ln3g, ln3b = self.ln[l]
         A = self.arena
-        # spatial-temporal self-attention
+        # spatial-temporal self-attention; on the integer path with the bf16
+        # attention kernel the q/k/v GEMMs write bf16 directly (no conversion pass)
+        int_path = self.tog.aigq_weights and self.tog.aigq_acts and bits < FP_BITS
+        qkv = self.qkv16 if (self.qkv16 is not None and int_path) else [self.q, self.k, self.v]
         self._site(l, None, bits, A, n, x_row0=xin_row0, ln=(ln1g, ln1b), mod=(sc1, sh1),
-                   outs=[self.q, self.k, self.v], sites=("sta_q", "sta_k", "sta_v"))
+                   outs=qkv, sites=("sta_q", "sta_k", "sta_v"),
+                   epi=N.EPI_STORE_BF16 if qkv is self.qkv16 else N.EPI_STORE)
         with self._ph("attention"):
-            self._attention(self.q, self.k, self.v, self.att, n, self.S, self.Sp)
+            self._attention(qkv[0], qkv[1], qkv[2], self.att, n, self.S, self.Sp)
         self._site(l, "sta_o", bits, self.att, n, epi=N.EPI_GATE_RESID, out=A,
                    out_row0=out_row0, resid=A, resid_row0=xin_row0, gate=g1)
         # cross-attention on the single cond token
@@ -477,7 +486,6 @@ class QuantCacheEngine:
         # element, with divergent exact evaluations compacted per warp.  (As the
         # ffn2 quantizer's prologue it measured slower: the exact-erfc path
         # diverges per thread there and the variant runs at 2 CTAs per SM.)
-        int_path = self.tog.aigq_weights and self.tog.aigq_acts and bits < FP_BITS
         self._site(l, "ffn1", bits, A, n, x_row0=out_row0, ln=(ln3g, ln3b), mod=(sc3, sh3),
                    epi=N.EPI_STORE if int_path else N.EPI_GELU, out=self.hid)
         if int_path:

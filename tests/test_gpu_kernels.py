@@ -400,6 +400,27 @@ class TestFp:
         bad = np.flatnonzero(got.view(np.int32) != want.view(np.int32))
         assert bad.size == 0, (bad.size, x[bad[:5]], got[bad[:5]], want[bad[:5]])
 
+    @pytest.mark.parametrize("M,K,Nn", [(8192, 1152, 1152), (640, 256, 200), (4096, 128, 384)])
+    def test_gemm_bf16_epilogue(self, D, M, K, Nn):
+        """EPI_STORE_BF16 (q/k/v for the bf16 attention path) == bf16(the exact f32
+        epilogue output), incl. segment padding rows and ragged N."""
+        from paper_2503_06545_b200 import _native as Nat
+        rng = np.random.default_rng(M + Nn)
+        x = rng.standard_normal((M, K)).astype(np.float32)
+        w = (rng.standard_normal((K, Nn)) / np.sqrt(K)).astype(np.float32)
+        pw = D.weight_prep(t(w), 8)
+        seg_rows = 256 if M % 256 == 0 else M
+        seg_valid = seg_rows - 16 if M % 256 == 0 else M
+        nseg = M // seg_rows
+        (a,) = D.act_quant(t(x), 8, [None], seg_rows=seg_rows, seg_valid=seg_valid, nseg=nseg)
+        f32 = D.gemm_u8(a, pw, M=M, seg_rows=seg_rows, seg_valid=seg_valid)
+        b16 = D.gemm_u8(a, pw, M=M, epilogue=Nat.EPI_STORE_BF16, seg_rows=seg_rows,
+                        seg_valid=seg_valid)
+        assert b16.dtype == torch.bfloat16
+        valid = np.concatenate([np.arange(v * seg_rows, v * seg_rows + seg_valid)
+                                for v in range(nseg)])
+        assert torch.equal(b16[valid], f32[valid].to(torch.bfloat16))
+
     def test_gemm_cta_pair_exact(self, D):
         """The opt-in CTA-pair GEMM (tcgen05 cta_group::2, QCB_GEMM_PAIR=1) gives
         the exact integer accumulators (run in a subprocess: the switch is read
