@@ -109,7 +109,7 @@ def _cpu_head_sample(rows: int, seed: int = 0) -> float:
 # Recompute fraction of the C3 QuantCache run (the reference's decisions equal
 # ours bit for bit -- tests/test_gpu_engine.py -- so both arms extrapolate with
 # the fraction our calibrated C3 run measures).
-C3_RECOMPUTE_FRACTION = 0.035
+C3_RECOMPUTE_FRACTION = 0.030
 
 
 def _videos_per_s_from_sample(t_block: float, t_head: float, rows: int, S: int, L: int,
@@ -445,11 +445,14 @@ def run_ours(args):
         rows = 4
         ts = _cpu_block_sample(rows, 0)
         th_ = _cpu_head_sample(rows, 0)
-        cpu = {"value": _videos_per_s_from_sample(ts, th_, rows, S, cfg.num_blocks, T, frac),
+        # the same constant fraction as the reference arm (the measured one of this
+        # run is reported as recompute_fraction)
+        cf = C3_RECOMPUTE_FRACTION
+        cpu = {"value": _videos_per_s_from_sample(ts, th_, rows, S, cfg.num_blocks, T, cf),
                "unit": "videos/s", "cores": 1, "kind": "port",
                "sample": f"oracle quantizer + 8 int GEMM sites of one C3 block ({ts:.1f} s) and "
                          f"the f64 noise head ({th_:.2f} s) on {rows} rows, extrapolated "
-                         f"x{S}/{rows} rows x {T} steps x (head + recompute fraction {frac:.3f} "
+                         f"x{S}/{rows} rows x {T} steps x (head + recompute fraction {cf:.3f} "
                          f"x 28 blocks); attention excluded"}
     tops = g_ops / g_time / 1e12 if g_time > 0 else None
     peak_tops = peak.get("tops") or NOMINAL_INT8_TOPS
