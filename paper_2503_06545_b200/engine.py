@@ -565,8 +565,9 @@ class QuantCacheEngine:
         """Run the full reverse trajectory for len(seeds) videos (one per seed).
 
         The initial latent and cond are drawn from NumPy's stream per seed like
-        the reference (sampler.py:108-111), unless device-resident x0_dev
-        [nv,S,d] / cond_dev [nv,c] are given (benchmark: inputs already in HBM).
+        the reference (sampler.py:108-111), unless x0_dev [nv,S,d] / cond_dev
+        [nv,c] are given: device tensors (inputs already in HBM) or host tensors
+        (pinned for an async copy), copied into the video's slots.
         collect_features (list, optional): appended per step with
         (t, x_t [nv,S,d], [block outputs [nv,S,d] per layer]) host copies, like
         the reference's generate(collect_features=...) (sampler.py:113-126).
