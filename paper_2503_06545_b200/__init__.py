@@ -31,7 +31,8 @@ def __getattr__(name):
         "BalanceTransform": "quant", "allocate_weight_bits": "quant",
         "WeightBitPlan": "quant",
         "matmul_int": "tensor", "matmul_fp": "tensor", "mm": "tensor", "attention": "tensor",
-        "layernorm": "tensor", "Tensor": "tensor",
+        "layernorm": "tensor", "Tensor": "tensor", "divergence_score": "tensor",
+        "layer_similarity": "tensor", "cumulative_variation": "tensor",
         "RunConfig": "harness", "RunMetrics": "harness", "CalibrationData": "harness",
         "parse_config": "harness", "load_config": "harness", "run_single": "harness",
         "run_benchmark": "harness", "compare_outputs": "harness", "export_trace": "harness",

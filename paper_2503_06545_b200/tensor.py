@@ -123,3 +123,72 @@ def layernorm(x: Tensor, gamma: Tensor, beta: Tensor) -> Tensor:
     x2 = xd.reshape(-1, shape[-1])
     out = Dv.ln_mod(x2, g, b)
     return Tensor(out.reshape(shape), frame_axis=getattr(x, "frame_axis", None))
+
+
+# ---------------------------------------------------------------------------
+# Policy statistics (schedule.py:67-133) on the device reduction kernels: the
+# same f64 sums the engine's HLC / SRAP / V paths use, over one flat segment.
+
+def _shape(x):
+    return tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
+
+
+def _flat(x) -> torch.Tensor:
+    return _cuda(x).reshape(1, -1)
+
+
+def _res(n: int) -> torch.Tensor:
+    return torch.zeros(n, dtype=torch.float64, device="cuda")
+
+
+def divergence_score(p_now, p_cached, k: int, m_now, m_prev) -> float:
+    """(sum|p_now - p_cached| / k) * ||m_now - m_prev||_2 (schedule.py:67-82)."""
+    if _shape(p_now) != _shape(p_cached) or _shape(m_now) != _shape(m_prev):
+        raise DimensionError("divergence operands must share shapes")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    a, b, m, mp = _flat(p_now), _flat(p_cached), _flat(m_now), _flat(m_prev)
+    r1, r2 = _res(1), _res(2)
+    Dv.reduce_l1(Dv.feat(a), Dv.feat(b), 1, a.shape[1], 1, r1)
+    Dv.reduce_hlc(Dv.feat(m), Dv.feat(m), Dv.feat(mp), 1, m.shape[1], 1, r2)
+    return (float(r1[0]) / k) * float(np.sqrt(float(r2[1])))
+
+
+def layer_similarity(p_l, p_l1) -> float:
+    """Cosine of two flattened feature maps, 0 when a norm is 0
+    (schedule.py:108-116)."""
+    if _shape(p_l) != _shape(p_l1):
+        raise DimensionError("similarity operands must share shapes")
+    a, b = _flat(p_l), _flat(p_l1)
+    r = _res(3)
+    Dv.reduce_srap(Dv.feat(a), Dv.feat(b), 1, a.shape[1], 1, r.view(1, 3))
+    dot, aa, bb = (float(v) for v in r.cpu())
+    na, nb = float(np.sqrt(aa)), float(np.sqrt(bb))
+    if na == 0.0 or nb == 0.0:
+        return 0.0
+    return dot / (na * nb)
+
+
+def cumulative_variation(history, current) -> float:
+    """sum over the history of sum|current - h| (schedule.py:128-133)."""
+    hist = list(history)
+    if not hist:
+        return 0.0
+    cur = _flat(current)
+    hs = [_flat(h) for h in hist]
+    for h in hs:
+        if h.shape != cur.shape:
+            raise DimensionError("variation operands must share shapes")
+    total = 0.0
+    for i in range(0, len(hs), 8):   # up to 8 history entries per pass over x
+        part = hs[i:i + 8]
+        r = _res(len(part))
+        if cur.shape[1] % 4 == 0:
+            Dv.reduce_l1_hist(Dv.feat(cur), [Dv.feat(h) for h in part], 1, cur.shape[1], 1,
+                              r.view(len(part), 1))
+        else:
+            for j, h in enumerate(part):
+                Dv.reduce_l1(Dv.feat(cur), Dv.feat(h), 1, cur.shape[1], 1, r[j:j + 1])
+        for v in r.cpu().tolist():
+            total += v
+    return total

@@ -221,3 +221,17 @@ class TestTraceIO:  # test_harness.py:249-312
         assert harness.compare_outputs(a, a) == (0.0, 99.0)
         mse, psnr = harness.compare_outputs(a, a * 2)
         assert mse == 1.0 and psnr == pytest.approx(0.0)
+
+
+class TestPolicyStatsErrors:   # schedule.py:67-82, 108-116 error conventions
+    def test_shape_and_k_checks(self):
+        from paper_2503_06545_b200 import (cumulative_variation, divergence_score,
+                                           layer_similarity)
+        from paper_2503_06545_b200.errors import DimensionError
+        with pytest.raises(DimensionError):
+            divergence_score(np.zeros(3), np.zeros(4), 1, np.zeros(2), np.zeros(2))
+        with pytest.raises(ValueError):
+            divergence_score(np.zeros(3), np.zeros(3), 0, np.zeros(2), np.zeros(2))
+        with pytest.raises(DimensionError):
+            layer_similarity(np.zeros((2, 3)), np.zeros((3, 2)))
+        assert cumulative_variation([], np.zeros(5)) == 0.0

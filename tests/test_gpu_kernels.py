@@ -558,6 +558,23 @@ class TestReductions:
                          S, d, nseg, again)
         assert torch.equal(again, res)   # deterministic (fixed-order sums)
 
+    @pytest.mark.parametrize("n", [64 * 64, 4 * 16 * 64 + 3, 4096 * 1152])
+    def test_policy_statistics_api(self, D, n):
+        """divergence_score / layer_similarity / cumulative_variation on the device
+        == the reference formulas (oracle, schedule.py:67-133), incl. a length that
+        is not a multiple of 4, zero-norm similarity and > 8 history entries."""
+        from paper_2503_06545_b200 import (cumulative_variation, divergence_score,
+                                           layer_similarity)
+        rng = np.random.default_rng(n % 97)
+        a, b, m, mp = (rng.standard_normal(n).astype(np.float32) for _ in range(4))
+        assert divergence_score(a, b, 3, m, mp) == pytest.approx(
+            O.divergence5(a, b, 3, m, mp), rel=1e-12)
+        assert layer_similarity(a, b) == pytest.approx(O.similarity(a, b), rel=1e-12,
+                                                       abs=1e-15)
+        assert layer_similarity(a, np.zeros(n, np.float32)) == 0.0
+        hist = [rng.standard_normal(n).astype(np.float32) for _ in range(9)]
+        assert cumulative_variation(hist, a) == pytest.approx(O.variation(hist, a), rel=1e-12)
+
     def test_srap_dedup_equals_full(self, D):
         """SRAP over (layer, video) segments with repeated slot pairs: reducing
         only the representatives (dup_src) gives the full results bit for bit,
