@@ -33,6 +33,7 @@ def __getattr__(name):
         "matmul_int": "tensor", "matmul_fp": "tensor", "mm": "tensor", "attention": "tensor",
         "layernorm": "tensor", "Tensor": "tensor", "divergence_score": "tensor",
         "layer_similarity": "tensor", "cumulative_variation": "tensor",
+        "predict_noise": "forward", "block_forward": "forward",
         "RunConfig": "harness", "RunMetrics": "harness", "CalibrationData": "harness",
         "parse_config": "harness", "load_config": "harness", "run_single": "harness",
         "run_benchmark": "harness", "compare_outputs": "harness", "export_trace": "harness",

@@ -95,16 +95,27 @@ def generate(model, sched: NoiseSchedule, scheduler=None, seed: int = 0,
     scheduler (schedule.Scheduler) receives the trace like the reference's."""
     from .engine import EngineOptions, QuantCacheEngine
     from .schedule import ThresholdConfig, Toggles
-    if extra_hooks is not None or collect_features is not None:
+    if scheduler is None and (extra_hooks is not None or collect_features is not None):
+        # caller hooks see every block: the per-block device path (forward.py)
+        from .forward import generate_hooked
+        return generate_hooked(model, sched, seed, collect_features, extra_hooks)
+    if extra_hooks is not None:
         raise NotImplementedError(
-            "per-call Python hooks are served by predict_noise-level APIs; generate() "
-            "runs the fused device engine")
+            "extra_hooks with a scheduler: the scheduled run is the fused device engine; "
+            "pass hooks without a scheduler (forward.generate_hooked)")
     if scheduler is None:
         eng = QuantCacheEngine(model, sched.alpha_bar, Toggles(),
                                ThresholdConfig(delta1=0.0, delta2=0.0), options=options)
     else:
         eng = scheduler.engine(model, sched, options)
-    out, traces = eng.generate([seed])
+    feats = [] if collect_features is not None else None
+    out, traces = eng.generate([seed], collect_features=feats)
     if scheduler is not None:
         scheduler.trace.extend(traces[0])
+    if feats is not None:   # the reference's (t, x_t, [block outputs]) of video 0
+        from .tensor import Tensor
+        shp = (model.cfg.frames, model.cfg.tokens_per_frame, model.cfg.model_dim)
+        for t, x_now, outs in feats:
+            collect_features.append((t, Tensor(x_now[0].reshape(shp), frame_axis=0),
+                                     [Tensor(o[0]) for o in outs]))
     return torch.as_tensor(out[0]).cuda()

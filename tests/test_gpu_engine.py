@@ -195,3 +195,35 @@ def test_device_calibration_matches_reference(golden_dir, cname):
     for l, v in ref.sensitivities.items():
         assert got.sensitivities[l] == pytest.approx(v, rel=1e-9), l
     assert got.meta == ref.meta
+
+
+def test_hooked_generate_and_predict_noise(golden_dir, runs):
+    """generate(..., collect_features / extra_hooks) and predict_noise run the
+    per-block device path (forward.py): bit-identical to the reference's
+    full-precision run, hooks see every block and every GEMM site."""
+    from paper_2503_06545_b200 import LayerHooks, generate, harness, predict_noise
+    from paper_2503_06545_b200.errors import DimensionError
+    from paper_2503_06545_b200.forward import _mm
+    from paper_2503_06545_b200.model import init_model
+    cfg = harness.parse_config(dict(SMALL))
+    model, sched = init_model(cfg.model_config()), cfg.noise_schedule()
+    seed = cfg.seeds["sampling"]
+    feats = []
+    out = generate(model, sched, seed=seed, collect_features=feats).cpu().numpy()
+    assert np.array_equal(out, runs["small_none"])
+    L = model.cfg.num_blocks
+    assert [f[0] for f in feats] == list(range(sched.steps - 1, -1, -1))
+    assert all(len(f[2]) == L for f in feats)
+    calls, seen = [], []
+    hooks = LayerHooks(after_block=lambda l, o: seen.append(l),
+                       gemm=lambda l, s, a, w: (calls.append((l, s)), _mm(a, w))[1])
+    out2 = generate(model, sched, seed=seed, extra_hooks=hooks).cpu().numpy()
+    assert np.array_equal(out2, runs["small_none"])
+    assert len(calls) == sched.steps * L * 10 and len(seen) == sched.steps * L
+    x = feats[0][1]
+    with pytest.raises(ValueError):
+        predict_noise(x, sched.steps, np.zeros(model.cfg.cond_dim, np.float32), model,
+                      total_steps=sched.steps)
+    with pytest.raises(DimensionError):
+        predict_noise(np.zeros((1, 2, 3), np.float32), 0,
+                      np.zeros(model.cfg.cond_dim, np.float32), model)
