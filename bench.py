@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--videos", type=int, default=2, help="videos per GPU per step")
+    ap.add_argument("--videos", type=int, default=4, help="videos per GPU per step")
     ap.add_argument("--timesteps", type=int, default=100)
     ap.add_argument("--wbits", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
