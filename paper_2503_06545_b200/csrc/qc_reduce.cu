@@ -72,17 +72,11 @@ QC_DEV void reduce4(const float4 x, const float4 y, const float4 z, bool alias, 
   }
 }
 
+// one (segment, chunk) work item of seg_reduce; leaves the block synchronised
 template <int KIND, int NV>
-__global__ void __launch_bounds__(kRThreads)
-    seg_reduce(FeatP f0, FeatP f1, FeatP f2, int rows, int cols, const int* seg_active,
-               double* partials, int* tickets, double* res, int chunks, int flat) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double scratch[NV * 8];
-  __shared__ bool last;
-  const int seg = blockIdx.y;
-  if (seg_active && !seg_active[seg]) return;
-  const int chunk = blockIdx.x;
+QC_DEV void seg_item(const FeatP& f0, const FeatP& f1, const FeatP& f2, int rows, int cols,
+                     double* partials, int* tickets, double* res, int chunks, int flat,
+                     int seg, int chunk, double* scratch, bool& last) {
   const int r0 = (int)((long long)rows * chunk / chunks);
   const int r1 = (int)((long long)rows * (chunk + 1) / chunks);
   double acc[NV];
@@ -209,6 +203,33 @@ __global__ void __launch_bounds__(kRThreads)
       for (int i = 0; i < NV; ++i) res[(size_t)seg * NV + i] = tot[i];
       tickets[seg] = 0;
     }
+  }
+  __syncthreads();  // scratch / last are reused by the next item
+}
+
+// Persistent grid over (segment, chunk) items, segment-major: a masked-out segment
+// costs each CTA one flag read per item instead of a CTA launch (SRAP masks most
+// of its L*videos segments, and launching ~64K idle CTAs cost ~100 us a step).
+template <int KIND, int NV>
+__global__ void __launch_bounds__(kRThreads)
+    seg_reduce(FeatP f0, FeatP f1, FeatP f2, int rows, int cols, int nseg,
+               const int* seg_active, double* partials, int* tickets, double* res, int chunks,
+               int flat) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double scratch[NV * 8];
+  __shared__ bool last;
+  const long long items = (long long)nseg * chunks;
+  for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+    const int seg = (int)(w / chunks);
+    if (seg_active && !seg_active[seg]) {
+      // skip the rest of this segment's items owned by this CTA
+      const long long seg_end = (long long)(seg + 1) * chunks;
+      if (seg_end - w > gridDim.x) w += ((seg_end - w - 1) / gridDim.x) * gridDim.x;
+      continue;
+    }
+    seg_item<KIND, NV>(f0, f1, f2, rows, cols, partials, tickets, res, chunks, flat, seg,
+                       (int)(w % chunks), scratch, last);
   }
 }
 
@@ -374,8 +395,10 @@ static int launch_reduce(QcbFeat a, QcbFeat b, QcbFeat c, int rows, int cols, in
   } else {
     ch = chunks_for(rows, cols, nseg);
   }
-  launch_pdl(seg_reduce<KIND, NV>, dim3(ch, nseg), dim3(kRThreads), 0, (cudaStream_t)stream,
-             fp(a), fp(b), fp(c), rows, cols, seg_active, partials, tickets, res, ch,
+  long long items = (long long)ch * nseg;
+  const int grid = (int)(items < 8LL * num_sms() ? items : 8LL * num_sms());
+  launch_pdl(seg_reduce<KIND, NV>, dim3(grid), dim3(kRThreads), 0, (cudaStream_t)stream,
+             fp(a), fp(b), fp(c), rows, cols, nseg, seg_active, partials, tickets, res, ch,
              flat ? 1 : 0);
   return launch_status();
 }
