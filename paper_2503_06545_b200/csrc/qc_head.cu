@@ -125,6 +125,23 @@ QC_DEV void head_digits(double r, int (&U)[kHeadDigits]) {
   }
 }
 
+// The same codes from the f32 bits on the integer pipe: F = floor(x 2^(47-e))
+// (|x| < 2^e, so |F| < 2^47) in two's complement; U_0 = (F >> 40) + 128 is byte 5
+// with its sign bit flipped and U_s (s >= 1) is byte 5 - s -- the base-256 floor
+// expansion head_digits forms for r = x 2^-e.  Returns F's low 48 bits.
+QC_DEV unsigned long long head_fixed(float x, int e) {
+  const unsigned b = __float_as_uint(x);
+  const int ex = (int)((b >> 23) & 0xFFu);
+  const long long m = (long long)((b & 0x7FFFFFu) | (ex ? 0x800000u : 0u));
+  // x = +-m 2^(max(ex,1) - 150); sh <= 23 for finite rows (the clamp only keeps a
+  // non-finite row's codes defined: its certificate is not finite -> fallback)
+  const int sh = max(ex, 1) - 103 - e;
+  const long long sm = (b >> 31) ? -m : m;
+  const long long f = sh >= 0 ? (long long)((unsigned long long)sm << min(sh, 23))
+                                : sm >> min(-sh, 40);   // floor
+  return (unsigned long long)f;
+}
+
 QC_DEV double up(double v) { return v * (1.0 + 0x1p-40); }   // generous upward padding
 
 // 2^n as f64 for |n| < 1000 (exact, no library call)
@@ -234,7 +251,7 @@ struct HeadRows {
 };
 
 // One warp per output row i: statistics, digit codes, planes, prefix code sums.
-__global__ void __launch_bounds__(32 * kHeadSliceWarps)
+__global__ void __launch_bounds__(32 * kHeadSliceWarps, 6)
     head_slice_rows(const HeadRows h, uint8_t* ws, HeadWsLayout L) {
   pdl_wait();
   pdl_trigger();
@@ -257,6 +274,7 @@ __global__ void __launch_bounds__(32 * kHeadSliceWarps)
   }
   const float* xr = h.x + ((h.x_row0 ? h.x_row0[seg] : (long long)seg * h.seg_rows) + r) * h.ldx;
   double amax = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll 3
   for (int k = 4 * lane; k < K; k += 128) {
     const float4 x4 = *reinterpret_cast<const float4*>(xr + k);
     const double a0 = fabs((double)x4.x), a1 = fabs((double)x4.y);
@@ -273,26 +291,33 @@ __global__ void __launch_bounds__(32 * kHeadSliceWarps)
   const int e = head_exponent(amax);
   int cs[kHeadDigits] = {0, 0, 0, 0, 0, 0};
   int sq[kHeadDigits] = {0, 0, 0, 0, 0, 0};   // sum (U - 128)^2 <= 128^2 K < 2^31
-  const double sc = pow2(-e);
-  // 4 consecutive k per lane -> one 32-bit store per plane (K % 4 == 0)
+  // 4 consecutive k per lane -> one 32-bit store per plane (K % 4 == 0); the
+  // codes are bytes of the fixed-point words (head_fixed), packed by PRMT, and
+  // the plane sums / squared balanced norms are byte dot products
   for (int k0 = 4 * lane; k0 < K; k0 += 128) {
-    uint32_t pk[kHeadDigits] = {0, 0, 0, 0, 0, 0};
     const float4 x4 = *reinterpret_cast<const float4*>(xr + k0);
-    const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+    const unsigned long long f0 = head_fixed(x4.x, e), f1 = head_fixed(x4.y, e);
+    const unsigned long long f2 = head_fixed(x4.z, e), f3 = head_fixed(x4.w, e);
+    const uint32_t lo01 = __byte_perm((uint32_t)f0, (uint32_t)f1, 0x5140);   // b0 b0' b1 b1'
+    const uint32_t lo23 = __byte_perm((uint32_t)f2, (uint32_t)f3, 0x5140);
+    const uint32_t mid01 = __byte_perm((uint32_t)f0, (uint32_t)f1, 0x7362);  // b2 b2' b3 b3'
+    const uint32_t mid23 = __byte_perm((uint32_t)f2, (uint32_t)f3, 0x7362);
+    const uint32_t top01 = __byte_perm((uint32_t)(f0 >> 32), (uint32_t)(f1 >> 32), 0x5140);
+    const uint32_t top23 = __byte_perm((uint32_t)(f2 >> 32), (uint32_t)(f3 >> 32), 0x5140);
+    uint32_t pk[kHeadDigits];
+    pk[0] = __byte_perm(top01, top23, 0x7632) ^ 0x80808080u;   // byte 5
+    pk[1] = __byte_perm(top01, top23, 0x5410);                 // byte 4
+    pk[2] = __byte_perm(mid01, mid23, 0x7632);                 // byte 3
+    pk[3] = __byte_perm(mid01, mid23, 0x5410);                 // byte 2
+    pk[4] = __byte_perm(lo01, lo23, 0x7632);                   // byte 1
+    pk[5] = __byte_perm(lo01, lo23, 0x5410);                   // byte 0
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int U[kHeadDigits];
-      head_digits((double)xv[u] * sc, U);
-#pragma unroll
-      for (int s = 0; s < kHeadDigits; ++s) {
-        pk[s] |= (uint32_t)U[s] << (8 * u);
-        cs[s] += U[s];
-        sq[s] += (U[s] - kZp) * (U[s] - kZp);
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < kHeadDigits; ++s)
+    for (int s = 0; s < kHeadDigits; ++s) {
+      cs[s] = (int)__dp4a(pk[s], 0x01010101u, (unsigned)cs[s]);
+      const int bal = (int)(pk[s] ^ 0x80808080u);   // B = U - 128 as s8 lanes
+      sq[s] = __dp4a(bal, bal, sq[s]);
       *reinterpret_cast<uint32_t*>(prow + (size_t)s * K + k0) = pk[s];
+    }
   }
 #pragma unroll
   for (int s = 0; s < kHeadDigits; ++s)

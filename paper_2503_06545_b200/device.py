@@ -281,6 +281,8 @@ def head_gemm(a: torch.Tensor, hw: HeadWeights, out=None, bias=None, seg_rows=No
     rows = nseg * seg_rows
     if out is None:
         out = torch.empty((rows, hw.N), dtype=torch.float32, device=dev)
+    elif out_row0 is None and (out.shape[0] < rows or out.shape[-1] < hw.N):
+        raise DimensionError(f"head output {tuple(out.shape)} smaller than ({rows}, {hw.N})")
     ws = _HWS.get(int(N.lib().qcb_head_workspace_bytes(rows, K, hw.N)))
     g = N.QcbHeadGemm()
     g.nseg, g.seg_rows, g.seg_valid, g.K, g.N = nseg, seg_rows, seg_valid, K, hw.N
