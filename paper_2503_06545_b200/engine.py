@@ -40,6 +40,15 @@ from .schedule import FP_BITS, ThresholdConfig, Toggles, TraceRecord, billed_mac
     prune_draw_table
 
 ACTION_NAMES = ("recompute", "reuse", "prune")
+_POLICY_DTYPE = None
+
+
+def _policy_dtype() -> np.dtype:
+    """numpy structured dtype of QcbPolicyVideo (same field offsets)."""
+    global _POLICY_DTYPE
+    if _POLICY_DTYPE is None:
+        _POLICY_DTYPE = np.dtype(N.QcbPolicyVideo)
+    return _POLICY_DTYPE
 
 
 def balance_scales(w: np.ndarray, act_absmax: np.ndarray) -> np.ndarray:
@@ -897,23 +906,37 @@ class QuantCacheEngine:
         return self._collect_traces(vids)
 
     def _collect_traces(self, vids) -> List[List[TraceRecord]]:
-        raw = self.pol_trace.cpu().numpy()
-        nv = len(vids)
+        """Per-video TraceRecords (schedule.py:187-210) from the per-step policy
+        records: one structured numpy view of the [T][videos] QcbPolicyVideo
+        array, columns converted to Python lists once (per-record ctypes
+        access cost ~40 ms per 4-video call)."""
+        nv, L = len(vids), self.L
+        npv = 1 if self.sync else nv
+        raw = self.pol_trace[:, :npv * self.pol_size].cpu().numpy()
+        rec = np.ascontiguousarray(raw).view(_policy_dtype()).reshape(self.T, npv)
+        A, DV, DN = rec["action"].tolist(), rec["d_valid"].tolist(), rec["d_now"].tolist()
+        SV, SM = rec["sim_valid"].tolist(), rec["sim"].tolist()
+        AB, VV = rec["abits"].tolist(), rec["v"].tolist()
+        wbs = [self.weight_bits.get(l, FP_BITS) if self.tog.aigq_weights else FP_BITS
+               for l in range(L)]
+        macs_of: Dict[int, list] = {}   # abits -> billed MACs per layer when recomputed
+        rc = N.ACT_RECOMPUTE
+        head_macs = self.head_macs * FP_BITS * FP_BITS
         traces = [[] for _ in range(nv)]
-        wb_of = lambda l: self.weight_bits.get(l, FP_BITS) if self.tog.aigq_weights else FP_BITS
+        layers = range(L)
         for t in range(self.T - 1, -1, -1):
             for v in range(nv):
                 pv = 0 if self.sync else v
-                p = N.QcbPolicyVideo.from_buffer_copy(
-                    raw[t, pv * self.pol_size:(pv + 1) * self.pol_size].tobytes())
-                for l in range(self.L):
-                    a = p.action[l]
-                    wb = wb_of(l)
-                    macs = billed_macs(self.block_cost, wb, p.abits) if a == N.ACT_RECOMPUTE else 0
-                    traces[v].append(TraceRecord(
-                        t, l, ACTION_NAMES[a], float(p.d_now[l]) if p.d_valid[l] else None,
-                        float(p.sim[l]) if p.sim_valid[l] else None, int(p.abits), wb, macs,
-                        float(p.v)))
-                traces[v].append(TraceRecord(t, "head", "recompute", None, None, FP_BITS,
-                                             FP_BITS, self.head_macs * FP_BITS * FP_BITS))
+                ab, vf = int(AB[t][pv]), float(VV[t][pv])
+                mt = macs_of.get(ab)
+                if mt is None:
+                    mt = macs_of[ab] = [billed_macs(self.block_cost, wb, ab) for wb in wbs]
+                out = traces[v]
+                out.extend([TraceRecord(t, l, ACTION_NAMES[a], dn if dv else None,
+                                        sm if sv else None, ab, wb, m if a == rc else 0, vf)
+                            for l, a, dv, dn, sv, sm, wb, m in
+                            zip(layers, A[t][pv], DV[t][pv], DN[t][pv], SV[t][pv], SM[t][pv],
+                                wbs, mt)])
+                out.append(TraceRecord(t, "head", "recompute", None, None, FP_BITS, FP_BITS,
+                                       head_macs))
         return traces
