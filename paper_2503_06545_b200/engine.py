@@ -25,6 +25,7 @@ values (D, S, V) stay on device until the end of the run.
 from __future__ import annotations
 
 import contextlib
+import gc
 import time
 import ctypes as C
 from dataclasses import dataclass, field
@@ -645,10 +646,19 @@ class QuantCacheEngine:
             for vs in vids:
                 vs.seen += 1
             self._run_step(t, vids, act_tab, abits_of, collect_features, gen)
-        out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
         if return_device:
+            out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
             return out, vids
-        return out.cpu().numpy(), self._collect_traces(vids)
+        # latents to the host: a pinned block from torch's caching host allocator
+        # (a new array per call, reused only once the caller drops it) filled by
+        # async per-video D2H copies on the engine stream (a pageable .cpu() of
+        # the stacked latents ran at ~2 GB/s: 36 ms for 4 C3 videos)
+        host = torch.empty((nv, S, d), dtype=torch.float32, pin_memory=True)
+        for v, vs in enumerate(vids):
+            host[v].copy_(self.slot_view(vs.x), non_blocking=True)
+        traces = self._collect_traces(vids)   # its trace read-back follows the copies
+        st.synchronize()
+        return host.numpy().reshape(nv, F, Tk, d), traces
 
     def _plan_step(self, t: int, vids):
         """Per-video plan of step t: V reductions, plan_reuse + SRAP (unless the
@@ -910,6 +920,15 @@ class QuantCacheEngine:
         records: one structured numpy view of the [T][videos] QcbPolicyVideo
         array, columns converted to Python lists once (per-record ctypes
         access cost ~40 ms per 4-video call)."""
+        gc_was = gc.isenabled()
+        gc.disable()   # ~12k new records would trigger collections (+45 ms when one hits gen 2)
+        try:
+            return self._collect_traces_impl(vids)
+        finally:
+            if gc_was:
+                gc.enable()
+
+    def _collect_traces_impl(self, vids) -> List[List[TraceRecord]]:
         nv, L = len(vids), self.L
         npv = 1 if self.sync else nv
         raw = self.pol_trace[:, :npv * self.pol_size].cpu().numpy()
