@@ -282,7 +282,10 @@ class QuantCacheEngine:
         self._abits_off = N.QcbPolicyVideo.abits.offset // 4
         self.pol = torch.zeros(nv * self.pol_size, dtype=torch.uint8, device=dev)
         self.pol_host = torch.zeros(nv * self.pol_size, dtype=torch.uint8).pin_memory()
-        self.pol_trace = torch.zeros((self.T, nv * self.pol_size), dtype=torch.uint8, device=dev)
+        # per-step policy records, copied D2H after each step's observe into pinned
+        # host memory, where the host turns finished steps into TraceRecords while
+        # it waits on the next decision sync
+        self.pol_trace = torch.zeros((self.T, nv * self.pol_size), dtype=torch.uint8).pin_memory()
         self.srap = torch.zeros((L, nv, 3), dtype=torch.float64, device=dev)
         self.mask = torch.zeros((L, nv), dtype=torch.int32, device=dev)
         self.hist_l1 = torch.zeros((self.th.history_k + 1, nv), dtype=torch.float64, device=dev)
@@ -624,6 +627,8 @@ class QuantCacheEngine:
             self.sync_mask_v = self.sync_mask.view(-1)[:L * nv].view(L, nv)
             self.sync_mask_v.fill_(1)
             self.sync_mask_v[0].zero_()
+        traces = [[] for _ in range(nv)]
+        t_built = T - 1   # the next step whose records are turned into TraceRecords
         for t in range(T - 1, -1, -1):
             self._begin_step(t)
             # ---------------- plan (device) ----------------
@@ -634,6 +639,11 @@ class QuantCacheEngine:
                 self._plan_step(t, vids)
             N.check(N.lib().qcb_copy_async(self.pol_host.data_ptr(), self.pol.data_ptr(),
                                            self.pol.numel(), N.stream_ptr()), "copy_async")
+            # steps >= t + 2 had their records copied before the previous sync:
+            # turn them into TraceRecords while the device runs this plan
+            if t + 2 <= t_built:
+                self._trace_steps(traces, range(t_built, t + 1, -1))
+                t_built = t + 1
             st.synchronize()
             # the decisions straight from the pinned copy (QcbPolicyVideo.action /
             # .abits as int32 words; ctypes parsing costs ~10 us per video)
@@ -648,6 +658,10 @@ class QuantCacheEngine:
             self._run_step(t, vids, act_tab, abits_of, collect_features, gen)
         if return_device:
             out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
+            st.synchronize()
+            self._trace_steps(traces, range(t_built, -1, -1))
+            for vs, tr in zip(vids, traces):
+                vs.trace = tr
             return out, vids
         # latents to the host: a pinned block from torch's caching host allocator
         # (a new array per call, reused only once the caller drops it) filled by
@@ -656,8 +670,10 @@ class QuantCacheEngine:
         host = torch.empty((nv, S, d), dtype=torch.float32, pin_memory=True)
         for v, vs in enumerate(vids):
             host[v].copy_(self.slot_view(vs.x), non_blocking=True)
-        traces = self._collect_traces(vids)   # its trace read-back follows the copies
         st.synchronize()
+        self._trace_steps(traces, range(t_built, -1, -1))
+        for vs, tr in zip(vids, traces):
+            vs.trace = tr
         return host.numpy().reshape(nv, F, Tk, d), traces
 
     def _plan_step(self, t: int, vids):
@@ -913,26 +929,37 @@ class QuantCacheEngine:
             self._sync_decide(t, vids)
 
     def traces_of(self, vids) -> List[List[TraceRecord]]:
-        return self._collect_traces(vids)
+        return [vs.trace for vs in vids]
 
     def _collect_traces(self, vids) -> List[List[TraceRecord]]:
-        """Per-video TraceRecords (schedule.py:187-210) from the per-step policy
-        records: one structured numpy view of the [T][videos] QcbPolicyVideo
-        array, columns converted to Python lists once (per-record ctypes
-        access cost ~40 ms per 4-video call)."""
+        """Per-video TraceRecords (schedule.py:187-210) of every step, from the
+        per-step policy records in pinned host memory."""
+        traces = [[] for _ in range(len(vids))]
+        self._trace_steps(traces, range(self.T - 1, -1, -1))
+        return traces
+
+    def _trace_steps(self, traces, steps) -> None:
+        """Append the records of `steps` (descending t) to traces[v]: one
+        structured numpy view of those rows of the [T][videos] QcbPolicyVideo
+        array, columns converted to Python lists once (per-record ctypes access
+        cost ~40 ms per 4-video call)."""
+        steps = list(steps)
+        if not steps:
+            return
         gc_was = gc.isenabled()
         gc.disable()   # ~12k new records would trigger collections (+45 ms when one hits gen 2)
         try:
-            return self._collect_traces_impl(vids)
+            self._trace_steps_impl(traces, steps)
         finally:
             if gc_was:
                 gc.enable()
 
-    def _collect_traces_impl(self, vids) -> List[List[TraceRecord]]:
-        nv, L = len(vids), self.L
+    def _trace_steps_impl(self, traces, steps) -> None:
+        nv, L = len(traces), self.L
         npv = 1 if self.sync else nv
-        raw = self.pol_trace[:, :npv * self.pol_size].cpu().numpy()
-        rec = np.ascontiguousarray(raw).view(_policy_dtype()).reshape(self.T, npv)
+        lo, hi = steps[-1], steps[0]
+        raw = self.pol_trace[lo:hi + 1, :npv * self.pol_size].numpy()
+        rec = np.ascontiguousarray(raw).view(_policy_dtype()).reshape(hi + 1 - lo, npv)
         A, DV, DN = rec["action"].tolist(), rec["d_valid"].tolist(), rec["d_now"].tolist()
         SV, SM = rec["sim_valid"].tolist(), rec["sim"].tolist()
         AB, VV = rec["abits"].tolist(), rec["v"].tolist()
@@ -941,12 +968,12 @@ class QuantCacheEngine:
         macs_of: Dict[int, list] = {}   # abits -> billed MACs per layer when recomputed
         rc = N.ACT_RECOMPUTE
         head_macs = self.head_macs * FP_BITS * FP_BITS
-        traces = [[] for _ in range(nv)]
         layers = range(L)
-        for t in range(self.T - 1, -1, -1):
+        for t in steps:
+            k = t - lo
             for v in range(nv):
                 pv = 0 if self.sync else v
-                ab, vf = int(AB[t][pv]), float(VV[t][pv])
+                ab, vf = int(AB[k][pv]), float(VV[k][pv])
                 mt = macs_of.get(ab)
                 if mt is None:
                     mt = macs_of[ab] = [billed_macs(self.block_cost, wb, ab) for wb in wbs]
@@ -954,8 +981,7 @@ class QuantCacheEngine:
                 out.extend([TraceRecord(t, l, ACTION_NAMES[a], dn if dv else None,
                                         sm if sv else None, ab, wb, m if a == rc else 0, vf)
                             for l, a, dv, dn, sv, sm, wb, m in
-                            zip(layers, A[t][pv], DV[t][pv], DN[t][pv], SV[t][pv], SM[t][pv],
+                            zip(layers, A[k][pv], DV[k][pv], DN[k][pv], SV[k][pv], SM[k][pv],
                                 wbs, mt)])
                 out.append(TraceRecord(t, "head", "recompute", None, None, FP_BITS, FP_BITS,
                                        head_macs))
-        return traces

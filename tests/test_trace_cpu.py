@@ -35,6 +35,8 @@ def _fake_engine(T, nv, sync, seed):
         weight_bits={l: 4 + (l % 3) for l in range(L)},
         tog=SimpleNamespace(aigq_weights=True), head_macs=1000,
         block_cost=None)
+    for name in ("_trace_steps", "_trace_steps_impl"):
+        setattr(eng, name, getattr(QuantCacheEngine, name).__get__(eng))
     return eng
 
 
@@ -72,4 +74,24 @@ def test_collect_traces_matches_per_record_reading(monkeypatch, sync):
     got = QuantCacheEngine._collect_traces(eng, [None] * nv)
     want = _reference(eng, nv)
     assert [[r.to_json_obj() for r in tv] for tv in got] == \
+        [[r.to_json_obj() for r in tv] for tv in want]
+
+
+@pytest.mark.parametrize("sync", [False, True])
+def test_incremental_trace_build_matches_full_reading(monkeypatch, sync):
+    """generate() builds finished steps while it waits on each decision sync
+    (steps >= t + 2 at step t, the rest after the loop): same records, same order."""
+    import paper_2503_06545_b200.engine as E
+    monkeypatch.setattr(E, "billed_macs", lambda cost, wb, ab: _macs(wb, ab))
+    nv, T = 2, 7
+    eng = _fake_engine(T=T, nv=nv, sync=sync, seed=2)
+    traces = [[] for _ in range(nv)]
+    t_built = T - 1
+    for t in range(T - 1, -1, -1):
+        if t + 2 <= t_built:
+            eng._trace_steps(traces, range(t_built, t + 1, -1))
+            t_built = t + 1
+    eng._trace_steps(traces, range(t_built, -1, -1))
+    want = _reference(eng, nv)
+    assert [[r.to_json_obj() for r in tv] for tv in traces] == \
         [[r.to_json_obj() for r in tv] for tv in want]
