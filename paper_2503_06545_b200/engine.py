@@ -599,8 +599,10 @@ class QuantCacheEngine:
                             cache=[None] * L, prev=[None] * L)
             vs.x = vs.pool.alloc()
             if x0_dev is not None:
-                self.slot_view(vs.x).copy_(x0_dev[v].reshape(S, d))
-                self.cond[v].copy_(cond_dev[v])
+                # async from pinned host memory (the first decision sync of the
+                # loop orders it before generate() returns); device sources too
+                self.slot_view(vs.x).copy_(x0_dev[v].reshape(S, d), non_blocking=True)
+                self.cond[v].copy_(cond_dev[v], non_blocking=True)
             else:
                 x0 = vs.rng.standard_normal((F, Tk, d)).astype(np.float32)
                 cond = vs.rng.standard_normal(self.c).astype(np.float32)
