@@ -1,28 +1,34 @@
 #!/usr/bin/env python
 """QuantCache B200 benchmark -- prints ONE JSON line (driver contract).
 
-Headline workload (BASELINE.json configs[2], "C3"): STDiT-XL/2 dimensions in the
-reference block (28 blocks, hidden 1152, 16 heads, FFN 4608, cond width 4096),
-16 frames of 256x256 (S = 16 x 16 x 16 = 4096 tokens), 100 DDPM steps with full
-QuantCache (HLC + AIGQ W6 / mixed-bit activations + SRAP), random-init weights,
-synthetic latents.  A bench "step" = one batch of videos sampled end to end.
+Headline workload (BASELINE.json north_star Target): STDiT-XL/2 dimensions in
+the reference block (28 blocks, hidden 1152, 16 heads, FFN 4608, cond width
+4096), 16 frames of 512x512 (S = 16 x 32 x 32 = 16,384 tokens: 8x spatial VAE,
+2x2 patches), 100 DDPM steps with full QuantCache (HLC + AIGQ W6 with
+mixed-bit activations + SRAP), random-init weights, synthetic latents.  A bench
+"step" = one batch of videos sampled end to end (`--workload c3` selects
+BASELINE configs[2], 16 frames 256x256, S = 4096, as the headline instead).
 
-  metric  videos/s (higher is better); s/video is reported alongside
-  roofline  the kernel class with the largest share of a profiled step: the
-          AIGQ activation quantizer (HBM-bound, GB/s vs MEASURED_PEAKS hbm) or
-          the tcgen05 u8 GEMM (TOP/s vs the measured cuBLASLt int8 peak); both
-          are listed under roofline_kernels
-  e2e     the same runs through the engine's public generate() with host
-          latents in and out (H2D/D2H inside the timed region)
+  value     videos/s of the whole job, device-timed (CUDA events, inputs in HBM)
+  e2e       the same metric through the engine's public generate() with pinned
+            host latents in and host latents out (H2D/D2H inside the timed region)
+  roofline  the dominant kernel class of OUR kernels in a profiled step;
+            all classes under roofline_kernels (attention = library bf16 SDPA)
+  lines     secondary measurements at N = 1: the other workload (C3 or target),
+            an all-recompute AIGQ-only run (every block recomputed every step:
+            the quantized block path without HLC/SRAP skipping), the C2 GEMM /
+            quantizer microbench (W8A8 / W6A8 / W4A8 / W4A6 at M = 16,384) and
+            the C1 latency of the reference's tiny configs
 
-Multi-GPU: one process per GPU (torchrun); videos are sharded across ranks
-with no collective in the sampling loop (per-video decisions, reference
-semantics) -> "scaling": "weak"; the timed region is bracketed by barriers and
-the max elapsed over ranks is reported.
+Multi-GPU: one process per GPU.  `--gpus N` re-launches itself under
+torch.distributed.run when WORLD_SIZE is unset.  Videos are sharded across
+ranks with no collective in the sampling loop (per-video decisions, reference
+semantics) -> "scaling": "weak"; barrier + max-over-ranks timing.
 
-`--impl reference` times the CPU oracle restatement of the reference's hot path
-(oracle/qc_oracle.py: quantizer + integer GEMMs of a recomputed block) on a
-bounded row slice, on all host cores, extrapolated to the same metric.
+`--impl reference` times the reference's own CPU implementation (the
+unmodified `ditrt` package installed in baseline/_ref; the oracle port when
+absent) on all host cores: one recomputed block + head + DDPM update on row
+slices, extrapolated to videos/s of the same workload (bench_cpu.py).
 """
 
 from __future__ import annotations
@@ -41,11 +47,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-C3 = dict(num_blocks=28, model_dim=1152, num_heads=16, tokens_per_frame=256, frames=16,
-          cond_dim=4096)
-SITES_KN = {"sta_q": (1152, 1152), "sta_k": (1152, 1152), "sta_v": (1152, 1152),
-            "sta_o": (1152, 1152), "ca_q": (1152, 1152), "ca_o": (1152, 1152),
-            "ffn1": (1152, 4608), "ffn2": (4608, 1152)}
+STDIT = dict(num_blocks=28, model_dim=1152, num_heads=16, cond_dim=4096, frames=16)
+WORKLOADS = {
+    "target": dict(tokens_per_frame=1024, label="north_star Target: STDiT-XL/2 dims (28x1152, "
+                   "16 heads, FFN 4608, cond 4096), 16 frames 512x512 (S=16384), DDPM T=100, "
+                   "full QuantCache"),
+    "c3": dict(tokens_per_frame=256, label="C3: STDiT-XL/2 dims (28x1152, 16 heads, FFN 4608, "
+               "cond 4096), 16 frames 256x256 (S=4096), DDPM T=100, full QuantCache"),
+}
+# Recompute fraction of the full-QuantCache runs, measured by this bench on the
+# B200 (recompute_fraction in BENCH lines); the reference's decisions equal ours
+# (tests/test_gpu_engine.py), so the CPU arm extrapolates with the same fraction.
+RECOMPUTE_FRACTION = {"target": 0.030, "c3": 0.030}
 NOMINAL_INT8_TOPS = 4500.0
 
 
@@ -55,119 +68,102 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="target", choices=sorted(WORKLOADS))
     ap.add_argument("--videos", type=int, default=4, help="videos per GPU per step")
     ap.add_argument("--timesteps", type=int, default=100)
     ap.add_argument("--wbits", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary lines")
     ap.add_argument("--decisions", default="per_video", choices=["per_video", "synchronized"],
                     help="per-video decisions (reference semantics, no collective) or one "
                          "policy for the whole batch (one NCCL all-reduce per step)")
     return ap.parse_args()
 
 
+def model_dims(workload: str) -> dict:
+    w = WORKLOADS[workload]
+    return dict(STDIT, tokens_per_frame=w["tokens_per_frame"])
+
+
 # ---------------------------------------------------------------------------
-# CPU arm: the oracle restatement of the reference's quantized block, on rows
+# CPU arm
 
 
-def _cpu_block_sample(rows: int, seed: int = 0) -> float:
-    """Seconds for the reference algorithm's hot path of ONE recomputed C3 block
-    (per-tensor AIGQ quantizer with the sequential f64 rotation + the 8 large
-    integer-GEMM sites, tensor.py:68-112 / quant.py:83-165) on `rows` rows."""
-    from oracle import qc_oracle as O
-    rng = np.random.default_rng(seed)
-    rot = {}
-    t0 = time.perf_counter()
-    for site, (K, N) in SITES_KN.items():
-        x = rng.standard_normal((rows, K)).astype(np.float32)
-        w = (rng.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32)
-        c = np.ones(K)
-        if K not in rot:
-            rot[K] = O.rotation_dense(K, 0).astype(np.float32)
-        y = (x.astype(np.float64) / c[None, :]).astype(np.float32)
-        xe = O.seq_mm(y, rot[K])
-        sa, za = O.act_params(xe, 8)
-        ca = O.codes_of(xe, sa, za, 8)
-        sw, zw = O.chan_params(w, 6)
-        cw = O.codes_of(w, sw[None], zw[None], 6)
-        O.matmul_int_seq(ca, sa, za, cw, sw, zw)
-    return time.perf_counter() - t0
+def _ref_worker(args):
+    """One core's sample (fork child: the BlockSample was built before fork)."""
+    r1, r2, S, warm = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import bench_cpu
+    s = _SAMPLE[0]
+    if warm:
+        return s.block_seconds(r1), s.head_seconds(r1)
+    fb = bench_cpu.fit_seconds(s.block_seconds, r1, r2, S)
+    fh = bench_cpu.fit_seconds(s.head_seconds, r1, r2, S)
+    return fb, fh
 
 
-def _cpu_head_sample(rows: int, seed: int = 0) -> float:
-    """Seconds for the reference's FP noise head `mm(x, head_w) + head_b`
-    (model.py:228, tensor.py:43-60, sequential f64) on `rows` rows."""
-    from oracle import qc_oracle as O
-    rng = np.random.default_rng(seed)
-    d = C3["model_dim"]
-    x = rng.standard_normal((rows, d)).astype(np.float32)
-    w = (rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)
-    t0 = time.perf_counter()
-    O.seq_mm(x, w)
-    return time.perf_counter() - t0
+_SAMPLE = [None]
+R1, R2 = 4, 16
 
 
-# Recompute fraction of the C3 QuantCache run (the reference's decisions equal
-# ours bit for bit -- tests/test_gpu_engine.py -- so both arms extrapolate with
-# the fraction our calibrated C3 run measures; see DESIGN.md section 6).
-C3_RECOMPUTE_FRACTION = 0.030
-
-
-def _videos_per_s_from_sample(t_block: float, t_head: float, rows: int, S: int, L: int,
-                              T: int, frac: float) -> float:
-    """Per video: T steps x (head + frac x L recomputed blocks), each sample
-    scaled from `rows` rows to S rows."""
-    sec_per_video = (S / rows) * T * (t_head + frac * L * t_block)
-    return 1.0 / sec_per_video
-
-
-def _pool_worker(args):
-    rows, seed = args
-    return _cpu_block_sample(rows, seed) + 0.0, _cpu_head_sample(rows, seed)
+def cpu_sample_line(workload: str, steps: int, warmup: int, cores: int, timesteps: int,
+                    wbits: int) -> dict:
+    """Reference CPU throughput (videos/s) on `cores` processes; each step times
+    one recomputed block + the head + DDPM on R1 and R2 rows per process and
+    extrapolates with the linear fit t(S) = a + b S."""
+    import multiprocessing as mp
+    import bench_cpu
+    dims = model_dims(workload)
+    S = dims["tokens_per_frame"] * dims["frames"]
+    _SAMPLE[0] = bench_cpu.BlockSample(S, dims["model_dim"], dims["num_heads"],
+                                       dims["cond_dim"], wbits=wbits, abits=8)
+    frac = RECOMPUTE_FRACTION[workload]
+    ctx = mp.get_context("fork")
+    rates, step_s = [], []
+    with ctx.Pool(cores) as pool:
+        for _ in range(warmup):
+            pool.map(_ref_worker, [(R1, R2, S, True)] * cores)
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker, [(R1, R2, S, False)] * cores)
+            step_s.append(time.perf_counter() - t0)
+            # every process extrapolates its own per-video time; the job's rate
+            # is the sum over the concurrently running processes
+            rates.append(sum(bench_cpu.videos_per_s(fb["t_S"], fh["t_S"], timesteps,
+                                                    dims["num_blocks"], frac)
+                             for fb, fh in res))
+            last = res
+    fb, fh = last[0]
+    kind = _SAMPLE[0].kind
+    return {
+        "value": statistics.median(rates), "unit": "videos/s", "cores": cores, "kind": kind,
+        "ms_per_step": statistics.median(step_s) * 1e3,
+        "sample": (f"{'ditrt (unmodified reference, baseline/_ref)' if kind == 'reference' else 'oracle port'}: "
+                   f"one recomputed block (10 GEMM sites via QuantRuntime.gemm_fn, _ln, _mha over "
+                   f"all {S} keys, _gelu) and head mm + reverse_step on {R1} and {R2} rows per "
+                   f"process x {cores} processes; per-process fit t(S)=a+b*S "
+                   f"(block a={fb['a']:.2f}s b={fb['b'] * 1e3:.1f}ms/row -> {fb['t_S']:.0f}s, head "
+                   f"{fh['t_S']:.1f}s at S={S}); per video = {timesteps} x (head + {frac} "
+                   f"recompute fraction x {dims['num_blocks']} blocks)"),
+    }
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on all host threads (one process per core,
-    each on its own row slice), extrapolated to videos/s of the C3 workload."""
-    import multiprocessing as mp
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: rank 0 only (other ranks exit without work)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     cores = os.cpu_count() or 1
-    rows = 8
-    S = C3["tokens_per_frame"] * C3["frames"]
-    frac = C3_RECOMPUTE_FRACTION
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        for _ in range(args.warmup):
-            pool.map(_pool_worker, [(rows, i) for i in range(cores)])
-        times = []
-        for k in range(args.steps):
-            t0 = time.perf_counter()
-            res = pool.map(_pool_worker, [(rows, 100 + k * cores + i) for i in range(cores)])
-            wall = time.perf_counter() - t0
-            # split the wall time of the parallel sample by the per-core shares
-            tb = statistics.mean(r[0] for r in res)
-            th = statistics.mean(r[1] for r in res)
-            times.append((wall * tb / (tb + th), wall * th / (tb + th)))
-    t_block = statistics.median(t[0] for t in times)
-    t_head = statistics.median(t[1] for t in times)
-    step = t_block + t_head
-    # cores row-slices of `rows` rows each finished in `step` seconds
-    vps = _videos_per_s_from_sample(t_block, t_head, rows * cores, S, C3["num_blocks"],
-                                    args.timesteps, frac)
+    c = cpu_sample_line(args.workload, args.steps, args.warmup, cores, args.timesteps,
+                        args.wbits)
     line = {
-        "impl": "reference", "metric": "videos_per_s", "value": vps, "unit": "videos/s",
+        "impl": "reference", "metric": "videos_per_s", "value": c["value"], "unit": "videos/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "C3 STDiT-XL/2 16x256^2 T=100 (CPU oracle sample)",
-                   "timesteps": args.timesteps},
-        "cpu_baseline": {"value": vps, "unit": "videos/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle quantizer + 8 int GEMM sites of one C3 block and the "
-                                   f"f64 noise head on {rows} rows per core x {cores} cores, "
-                                   f"extrapolated x{S}/rows x {args.timesteps} steps x (head + "
-                                   f"{frac} recompute fraction x 28 blocks); attention excluded"},
-        "e2e": {"value": vps, "unit": "videos/s", "h2d_bytes_per_step": 0,
+        "ms_per_step": c["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic latents, random-init weights",
+        "config": {"workload": WORKLOADS[args.workload]["label"] + " (CPU reference sample)",
+                   "timesteps": args.timesteps, "weight_bits": args.wbits},
+        "cpu_baseline": {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": c["value"], "unit": "videos/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -223,14 +219,17 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def _measured_hbm() -> dict:
-    """HBM copy bandwidth from the driver-written MEASURED_PEAKS.json."""
+def _peaks() -> dict:
+    """Roofline denominators from the driver-written MEASURED_PEAKS.json."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return {"gbs": float(json.load(f)["hbm_gbs"]),
-                    "source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+            p = json.load(f)
+        return {"hbm": float(p["hbm_gbs"]), "bf16": float(p["bf16_tflops"]),
+                "bf16_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                "source": "MEASURED_PEAKS.json"}
     except Exception:
-        return {"gbs": 7700.0, "source": "nominal 7.7 TB/s (MEASURED_PEAKS.json absent)"}
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"}
 
 
 def _ncu_traffic() -> dict:
@@ -267,10 +266,9 @@ def measured_int8_peak(torch) -> dict:
         return {"tops": None, "source": f"unavailable: {type(exc).__name__}"}
 
 
-def fast_model(torch, cfg):
-    """Random-init weights of the C3 architecture (N(0, fan_in^-1/2), like
-    init_model) drawn with NumPy's float32 normal generator for speed; C3 has no
-    CPU oracle so the reference draw order is not needed here."""
+def fast_model(cfg):
+    """Random-init weights of the STDiT-XL/2 block architecture (N(0, fan_in^-1/2),
+    like init_model) drawn with NumPy's float32 normal generator for speed."""
     from paper_2503_06545_b200.model import BlockWeights, DiTModel, _shapes
     rng = np.random.default_rng(cfg.seed)
     blocks = []
@@ -290,242 +288,460 @@ def fast_model(torch, cfg):
                     rng.standard_normal(d, dtype=np.float32) * np.float32(d ** -0.5))
 
 
-def run_ours(args):
-    import torch
+# sites that read the same activation tensor share its calibration statistics
+_INPUT_OF = {"sta_q": "h1", "sta_k": "h1", "sta_v": "h1", "sta_o": "att", "ca_q": "h2",
+             "ca_k": "cond", "ca_v": "cond", "ca_o": "ca", "ffn1": "h3", "ffn2": "hid"}
+
+
+def synthetic_absmax(model, seed: int = 0):
+    """Per-(layer, site) channel |x| maxima standing in for harness.calibrate's
+    (harness.py:305-311): one log-normal vector per block INPUT tensor, shared by
+    the sites that read it, so every site gets its own balance scales
+    c_j = sqrt(absmax_x / absmax_w) (quant.py:179-200) and the q/k/v quantizer
+    emits three different rotations of h1, as with a real calibration."""
+    rng = np.random.default_rng(seed)
+    out = {}
+    for l, b in enumerate(model.blocks):
+        per_input = {}
+        out[l] = {}
+        for site, inp in _INPUT_OF.items():
+            K = getattr(b, site).shape[0]
+            if inp not in per_input:
+                per_input[inp] = 4.0 * np.exp(0.5 * rng.standard_normal(K))
+            out[l][site] = per_input[inp]
+    return out
+
+
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def _agg(prof):
+    tot_work, tot_t, sites = 0, 0.0, {}
+    for e_s, e_e, work, site in prof:
+        dt = e_s.elapsed_time(e_e) / 1e3
+        tot_work += work
+        tot_t += dt
+        a = sites.setdefault(site, [0, 0.0, 0])
+        a[0] += work
+        a[1] += dt
+        a[2] += 1
+    return tot_work, tot_t, sites
+
+
+def profile_call(torch, eng, seeds, x0, cond, S, d, H, int8_peak, peaks, traffic):
+    """One generate() with CUDA events around every quantizer call, every u8 GEMM
+    and every other phase (attention, GELU, head, plan, HLC, sampler): per
+    kernel-class time, achieved rate and roofline fraction."""
+    eng.gemm_profile, eng.quant_profile, eng.phase_profile, eng.host_profile = [], [], [], []
+    eng.head_fallbacks.zero_()
+    eng.att_flops = 0.0
+    p0, p1 = _events(torch)
+    p0.record()
+    eng.generate(seeds, x0_dev=x0, cond_dev=cond, return_device=True)
+    p1.record()
+    torch.cuda.synchronize()
+    step = p0.elapsed_time(p1) / 1e3
+    g_ops, g_time, per_site = _agg(eng.gemm_profile)
+    q_bytes, q_time, q_sites = _agg(eng.quant_profile)
+    phases = {"act_quant": q_time * 1e3, "gemm_u8": g_time * 1e3}
+    for name, e_s, e_e in eng.phase_profile:
+        phases[name] = phases.get(name, 0.0) + e_s.elapsed_time(e_e)
+    phases["other_and_gaps"] = step * 1e3 - sum(phases.values())
+    host_loop_ms = sum(h[0] for h in eng.host_profile) * 1e3
+    nv = len(seeds)
+    head_fb = int(eng.head_fallbacks.item()) / float(eng.T * nv * S * d)
+    att_flops = eng.att_flops
+    eng.att_flops = 0.0
+    eng.gemm_profile = eng.quant_profile = eng.phase_profile = eng.host_profile = None
+    peak_tops = int8_peak.get("tops") or NOMINAL_INT8_TOPS
+    tops = g_ops / g_time / 1e12 if g_time > 0 else None
+    qgbs = q_bytes / q_time / 1e9 if q_time > 0 else None
+    kern = {
+        "act_quant": {
+            "bound": "hbm", "achieved": qgbs, "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": (qgbs / peaks["hbm"]) if qgbs else None,
+            "traffic": traffic.get("act_quant"),
+            "kernel": "act_quant (aq4_pass1 + aq2_pass2_hot + init_keys)",
+            "peak_source": peaks["source"] + " hbm_gbs (burst copy)",
+            "share_of_step": q_time / step if step else None,
+            "algorithmic": "4*M_valid*K (f32 read) + n_out*M_valid*K (u8 codes) bytes per call",
+            "per_site": {s: {"gbs": a[0] / a[1] / 1e9, "launches": a[2], "ms_total": a[1] * 1e3}
+                         for s, a in q_sites.items()}},
+        "gemm_u8": {
+            "bound": "tensor", "achieved": tops, "peak": peak_tops, "unit": "TOP/s",
+            "frac": (tops / peak_tops) if tops else None,
+            "traffic": traffic.get("gemm_u8_tcgen05"),
+            "kernel": "gemm_u8_tcgen05 (+ gemm_u8_small_m for the cond token)",
+            "peak_source": int8_peak.get("source"), "nominal_int8_dense_tops": NOMINAL_INT8_TOPS,
+            "share_of_step": g_time / step if step else None,
+            "algorithmic": "2*M_valid*N*K ops per launch",
+            "per_site": {s: {"tops": a[0] / a[1] / 1e12, "launches": a[2], "ms_total": a[1] * 1e3}
+                         for s, a in per_site.items()}},
+    }
+    att_ms = phases.get("attention", 0.0)
+    if att_ms > 0 and att_flops > 0:
+        tf = att_flops / (att_ms / 1e3) / 1e12
+        kern["attention"] = {
+            "bound": "tensor", "achieved": tf, "peak": peaks["bf16"], "unit": "TFLOP/s",
+            "frac": tf / peaks["bf16"], "library": "cuDNN SDPA via torch (bf16), not ours",
+            "peak_source": peaks["source"] + " bf16_tflops (burst cuBLAS)",
+            "share_of_step": att_ms / 1e3 / step,
+            "algorithmic": "4*S^2*d flops per recomputed block per video (QK^T + PV)"}
+    return step, {k: round(v, 3) for k, v in phases.items()}, kern, host_loop_ms, head_fb
+
+
+def _rank_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def _calibrated_thresholds(torch, model, sched, wbits, absmax, T):
+    """Threshold calibration pass (harness.py:319-345 on the quantized path):
+    every block recomputed (HLC with delta = 0), D/V recorded, delta = p33/p66 of
+    D, v = p25/p75 of V.  The same calibration video on every rank."""
+    from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
+    from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles
+    tog_cal = Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=False)
+    eng = QuantCacheEngine(model, sched.alpha_bar, tog_cal,
+                           ThresholdConfig(delta1=0.0, delta2=0.0), wbits, absmax,
+                           sign_seed=0, prune_seed=0, max_videos=1,
+                           options=EngineOptions(attention="fast", noise="device"))
+    _, tr = eng.generate([1000])
+    ds = [r.d for r in tr[0] if r.d is not None]
+    vs = [r.v for r in tr[0] if r.layer == 0 and r.v is not None and r.v > 0]
+    del eng
+    torch.cuda.empty_cache()
+    return ThresholdConfig(delta1=float(np.percentile(ds, 33)),
+                           delta2=float(np.percentile(ds, 66)),
+                           v_low=float(np.percentile(vs, 25)), v_high=float(np.percentile(vs, 75)))
+
+
+def run_workload(torch, args, workload, model, absmax, *, world, rank, local, int8_peak,
+                 peaks, traffic, headline):
+    """Full-QuantCache videos/s of one workload (device-timed), its profiled
+    step and (headline only) the e2e run through the public generate()."""
     import torch.distributed as dist
     from paper_2503_06545_b200 import device as Dv
     from paper_2503_06545_b200 import dist as qdist
     from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
-    from paper_2503_06545_b200.model import DiTConfig
     from paper_2503_06545_b200.sampler import linear_beta_schedule
-    from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2503_06545_b200.schedule import Toggles
+    cfg = model.cfg
     B, T = args.videos, args.timesteps
-    cfg = DiTConfig(seed=0, **C3)
     S, d = cfg.seq_len, cfg.model_dim
-    model = fast_model(torch, cfg)
-    # Synthetic calibration (no reference calibration exists at this size):
-    # activation absmax := weight row absmax gives balance scales c == 1 while the
-    # randomized Hadamard rotation stays on (quant.py:179-200).
-    absmax = {l: {s: np.abs(getattr(b, s)).max(axis=1).astype(np.float64)
-                  for s in ("sta_q", "sta_k", "sta_v", "sta_o", "ca_q", "ca_k", "ca_v",
-                            "ca_o", "ffn1", "ffn2")}
-              for l, b in enumerate(model.blocks)}
     wbits = {l: args.wbits for l in range(cfg.num_blocks)}
     sched = linear_beta_schedule(T)
-    opts = EngineOptions(attention="fast", noise="device")
-    # Threshold calibration pass (harness.py:319-345 procedure on the quantized
-    # path): every block recomputed, D/V recorded, delta = p33/p66, v = p25/p75.
-    tog_cal = Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=False)
-    th0 = ThresholdConfig(delta1=0.0, delta2=0.0)
-    eng = QuantCacheEngine(model, sched.alpha_bar, tog_cal, th0, wbits, absmax, sign_seed=0,
-                           prune_seed=0, max_videos=B, options=opts)
-    # the same calibration video on every rank: one threshold set for the job
-    _, tr = eng.generate([1000], device_noise_seed=1000)
-    ds = [r.d for r in tr[0] if r.d is not None]
-    vs = [r.v for r in tr[0] if r.layer == 0 and r.v is not None and r.v > 0]
-    th = ThresholdConfig(delta1=float(np.percentile(ds, 33)), delta2=float(np.percentile(ds, 66)),
-                         v_low=float(np.percentile(vs, 25)), v_high=float(np.percentile(vs, 75)))
-    del eng
-    torch.cuda.empty_cache()
+    th = _calibrated_thresholds(torch, model, sched, wbits, absmax, T)
     tog = Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=True)
-    opts = EngineOptions(attention="fast", noise="device", decisions=args.decisions)
+    opts = EngineOptions(attention="fast", noise="device",
+                         decisions=args.decisions if headline else "per_video")
     eng = QuantCacheEngine(model, sched.alpha_bar, tog, th, wbits, absmax, sign_seed=0,
                            prune_seed=0, max_videos=B, options=opts)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(7 + rank)
     x0 = torch.randn((B, S, d), device="cuda", generator=gen)
     cond = torch.randn((B, cfg.cond_dim), device="cuda", generator=gen)
-    # video sharding: global video ids of this rank for bench step k (weak scaling:
-    # B videos per GPU per step), seeds follow the video id
+    # video sharding: the global video ids of this rank for bench step k (weak
+    # scaling: B videos per GPU per step); a video's seed follows its id
     seeds = lambda k: qdist.video_seeds(qdist.shard_videos(B * world, world, rank), 1_000 * k)
-    for k in range(args.warmup):
-        eng.generate(seeds(k), device_noise_seed=k, x0_dev=x0, cond_dev=cond,
-                     return_device=True)
+    n_steps, n_warm = (args.steps, args.warmup) if headline else (max(2, min(args.steps, 3)), 1)
+    for k in range(n_warm):
+        eng.generate(seeds(k), x0_dev=x0, cond_dev=cond, return_device=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks = ClockSampler(local) if headline else None
+    if clocks:
+        clocks.start()
     launches0 = Dv.LAUNCHES[0]
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0, e1 = _events(torch)
     torch.cuda.synchronize()
     # QC_PROFILE_RANGE=1: open the CUDA profiler range around the timed steps only,
     # so `ncu --profile-from-start off` lists exactly the timed region's launches
-    prof_range = os.environ.get("QC_PROFILE_RANGE") == "1"
+    prof_range = headline and os.environ.get("QC_PROFILE_RANGE") == "1"
     if prof_range:
         torch.cuda.cudart().cudaProfilerStart()
-    e0.record(stream)
+    e0.record()
     vids_all = []
-    for k in range(args.steps):
-        _, vids = eng.generate(seeds(args.warmup + k), device_noise_seed=args.warmup + k,
-                               x0_dev=x0, cond_dev=cond, return_device=True)
+    for k in range(n_steps):
+        _, vids = eng.generate(seeds(n_warm + k), x0_dev=x0, cond_dev=cond, return_device=True)
         vids_all.append(vids)
-    e1.record(stream)
+    e1.record()
     torch.cuda.synchronize()
     if prof_range:
         torch.cuda.cudart().cudaProfilerStop()
     elapsed = e0.elapsed_time(e1) / 1e3
     launches = Dv.LAUNCHES[0] - launches0
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
     if world > 1:
         dist.barrier()
     elapsed = qdist.max_over_ranks(elapsed, device="cuda")
-    # recompute fraction / decisions of the timed runs
     traces = [eng.traces_of(v) for v in vids_all]
     recs = [r for trs in traces for tv in trs for r in tv if r.layer != "head"]
     frac = sum(r.action == "recompute" for r in recs) / max(1, len(recs))
     prune_frac = sum(r.action == "prune" for r in recs) / max(1, len(recs))
-    # SRAP similarities evaluated (one reduction segment each) per video-step
-    srap_per_step = sum(r.s is not None for r in recs) / max(1, len(recs) / cfg.num_blocks)
     executed = sum(r.macs for trs in traces for tv in trs for r in tv)
-    # Kernel rooflines from one extra, separately profiled step (CUDA events
-    # around every u8 GEMM and every quantizer call on the engine's stream), so
-    # the timed region above carries no per-launch events.
-    eng.gemm_profile, eng.quant_profile, eng.phase_profile, eng.host_profile = [], [], [], []
-    eng.head_fallbacks.zero_()
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    eng.generate(seeds(900), device_noise_seed=900, x0_dev=x0, cond_dev=cond, return_device=True)
-    p1.record(stream)
-    torch.cuda.synchronize()
-    prof_step = p0.elapsed_time(p1) / 1e3
-    gprof, qprof, pprof = eng.gemm_profile, eng.quant_profile, eng.phase_profile
-    host_loop_ms = sum(h[0] for h in eng.host_profile) * 1e3
-    host_first_launch_ms = sum(h[1] for h in eng.host_profile) * 1e3
-    eng.host_profile = None
-    head_fb = int(eng.head_fallbacks.item()) / float(T * B * S * d)
-    eng.gemm_profile = eng.quant_profile = eng.phase_profile = None
-
-    def _agg(prof):
-        tot_work, tot_t, sites = 0, 0.0, {}
-        for e_s, e_e, work, site in prof:
-            dt = e_s.elapsed_time(e_e) / 1e3
-            tot_work += work
-            tot_t += dt
-            a = sites.setdefault(site, [0, 0.0, 0])
-            a[0] += work
-            a[1] += dt
-            a[2] += 1
-        return tot_work, tot_t, sites
-
-    g_ops, g_time, per_site = _agg(gprof)
-    q_bytes, q_time, q_sites = _agg(qprof)
-    phases = {"act_quant": q_time * 1e3, "gemm_u8": g_time * 1e3}
-    for name, e_s, e_e in pprof:
-        phases[name] = phases.get(name, 0.0) + e_s.elapsed_time(e_e)
-    phases["other_and_gaps"] = prof_step * 1e3 - sum(phases.values())
-    phases = {k: round(v, 3) for k, v in phases.items()}
-    peak = measured_int8_peak(torch) if rank == 0 else {"tops": None}
-    # e2e through the public API (host latents in, host latents out)
-    e2e_vps = None
-    h2d = B * (S * d + cfg.cond_dim) * 4
-    d2h = B * S * d * 4
-    if rank == 0:
-        # the step's inputs live in pinned host memory: generate() copies them in
-        # (H2D inside the timed region) and returns the latents on the host (D2H)
-        x0_host = torch.randn((B, S, d), generator=torch.Generator().manual_seed(11)).pin_memory()
-        cond_host = torch.randn((B, cfg.cond_dim),
-                                generator=torch.Generator().manual_seed(12)).pin_memory()
-        eng.generate(seeds(499), device_noise_seed=499, x0_dev=x0_host, cond_dev=cond_host)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            eng.generate(seeds(500 + k), device_noise_seed=500 + k, x0_dev=x0_host,
-                         cond_dev=cond_host)
-        torch.cuda.synchronize()
-        e2e_vps = args.steps * B * world / (time.perf_counter() - t0)
-    value = args.steps * B * world / elapsed
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        rows = 4
-        ts = _cpu_block_sample(rows, 0)
-        th_ = _cpu_head_sample(rows, 0)
-        # the same constant fraction as the reference arm (the measured one of this
-        # run is reported as recompute_fraction)
-        cf = C3_RECOMPUTE_FRACTION
-        cpu = {"value": _videos_per_s_from_sample(ts, th_, rows, S, cfg.num_blocks, T, cf),
-               "unit": "videos/s", "cores": 1, "kind": "port",
-               "sample": f"oracle quantizer + 8 int GEMM sites of one C3 block ({ts:.1f} s) and "
-                         f"the f64 noise head ({th_:.2f} s) on {rows} rows, extrapolated "
-                         f"x{S}/{rows} rows x {T} steps x (head + recompute fraction {cf:.3f} "
-                         f"x 28 blocks); attention excluded"}
-    tops = g_ops / g_time / 1e12 if g_time > 0 else None
-    peak_tops = peak.get("tops") or NOMINAL_INT8_TOPS
-    hbm = _measured_hbm()
-    traffic = _ncu_traffic()
-    roof_gemm = {"bound": "tensor", "achieved": tops, "peak": peak_tops, "unit": "TOP/s",
-                 "frac": (tops / peak_tops) if tops else None,
-                 "traffic": traffic.get("gemm_u8_tcgen05"),
-                 "kernel": "gemm_u8_tcgen05 (+ gemm_u8_small_m for the cond token)",
-                 "peak_source": peak.get("source"), "nominal_int8_dense_tops": NOMINAL_INT8_TOPS,
-                 "share_of_step": g_time / prof_step if prof_step else None,
-                 "algorithmic": "2*M_valid*N*K ops per launch",
-                 "per_site": {s: {"tops": a[0] / a[1] / 1e12, "launches": a[2],
-                                  "ms_total": a[1] * 1e3} for s, a in per_site.items()}}
-    qgbs = q_bytes / q_time / 1e9 if q_time > 0 else None
-    roof_quant = {"bound": "hbm", "achieved": qgbs, "peak": hbm["gbs"], "unit": "GB/s",
-                  "frac": (qgbs / hbm["gbs"]) if qgbs else None,
-                  "traffic": traffic.get("act_quant"),
-                  "kernel": "act_quant (aq4_pass1 + aq2_pass2 + init_keys)",
-                  "peak_source": hbm["source"],
-                  "share_of_step": q_time / prof_step if prof_step else None,
-                  "algorithmic": "4*M_valid*K (f32 read) + n_out*M_valid*K (u8 codes) bytes "
-                                 "per call",
-                  "per_site": {s: {"gbs": a[0] / a[1] / 1e9, "launches": a[2],
-                                   "ms_total": a[1] * 1e3} for s, a in q_sites.items()}}
-    dominant = roof_quant if q_time >= g_time else roof_gemm
-    line = {
-        "metric": "videos_per_s", "value": value, "unit": "videos/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic latents, random-init weights",
-        "config": {"workload": "C3: STDiT-XL/2 dims (28x1152, 16 heads, FFN 4608, cond 4096), "
-                               "16 frames 256x256 (S=4096), DDPM T=100, full QuantCache",
-                   "videos_per_gpu_per_step": B, "timesteps": T, "weight_bits": args.wbits,
-                   "parallelism": f"video-sharded x{world}" + (
-                       ", synchronised decisions (1 NCCL all-reduce of 1.1 KB per step)"
-                       if args.decisions == "synchronized" else ", per-video decisions"),
-                   "decisions": args.decisions, "attention": "bf16 SDPA (library)",
-                   "noise": "device Philox", "l2": "inputs > L2 (activation arena "
-                   f"{eng.arena.numel() * 4 / 2**30:.1f} GiB)",
-                   "thresholds": {"delta1": th.delta1, "delta2": th.delta2,
-                                  "v_low": th.v_low, "v_high": th.v_high}},
-        "s_per_video": elapsed / (args.steps * B),
-        "recompute_fraction": frac,
-        "prune_fraction": prune_frac,
-        "srap_segments_per_video_step": srap_per_step,
-        "executed_bit_macs_per_video": executed / (args.steps * B),
-        "roofline": dominant,
-        "roofline_kernels": {"act_quant": roof_quant, "gemm_u8": roof_gemm},
-        "profiled_step_ms": {"total": round(prof_step * 1e3, 3), **phases},
-        "head_exact_fallback_fraction": head_fb,
-        "host_block_loop_ms": round(host_loop_ms, 3),
-        "host_sync_to_first_launch_ms": round(host_first_launch_ms, 3),
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e_vps, "unit": "videos/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-        "clocks": clk,
+    out = {
+        "value": n_steps * B * world / elapsed, "unit": "videos/s",
+        "ms_per_step": elapsed / n_steps * 1e3, "s_per_video": elapsed / (n_steps * B),
+        "steps": n_steps, "warmup": n_warm, "videos_per_gpu_per_step": B,
+        "recompute_fraction": frac, "prune_fraction": prune_frac,
+        "executed_bit_macs_per_video": executed / (n_steps * B), "gpu_launches": launches,
+        "thresholds": {"delta1": th.delta1, "delta2": th.delta2, "v_low": th.v_low,
+                       "v_high": th.v_high},
+        "arena_gib": round(eng.arena.numel() * 4 / 2 ** 30, 2),
     }
-    print(json.dumps(line), flush=True)
+    if clk:
+        out["clocks"] = clk
+    step, phases, kern, host_ms, head_fb = profile_call(
+        torch, eng, seeds(900), x0, cond, S, d, cfg.num_heads, int8_peak, peaks, traffic)
+    out.update({"profiled_call_ms": round(step * 1e3, 3), "profiled_step_ms": phases,
+                "roofline_kernels": kern, "host_block_loop_ms": round(host_ms, 3),
+                "head_exact_fallback_fraction": head_fb})
+    if headline:
+        # e2e through the public API on every rank: the step's inputs live in
+        # pinned host memory, generate() copies them in (H2D inside the timed
+        # region) and returns the latents on the host (D2H); max over ranks
+        g = torch.Generator().manual_seed(11 + rank)
+        x0_host = torch.randn((B, S, d), generator=g).pin_memory()
+        cond_host = torch.randn((B, cfg.cond_dim), generator=g).pin_memory()
+        eng.generate(seeds(499), x0_dev=x0_host, cond_dev=cond_host)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(n_steps):
+            eng.generate(seeds(500 + k), x0_dev=x0_host, cond_dev=cond_host)
+        torch.cuda.synchronize()
+        wall = qdist.max_over_ranks(time.perf_counter() - t0, device="cuda")
+        out["e2e"] = {"value": n_steps * B * world / wall, "unit": "videos/s",
+                      "h2d_bytes_per_step": B * (S * d + cfg.cond_dim) * 4,
+                      "d2h_bytes_per_step": B * S * d * 4}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+def all_recompute_line(torch, args, model, absmax, int8_peak, peaks, traffic):
+    """AIGQ only (HLC/SRAP off): every block of every step recomputed through
+    the quantizer + u8 GEMM path, 1 video, T steps (device-timed, + a profiled
+    call for the per-kernel-class breakdown)."""
+    from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
+    from paper_2503_06545_b200.sampler import linear_beta_schedule
+    from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles
+    cfg = model.cfg
+    S, d, T = cfg.seq_len, cfg.model_dim, args.timesteps
+    sched = linear_beta_schedule(T)
+    wbits = {l: args.wbits for l in range(cfg.num_blocks)}
+    eng = QuantCacheEngine(model, sched.alpha_bar,
+                           Toggles(hlc=False, aigq_weights=True, aigq_acts=True, srap=False),
+                           ThresholdConfig(), wbits, absmax, sign_seed=0, prune_seed=0,
+                           max_videos=1, options=EngineOptions(attention="fast", noise="device"))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    x0 = torch.randn((1, S, d), device="cuda", generator=gen)
+    cond = torch.randn((1, cfg.cond_dim), device="cuda", generator=gen)
+    eng.generate([1], x0_dev=x0, cond_dev=cond, return_device=True)
+    torch.cuda.synchronize()
+    e0, e1 = _events(torch)
+    e0.record()
+    eng.generate([2], x0_dev=x0, cond_dev=cond, return_device=True)
+    e1.record()
+    torch.cuda.synchronize()
+    el = e0.elapsed_time(e1) / 1e3
+    step, phases, kern, host_ms, _ = profile_call(torch, eng, [3], x0, cond, S, d,
+                                                  cfg.num_heads, int8_peak, peaks, traffic)
+    del eng
+    torch.cuda.empty_cache()
+    blocks = cfg.num_blocks * T
+    return {"workload": f"AIGQ only (W{args.wbits}A8, HLC/SRAP off: all {cfg.num_blocks} blocks "
+                        f"recomputed at every one of {T} steps), S={S}, 1 video",
+            "value": 1.0 / el, "unit": "videos/s", "s_per_video": el,
+            "ms_per_block": el / blocks * 1e3, "profiled_call_ms": round(step * 1e3, 3),
+            "profiled_step_ms": phases, "roofline_kernels": kern}
+
+
+def c2_microbench(torch, int8_peak, peaks):
+    """BASELINE configs[1] (C2): the AIGQ quantized linear at M = 16,384 tokens
+    (one 16-frame 512^2 video), K,N in {1152, 4608}: quantizer (rotation +
+    per-tensor params + codes, no prologue) GB/s and tcgen05 u8 GEMM TOP/s, for
+    W8A8 / W6A8 / W4A8 / W4A6.  Each launch is timed alone with CUDA events on
+    its stream after a 256 MiB write that flushes L2."""
+    from paper_2503_06545_b200 import device as Dv
+    M = 16384
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    rng = torch.Generator(device="cuda")
+    rng.manual_seed(0)
+    res = {}
+    reps = 5
+
+    def timed(fn):
+        ts = []
+        for i in range(reps + 1):
+            flush.fill_(i & 0xFF)
+            e0, e1 = _events(torch)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+        return statistics.median(ts)
+
+    peak_tops = int8_peak.get("tops") or NOMINAL_INT8_TOPS
+    for K, Nn in ((1152, 1152), (1152, 4608), (4608, 1152)):
+        x = torch.randn((M, K), device="cuda", generator=rng)
+        w = torch.randn((K, Nn), device="cuda", generator=rng) / K ** 0.5
+        c = torch.exp(0.5 * torch.randn(K, device="cuda", generator=rng, dtype=torch.float64))
+        signs = torch.as_tensor(Dv.sign_vector(0, Dv.pow2_floor(K))).cuda()
+        for wb, ab in ((8, 8), (6, 8), (4, 8), (4, 6)):
+            pw = Dv.weight_prep(w, wb, c, signs)
+            tr = [(pw.chan_scale, pw.signs, pw.chan_recip)]
+            (a,) = Dv.act_quant(x, ab, tr)
+            out = torch.empty((M, Nn), dtype=torch.float32, device="cuda")
+            tq = timed(lambda: Dv.act_quant(x, ab, tr, out=[a]))
+            tg = timed(lambda: Dv.gemm_u8(a, pw, out=out))
+            tops = 2.0 * M * Nn * K / tg / 1e12
+            gbs = (4 + 1) * M * K / tq / 1e9
+            res[f"K{K}_N{Nn}_W{wb}A{ab}"] = {
+                "gemm_us": round(tg * 1e6, 2), "gemm_tops": round(tops, 1),
+                "gemm_frac_int8_peak": round(tops / peak_tops, 4),
+                "quant_us": round(tq * 1e6, 2), "quant_gbs": round(gbs, 1),
+                "quant_frac_hbm": round(gbs / peaks["hbm"], 4)}
+        del x, w
+    del flush
+    torch.cuda.empty_cache()
+    return {"workload": "C2: quantized linear at M=16384, (K,N) in {(1152,1152),(1152,4608),"
+                        "(4608,1152)}, weights per-channel, activations per-tensor with the "
+                        "balance/rotation transform; L2 flushed before every timed launch",
+            "int8_peak_tops": peak_tops, "int8_peak_source": int8_peak.get("source"),
+            "hbm_peak_gbs": peaks["hbm"], "results": res}
+
+
+def c1_latency(torch):
+    """BASELINE configs[0] (C1): the reference's tiny configs (small seed 3,
+    default seed 7) with full QuantCache and the reference's calibration, exact
+    mode (f64-softmax attention, NumPy noise): wall ms per sampling step through
+    harness.run_single."""
+    from paper_2503_06545_b200 import harness
+    golden = os.path.join(ROOT, "tests", "golden")
+    small = {"seed": 3, "model": {"num_blocks": 3, "model_dim": 16, "num_heads": 2,
+                                  "tokens_per_frame": 4, "frames": 2, "cond_dim": 8},
+             "schedule": {"steps": 10}, "calibration": os.path.join(golden, "calib_small.json")}
+    default = {"seed": 7, "calibration": os.path.join(golden, "calib_default.json")}
+    out = {}
+    full = {"hlc": True, "aigq_weights": True, "aigq_acts": True, "srap": True}
+    for name, obj in (("small", small), ("default", default)):
+        cfg = harness.parse_config(dict(obj, toggles=full))
+        calib = harness.load_calibration(cfg.calibration)
+        harness.run_single(cfg, cfg.toggles_obj(), calib)
+        walls = [harness.run_single(cfg, cfg.toggles_obj(), calib).wall_ms for _ in range(3)]
+        T = cfg.noise_schedule().steps
+        out[name] = {"ms_per_run": round(statistics.median(walls), 3),
+                     "us_per_step": round(statistics.median(walls) / T * 1e3, 1), "steps": T}
+    return {"workload": "C1: reference tiny configs, full QuantCache, exact mode "
+                        "(bit-identical to the reference), wall time through run_single "
+                        "(includes engine-internal host work; excludes engine construction)",
+            "results": out}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_06545_b200.model import DiTConfig, DiTModel
+
+    world, rank, local = _rank_env()
+    torch.cuda.set_device(local)
     if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = _peaks()
+    traffic = _ncu_traffic()
+    int8_peak = measured_int8_peak(torch) if rank == 0 else {"tops": None}
+    cfg = DiTConfig(seed=0, **model_dims(args.workload))
+    model = fast_model(cfg)
+    absmax = synthetic_absmax(model)
+    head = run_workload(torch, args, args.workload, model, absmax, world=world, rank=rank,
+                        local=local, int8_peak=int8_peak, peaks=peaks, traffic=traffic,
+                        headline=True)
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra["all_recompute"] = all_recompute_line(torch, args, model, absmax, int8_peak,
+                                                    peaks, traffic)
+        other = "c3" if args.workload == "target" else "target"
+        # the same block weights: only the token count S differs
+        m2 = DiTModel(DiTConfig(seed=0, **model_dims(other)), model.blocks, model.head_w,
+                      model.head_b)
+        o = run_workload(torch, args, other, m2, absmax, world=1, rank=0, local=local,
+                         int8_peak=int8_peak, peaks=peaks, traffic=traffic, headline=False)
+        extra[other] = dict({"workload": WORKLOADS[other]["label"]}, **o)
+        extra["c2_gemm"] = c2_microbench(torch, int8_peak, peaks)
+        extra["c1_latency"] = c1_latency(torch)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        c = cpu_sample_line(args.workload, 1, 0, 1, args.timesteps, args.wbits)
+        cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        kern = head["roofline_kernels"]
+        ours = {k: v for k, v in kern.items() if k in ("act_quant", "gemm_u8")}
+        dominant = max(ours.values(), key=lambda r: r.get("share_of_step") or 0.0)
+        line = {
+            "metric": "videos_per_s", "value": head["value"], "unit": "videos/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic latents, random-init weights",
+            "config": {"workload": WORKLOADS[args.workload]["label"],
+                       "videos_per_gpu_per_step": args.videos, "timesteps": args.timesteps,
+                       "weight_bits": args.wbits,
+                       "parallelism": f"video-sharded x{world}" + (
+                           ", synchronised decisions (1 NCCL all-reduce of 1.1 KB per step)"
+                           if args.decisions == "synchronized" else ", per-video decisions"),
+                       "decisions": args.decisions, "attention": "bf16 SDPA (library)",
+                       "noise": "device Philox keyed by each video's seed",
+                       "calibration": "synthetic per-input channel absmax (log-normal), "
+                                      "thresholds from a device calibration pass",
+                       "l2": f"inputs > L2 (activation arena {head['arena_gib']} GiB per GPU)",
+                       "thresholds": head["thresholds"]},
+            "s_per_video": head["s_per_video"],
+            "recompute_fraction": head["recompute_fraction"],
+            "prune_fraction": head["prune_fraction"],
+            "executed_bit_macs_per_video": head["executed_bit_macs_per_video"],
+            "roofline": dominant,
+            "roofline_kernels": kern,
+            "profiled_step_ms": head["profiled_step_ms"],
+            "profiled_call_ms": head["profiled_call_ms"],
+            "head_exact_fallback_fraction": head["head_exact_fallback_fraction"],
+            "host_block_loop_ms": head["host_block_loop_ms"],
+            "cpu_baseline": cpu,
+            "e2e": head["e2e"],
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head.get("clocks"),
+            "lines": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
+
+
+def relaunch(args) -> int:
+    """--gpus N without a torchrun environment: one process per GPU."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

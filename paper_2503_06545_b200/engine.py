@@ -68,6 +68,20 @@ def balance_scales(w: np.ndarray, act_absmax: np.ndarray) -> np.ndarray:
     return c
 
 
+def noise_key(seed: int, salt: Optional[int] = None) -> int:
+    """64-bit Philox key of a video's device noise stream: splitmix64 of its
+    seed (and of the optional salt), so nearby seeds get unrelated streams."""
+    def mix(z: int) -> int:
+        z = (z + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        return z ^ (z >> 31)
+    k = mix(int(seed) & 0xFFFFFFFFFFFFFFFF)
+    if salt is not None:
+        k = mix(k ^ (int(salt) & 0xFFFFFFFFFFFFFFFF))
+    return k
+
+
 class DevRows:
     """An uploaded int64 row table: its device address (all the kernels need)
     and, on demand, the torch view of it."""
@@ -191,6 +205,7 @@ class QuantCacheEngine:
         self.gemm_profile: Optional[list] = None   # set to [] to time every u8 GEMM
         self.quant_profile: Optional[list] = None  # set to [] to time every act_quant
         self.phase_profile: Optional[list] = None  # set to [] to time the other phases
+        self.att_flops = 0.0                       # self-attention flops while phase-profiled
         self.host_profile: Optional[list] = None   # set to []: host s from plan sync to the
                                                    # end of the block loop, per step
         # set to {} to record, per (layer, site), the channel max |x| of every
@@ -304,7 +319,12 @@ class QuantCacheEngine:
         # the next step's reuse plan + SRAP similarities run on a side stream
         # while this step's FP64 noise head runs (see _early_plan)
         self.side = torch.cuda.Stream(device=dev)
+        # the side stream's reduction workspace is sized and zeroed HERE, on the
+        # main stream, and the constructor synchronises below: its tickets must be
+        # zero before the side stream's first SRAP launch (the kernels' last CTA
+        # re-zeroes them after every use)
         self._srap_ws = Dv.Workspace()
+        self._srap_ws.get(int(N.lib().qcb_reduce_workspace_bytes(L * nv)))
         n_idx = 2 * max(1 << 15, 16 * L * (nv + 4) + 64)
         self.idx_host = torch.zeros(n_idx, dtype=torch.int64).pin_memory()
         self.idx_dev = torch.zeros(n_idx, dtype=torch.int64, device=dev)
@@ -312,6 +332,7 @@ class QuantCacheEngine:
         self._idx_hptr = self.idx_host.data_ptr()
         self._idx_dptr = self.idx_dev.data_ptr()
         self._begin_step(0)
+        torch.cuda.synchronize(dev)
 
     # ------------------------------------------------------------------ index tables
     def _begin_step(self, t: int):
@@ -485,12 +506,14 @@ class QuantCacheEngine:
                    epi=N.EPI_STORE_BF16 if qkv is self.qkv16 else N.EPI_STORE)
         with self._ph("attention"):
             self._attention(qkv[0], qkv[1], qkv[2], self.att, n, self.S, self.Sp)
+        if self.phase_profile is not None:   # 4 S^2 d flops per video (QK^T and PV)
+            self.att_flops += 4.0 * self.S * self.S * self.d * n
         self._site(l, "sta_o", bits, self.att, n, epi=N.EPI_GATE_RESID, out=A,
                    out_row0=out_row0, resid=A, resid_row0=xin_row0, gate=g1)
         # cross-attention on the single cond token
         self._site(l, "ca_q", bits, A, n, x_row0=out_row0, ln=(ln2g, ln2b), out=self.q2)
         k2, v2 = self._cond_kv(l, bits, vids, cond_row0)
-        with self._ph("attention"):
+        with self._ph("attention_ca"):
             self._attention(self.q2, k2, v2, self.att, n, 1, 1)
         self._site(l, "ca_o", bits, self.att, n, epi=N.EPI_RESID, out=A, out_row0=out_row0,
                    resid=A, resid_row0=out_row0)
@@ -591,7 +614,9 @@ class QuantCacheEngine:
             raise ValueError(f"engine sized for {self.nv} videos")
         L, S, d, T = self.L, self.S, self.d, self.T
         F, Tk = self.cfg.frames, self.cfg.tokens_per_frame
-        st = self.stream
+        # every launch, copy, event and synchronize of this call goes to the
+        # stream current at the call (the C ABI wrappers read it per launch)
+        st = self.stream = torch.cuda.current_stream(self.dev)
         self.pol.zero_()
         vids = []
         for v, seed in enumerate(seeds):
@@ -609,9 +634,11 @@ class QuantCacheEngine:
                 self.slot_view(vs.x).copy_(torch.from_numpy(x0.reshape(S, d)))
                 self.cond[v].copy_(torch.from_numpy(cond))
             vids.append(vs)
-        # device-noise mode: N(0,1) drawn inside the DDPM kernel (Philox4x32-10 keyed
-        # by this seed, one counter range per (step, video))
-        gen = int(device_noise_seed if device_noise_seed is not None else seeds[0]) \
+        # device-noise mode: N(0,1) drawn inside the DDPM kernel, Philox4x32-10 keyed
+        # by each video's OWN seed (mixed with the optional call-wide salt
+        # device_noise_seed), one counter range per step: a video's noise does not
+        # depend on its slot in the batch or on the rank that runs it
+        gen = [noise_key(s, device_noise_seed) for s in seeds] \
             if self.opts.noise == "device" else None
         self._early = None
         # cross-attention K/V of the cond tokens, per (layer, bits), for this call
@@ -902,7 +929,7 @@ class QuantCacheEngine:
                             float(np.sqrt(alpha)),
                             self.noise_dev[v] if (t > 1 and not dev_noise) else None, c3,
                             out=self.slot_view(new),
-                            noise_gen=(gen, (t * self.nv + v) * quads) if dev_noise else None)
+                            noise_gen=(gen[v], t * quads) if dev_noise else None)
                 else:
                     Dv.ddpm(self.slot_view(vs.x), eps_v, float(np.sqrt(1.0 - self.ab[0])),
                             float(np.sqrt(self.ab[0])), out=self.slot_view(new))
