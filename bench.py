@@ -536,7 +536,8 @@ def all_recompute_line(torch, args, model, absmax, int8_peak, peaks, traffic):
     wbits = {l: args.wbits for l in range(cfg.num_blocks)}
     eng = QuantCacheEngine(model, sched.alpha_bar,
                            Toggles(hlc=False, aigq_weights=True, aigq_acts=True, srap=False),
-                           ThresholdConfig(), wbits, absmax, sign_seed=0, prune_seed=0,
+                           ThresholdConfig(delta1=1.0, delta2=2.0), wbits, absmax, sign_seed=0,
+                           prune_seed=0,
                            max_videos=1, options=EngineOptions(attention="fast", noise="device"))
     gen = torch.Generator(device="cuda")
     gen.manual_seed(3)
@@ -636,7 +637,7 @@ def c1_latency(torch):
         cfg = harness.parse_config(dict(obj, toggles=full))
         calib = harness.load_calibration(cfg.calibration)
         harness.run_single(cfg, cfg.toggles_obj(), calib)
-        walls = [harness.run_single(cfg, cfg.toggles_obj(), calib).wall_ms for _ in range(3)]
+        walls = [harness.run_single(cfg, cfg.toggles_obj(), calib).wall_time_ms for _ in range(3)]
         T = cfg.noise_schedule().steps
         out[name] = {"ms_per_run": round(statistics.median(walls), 3),
                      "us_per_step": round(statistics.median(walls) / T * 1e3, 1), "steps": T}
@@ -664,6 +665,9 @@ def run_ours(args):
     head = run_workload(torch, args, args.workload, model, absmax, world=world, rank=rank,
                         local=local, int8_peak=int8_peak, peaks=peaks, traffic=traffic,
                         headline=True)
+    if rank == 0:
+        print("headline:", json.dumps({k: head[k] for k in ("value", "s_per_video",
+              "recompute_fraction", "profiled_step_ms")}), file=sys.stderr, flush=True)
     extra = {}
     if rank == 0 and world == 1 and not args.no_extra:
         extra["all_recompute"] = all_recompute_line(torch, args, model, absmax, int8_peak,
@@ -675,6 +679,7 @@ def run_ours(args):
         o = run_workload(torch, args, other, m2, absmax, world=1, rank=0, local=local,
                          int8_peak=int8_peak, peaks=peaks, traffic=traffic, headline=False)
         extra[other] = dict({"workload": WORKLOADS[other]["label"]}, **o)
+        print("extra:", json.dumps(extra, default=str)[:3000], file=sys.stderr, flush=True)
         extra["c2_gemm"] = c2_microbench(torch, int8_peak, peaks)
         extra["c1_latency"] = c1_latency(torch)
     cpu = None

@@ -107,6 +107,11 @@ QC_DEV uint64_t l2_policy_evict_first() {
 QC_DEV void st_f32_hint(float* a, float v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
 }
+QC_DEV void st_f32x4_hint(float* a, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
 QC_DEV void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                            uint64_t pol) {
   asm volatile(

@@ -318,8 +318,11 @@ QC_DEV T block_reduce256(T v, T* scratch, Op op) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) ln_mod_k(const QcbLnMod q) {
+#include "qc_pairwise.cuh"
+
+__global__ void __launch_bounds__(256) ln_mod_k(const QcbLnMod q, const PairwisePlan pl) {
   __shared__ double red[32];
+  __shared__ double pw_scr[608];
   const int seg = blockIdx.y, r = blockIdx.x;
   if (r >= (q.seg_valid > 0 ? q.seg_valid : q.seg_rows)) return;
   const long long irow = (q.x_row0 ? q.x_row0[seg] : (long long)seg * q.seg_rows) + r;
@@ -327,16 +330,20 @@ __global__ void __launch_bounds__(256) ln_mod_k(const QcbLnMod q) {
   const float* x = q.x + irow * q.ldx;
   float* o = q.out + orow * q.ldo;
   const int K = q.K;
-  double s = 0.0;
-  for (int j = threadIdx.x; j < K; j += 256) s += (double)x[j];
-  const double mean = block_reduce256(s, red, [](double a, double b) { return a + b; }) / K;
-  double v = 0.0;
-  for (int j = threadIdx.x; j < K; j += 256) {
-    const double d = (double)x[j] - mean;
-    v += d * d;
+  // mean / variance in numpy's pairwise order (qc_pairwise.cuh) by warp 0
+  if (threadIdx.x < 32) {
+    const double mean_w = __ddiv_rn(np_pairwise_row<false>(x, 0.0, pl, pw_scr, threadIdx.x),
+                                    (double)K);
+    const double var_w = __ddiv_rn(np_pairwise_row<true>(x, mean_w, pl, pw_scr, threadIdx.x),
+                                   (double)K);
+    if (threadIdx.x == 0) {
+      red[0] = mean_w;
+      red[1] = var_w;
+    }
   }
-  const double var = block_reduce256(v, red, [](double a, double b) { return a + b; }) / K;
-  const double sd = sqrt(var + 1e-5);
+  __syncthreads();
+  const double mean = red[0];
+  const double sd = __dsqrt_rn(__dadd_rn(red[1], 1e-5));
   for (int j = threadIdx.x; j < K; j += 256) {
     const double g = q.ln_g ? (double)q.ln_g[j] : 1.0;
     const double b = q.ln_b ? (double)q.ln_b[j] : 0.0;
@@ -347,7 +354,9 @@ __global__ void __launch_bounds__(256) ln_mod_k(const QcbLnMod q) {
 
 int ln_mod_launch(const QcbLnMod* q, cudaStream_t st) {
   dim3 grid(q->seg_valid > 0 ? q->seg_valid : q->seg_rows, q->nseg);
-  ln_mod_k<<<grid, 256, 0, st>>>(*q);
+  PairwisePlan pl{};
+  if (!pairwise_plan(q->K, pl)) return QCB_ERR_DIM;
+  ln_mod_k<<<grid, 256, 0, st>>>(*q, pl);
   return launch_status();
 }
 

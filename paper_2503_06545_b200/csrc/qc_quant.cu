@@ -22,6 +22,8 @@ namespace qc {
 
 constexpr int kQThreads = 256;
 
+#include "qc_pairwise.cuh"
+
 // Block-wide f64 sum / min / max via warp shuffles + smem (blockDim == 256).
 template <typename T, typename Op>
 QC_DEV T block_reduce(T v, T* scratch, Op op) {
@@ -101,7 +103,7 @@ QC_DEV void rotate_row(const ActQuantParams& p, int o, const float* hrow, double
 
 // Prologue: h = f32(LN64(x)) * scale1 + shift (or x itself), into hrow (f32 smem).
 QC_DEV void prologue_row(const ActQuantParams& p, const float* xrow, float* hrow,
-                         double* red) {
+                         double* red, const PairwisePlan& pl, double* pw_scr) {
   const int K = p.K;
   if (p.prologue == QCB_PRO_NONE) {
     for (int j = threadIdx.x; j < K; j += blockDim.x) hrow[j] = xrow[j];
@@ -113,16 +115,21 @@ QC_DEV void prologue_row(const ActQuantParams& p, const float* xrow, float* hrow
     __syncthreads();
     return;
   }
-  double s = 0.0;
-  for (int j = threadIdx.x; j < K; j += blockDim.x) s += (double)xrow[j];
-  const double mean = block_reduce(s, red, [](double a, double b) { return a + b; }) / K;
-  double v = 0.0;
-  for (int j = threadIdx.x; j < K; j += blockDim.x) {
-    const double d = (double)xrow[j] - mean;
-    v += d * d;
+  // mean / variance in numpy's pairwise order (qc_pairwise.cuh) by warp 0
+  if (threadIdx.x < 32) {
+    const double mean_w = __ddiv_rn(np_pairwise_row<false>(xrow, 0.0, pl, pw_scr, threadIdx.x),
+                                    (double)K);
+    const double var_w = __ddiv_rn(np_pairwise_row<true>(xrow, mean_w, pl, pw_scr, threadIdx.x),
+                                   (double)K);
+    if (threadIdx.x == 0) {
+      red[0] = mean_w;
+      red[1] = var_w;
+    }
   }
-  const double var = block_reduce(v, red, [](double a, double b) { return a + b; }) / K;
-  const double sd = sqrt(var + 1e-5);
+  __syncthreads();
+  const double mean = red[0];
+  const double sd = __dsqrt_rn(__dadd_rn(red[1], 1e-5));
+  __syncthreads();
   for (int j = threadIdx.x; j < K; j += blockDim.x) {
     const double g = p.ln_g ? (double)p.ln_g[j] : 1.0;
     const double bb = p.ln_b ? (double)p.ln_b[j] : 0.0;
@@ -135,11 +142,13 @@ QC_DEV void prologue_row(const ActQuantParams& p, const float* xrow, float* hrow
 
 // Grid: one CTA per (segment, row).  kPass 1: min/max; kPass 2: codes.
 template <int kPass>
-__global__ void __launch_bounds__(kQThreads) act_quant_rows(const ActQuantParams p) {
+__global__ void __launch_bounds__(kQThreads)
+    act_quant_rows(const ActQuantParams p, const PairwisePlan pl) {
   extern __shared__ __align__(16) uint8_t sm[];
   double* buf = reinterpret_cast<double*>(sm);
   float* hrow = reinterpret_cast<float*>(buf + p.K);
   __shared__ double red[32];
+  __shared__ double pw_scr[608];
   __shared__ float fred[32];
   __shared__ int ired[32];
   __shared__ double s_scale[3];
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(kQThreads) act_quant_rows(const ActQuantParams
     }
   }
 
-  prologue_row(p, xrow, hrow, red);
+  prologue_row(p, xrow, hrow, red, pl, pw_scr);
   for (int o = 0; o < p.n_out; ++o) {
     rotate_row(p, o, hrow, buf);
     if (kPass == 1) {
@@ -852,7 +861,8 @@ QC_DEV double flip_sign(double x, uint32_t bit) {
 // kPro: the prologue compiled in (0 none, 1 LN + modulation, 2 GELU), so each
 // variant gets its own register allocation.
 template <int B, bool kPow2Scale, int kMinCtas, int kPro>
-__global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuantParams p, const AQ2 a) {
+__global__ void __launch_bounds__(kV4Threads, kMinCtas)
+    aq4_pass1(const ActQuantParams p, const AQ2 a, const PairwisePlan pl) {
   pdl_wait();   // x rows / keys come from the preceding kernels
   pdl_trigger();
   constexpr int R = 4096 / B;               // row slots per CTA
@@ -962,35 +972,15 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas) aq4_pass1(const ActQuant
       ht[i] = (t < T) ? xs[B + t] : 0.f;
     }
     if (kPro == 1) {
-      double s0 = 0.0, s1 = 0.0;   // two chains
+      // mean and variance in numpy's pairwise order (qc_pairwise.cuh) by the
+      // slot's threads on the row in shared memory, the FWHT work row as scratch
+      const double mean = __ddiv_rn(
+          np_pairwise_group<false>(xs, 0.0, pl, sm.f[rl], lt, TPR, row_sync), (double)K);
+      const double var = __ddiv_rn(
+          np_pairwise_group<true>(xs, mean, pl, sm.f[rl], lt, TPR, row_sync), (double)K);
+      const double sd = __dsqrt_rn(__dadd_rn(var, 1e-5));
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        s0 += (double)h[2 * i];
-        s1 += (double)h[2 * i + 1];
-      }
-      double s = s0 + s1;
-#pragma unroll
-      for (int i = 0; i < kV4Tail; ++i) s += (double)ht[i];
-      const double mean = slot_sum(s, sm.red[0]) / K;
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {   // x - mean parked in the thread's own stage-A slots
-        const double d0 = (double)h[2 * i] - mean, d1 = (double)h[2 * i + 1] - mean;
-        fa[SA * (2 * i)] = d0;
-        fa[SA * (2 * i + 1)] = d1;
-        v0 += d0 * d0;
-        v1 += d1 * d1;
-      }
-      double v = v0 + v1;
-#pragma unroll
-      for (int i = 0; i < kV4Tail; ++i) {
-        if (lt + TPR * i < T) {
-          const double d = (double)ht[i] - mean;
-          v += d * d;
-        }
-      }
-      const double vt = slot_sum(v, sm.red[1]);
-      const double sd = sqrt(vt / K + 1e-5);
+      for (int i = 0; i < 16; ++i) fa[SA * i] = __dsub_rn((double)h[i], mean);   // x - mean
       const double rsd = 1.0 / sd;
       // fast path x*(1/sd) for all 16, one sticky flag; exact division only
       // for elements next to an f32 tie or with cancellation (ln_from_xm)
@@ -1463,12 +1453,18 @@ __global__ void recip_k(const double* c, const float* signs, int b, double* rc, 
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// pass 2 launch: the streaming kernel for codes-only calls, else the general one
-static void launch_pass2(const qc::ActQuantParams& p, const qc::AQ2& a, cudaStream_t st) {
+// codes-only calls that the streaming pass 2 serves
+static bool pass2_hot_ok(const qc::ActQuantParams& p, const qc::AQ2& a) {
   bool hot = (p.K & 3) == 0 && (p.ldc & 3) == 0 && p.n_out * p.nseg <= qc::kP2Pairs &&
              a.ld_stash % 4 == 0;
   for (int o = 0; o < p.n_out; ++o)
     if (!p.codes[o] || p.deq_out[o] || (reinterpret_cast<uintptr_t>(p.codes[o]) & 3)) hot = false;
+  return hot;
+}
+
+// pass 2 launch: the streaming kernel for codes-only calls, else the general one
+static void launch_pass2(const qc::ActQuantParams& p, const qc::AQ2& a, cudaStream_t st) {
+  const bool hot = pass2_hot_ok(p, a);
   if (hot) {
     static int resident = 0;
     if (!resident) {
@@ -1528,6 +1524,9 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
   p.b = b;
   p.rscale = (float)(1.0 / sqrt((double)b));
   p.keys = reinterpret_cast<uint32_t*>(q->workspace);
+  // the LN prologue's numpy pairwise-sum plan over K (qc_pairwise.cuh)
+  PairwisePlan pl{};
+  if (q->prologue == QCB_PRO_LN_MOD && !pairwise_plan(q->K, pl)) return QCB_ERR_DIM;
   const int nkeys = 2 * q->n_out * q->nseg;
   launch_pdl(init_keys, dim3((nkeys + 255) / 256), dim3(256), 0, st, p.keys, nkeys);
   // v2: register FWHT for b in {1024, 2048, 4096} with a short tail
@@ -1586,7 +1585,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
 #define QC_AQ4(BB, P2, MC, PRO, FLAG)                                                          \
   allow_max_smem(aq4_pass1<BB, P2, MC, PRO>, FLAG);                                            \
   launch_pdl(aq4_pass1<BB, P2, MC, PRO>, dim3(b1), dim3(kV4Threads),                           \
-             sizeof(V4Smem<BB>) + ln_bytes, st, p, a);                                         \
+             sizeof(V4Smem<BB>) + ln_bytes, st, p, a, pl);                                     \
   break;
         case 4096: QC_AQ4(1024, true, 2, 0, a41)
         case 4097: QC_AQ4(1024, true, 2, 1, a41l)
@@ -1623,8 +1622,8 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
   allow_max_smem(act_quant_rows<1>, attr1);
   allow_max_smem(act_quant_rows<2>, attr2);
   dim3 grid(p.seg_valid, p.nseg);
-  act_quant_rows<1><<<grid, kQThreads, smem, st>>>(p);
-  act_quant_rows<2><<<grid, kQThreads, smem, st>>>(p);
+  act_quant_rows<1><<<grid, kQThreads, smem, st>>>(p, pl);
+  act_quant_rows<2><<<grid, kQThreads, smem, st>>>(p, pl);
   return launch_status();
 }
 

@@ -13,15 +13,17 @@ sys.path.insert(0, ".")
 from paper_2503_06545_b200 import device as D
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--M", type=int, default=8192)
+ap.add_argument("--M", type=int, default=16384)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--cases", default="")
 args = ap.parse_args()
 torch.manual_seed(0)
 M = args.M
 cases = [("qkv_ln", 1152, 3, True), ("ln1", 1152, 1, True), ("plain1152", 1152, 1, False),
-         ("plain4608", 4608, 1, False)]
+         ("plain4608", 4608, 1, False), ("gelu4608", 4608, 1, "gelu")]
 for name, K, nout, ln in cases:
+    gelu = ln == "gelu"
+    ln = ln is True
     if args.cases and name not in args.cases.split(","):
         continue
     x = torch.randn(M, K, device="cuda")
@@ -31,12 +33,12 @@ for name, K, nout, ln in cases:
         sg = torch.as_tensor(D.sign_vector(o, D.pow2_floor(K))).cuda()
         trs.append((c, sg))
     lnp = (torch.rand(K, device="cuda") + 0.5, torch.randn(K, device="cuda") * 0.1) if ln else None
-    outs = D.act_quant(x, 8, trs, ln=lnp, mod=(1.1, 0.05))
+    outs = D.act_quant(x, 8, trs, ln=lnp, mod=(1.1, 0.05), gelu=gelu)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.iters):
-        D.act_quant(x, 8, trs, ln=lnp, mod=(1.1, 0.05), out=outs)
+        D.act_quant(x, 8, trs, ln=lnp, mod=(1.1, 0.05), out=outs, gelu=gelu)
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / args.iters * 1e3
