@@ -455,6 +455,7 @@ def run_workload(torch, args, workload, model, absmax, *, world, rank, local, in
     if clocks:
         clocks.start()
     launches0 = Dv.LAUNCHES[0]
+    eng.head_calls = eng.head_skipped = 0
     e0, e1 = _events(torch)
     torch.cuda.synchronize()
     # QC_PROFILE_RANGE=1: open the CUDA profiler range around the timed steps only,
@@ -487,6 +488,7 @@ def run_workload(torch, args, workload, model, absmax, *, world, rank, local, in
         "ms_per_step": elapsed / n_steps * 1e3, "s_per_video": elapsed / (n_steps * B),
         "steps": n_steps, "warmup": n_warm, "videos_per_gpu_per_step": B,
         "recompute_fraction": frac, "prune_fraction": prune_frac,
+        "head_reuse_fraction": eng.head_skipped / max(1, eng.head_calls),
         "executed_bit_macs_per_video": executed / (n_steps * B), "gpu_launches": launches,
         "thresholds": {"delta1": th.delta1, "delta2": th.delta2, "v_low": th.v_low,
                        "v_high": th.v_high},
@@ -667,7 +669,8 @@ def run_ours(args):
                         headline=True)
     if rank == 0:
         print("headline:", json.dumps({k: head[k] for k in ("value", "s_per_video",
-              "recompute_fraction", "profiled_step_ms")}), file=sys.stderr, flush=True)
+              "recompute_fraction", "head_reuse_fraction", "profiled_step_ms")}),
+              file=sys.stderr, flush=True)
     extra = {}
     if rank == 0 and world == 1 and not args.no_extra:
         extra["all_recompute"] = all_recompute_line(torch, args, model, absmax, int8_peak,
@@ -710,6 +713,7 @@ def run_ours(args):
             "s_per_video": head["s_per_video"],
             "recompute_fraction": head["recompute_fraction"],
             "prune_fraction": head["prune_fraction"],
+            "head_reuse_fraction": head["head_reuse_fraction"],
             "executed_bit_macs_per_video": head["executed_bit_macs_per_video"],
             "roofline": dominant,
             "roofline_kernels": kern,

@@ -8,8 +8,10 @@ import sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass",
-                      "-k", f"regex:{kre}"], capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"]
+if kre != "all":
+    cmd += ["-k", f"regex:{kre}"]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ie = hdr.index("Instructions Executed")
