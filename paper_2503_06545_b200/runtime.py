@@ -57,8 +57,15 @@ class QuantRuntime:
         quant_acts = tog.aigq_acts and abits < FP_BITS
 
         def gemm(layer: int, site: str, x, w):
-            xt = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, np.float32))
-            xt = xt.float().cuda().contiguous()
+            # type-preserving at the LayerHooks boundary (model.py:89-90): an
+            # ndarray in (the reference's block_forward) gives an ndarray out
+            if not isinstance(x, torch.Tensor):
+                y = gemm_dev(layer, site, torch.as_tensor(np.asarray(x, np.float32)), w)
+                return y.cpu().numpy()
+            return gemm_dev(layer, site, x, w)
+
+        def gemm_dev(layer: int, site: str, x: torch.Tensor, w):
+            xt = x.float().cuda().contiguous()
             if tog.aigq_weights:
                 pw = self._prepared[(layer, site)]
                 tr = [(pw.chan_scale, pw.signs)] if pw.chan_scale is not None else [None]

@@ -99,10 +99,8 @@ def generate(model, sched: NoiseSchedule, scheduler=None, seed: int = 0,
         # caller hooks see every block: the per-block device path (forward.py)
         from .forward import generate_hooked
         return generate_hooked(model, sched, seed, collect_features, extra_hooks)
-    if extra_hooks is not None:
-        raise NotImplementedError(
-            "extra_hooks with a scheduler: the scheduled run is the fused device engine; "
-            "pass hooks without a scheduler (forward.generate_hooked)")
+    # with a scheduler the reference uses only the scheduled hooks: extra_hooks
+    # is ignored (reference sampler.py:114-119)
     if scheduler is None:
         eng = QuantCacheEngine(model, sched.alpha_bar, Toggles(),
                                ThresholdConfig(delta1=0.0, delta2=0.0), options=options)
