@@ -565,6 +565,59 @@ def all_recompute_line(torch, args, model, absmax, int8_peak, peaks, traffic):
             "profiled_step_ms": phases, "roofline_kernels": kern}
 
 
+def c4_cfg_line(torch, args, model, absmax, th_target, S_target, cfg_scale=4.5):
+    """BASELINE configs[3] (C4) on one GPU: STDiT-XL/2 dims, 64 frames 512x512
+    (S = 65,536), classifier-free guidance (an EXTENSION: the reference has no
+    CFG) as a cond and an uncond branch per video with their own QuantCache
+    decisions, HLC + SRAP + mixed-bit AIGQ, T steps, 1 video.  Thresholds: the
+    target's calibrated ones scaled by the D / V scaling laws (D = L1 x L2 over
+    S x d elements ~ S^1.5, V = L1 ~ S) -- an all-recompute calibration pass at
+    this size would take minutes."""
+    from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
+    from paper_2503_06545_b200.model import DiTConfig, DiTModel
+    from paper_2503_06545_b200.sampler import linear_beta_schedule
+    from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles
+    cfg = DiTConfig(seed=0, **dict(STDIT, frames=64, tokens_per_frame=1024))
+    m4 = DiTModel(cfg, model.blocks, model.head_w, model.head_b)
+    S, d, T = cfg.seq_len, cfg.model_dim, args.timesteps
+    r = S / S_target
+    th = ThresholdConfig(delta1=th_target["delta1"] * r ** 1.5,
+                         delta2=th_target["delta2"] * r ** 1.5,
+                         v_low=th_target["v_low"] * r, v_high=th_target["v_high"] * r)
+    wbits = {l: args.wbits for l in range(cfg.num_blocks)}
+    sched = linear_beta_schedule(T)
+    eng = QuantCacheEngine(m4, sched.alpha_bar,
+                           Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=True),
+                           th, wbits, absmax, sign_seed=0, prune_seed=0, max_videos=2,
+                           options=EngineOptions(attention="fast", noise="device",
+                                                 cfg_scale=cfg_scale))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(4)
+    x0 = torch.randn((1, S, d), device="cuda", generator=gen)
+    cond = torch.randn((1, cfg.cond_dim), device="cuda", generator=gen)
+    eng.generate([40], x0_dev=x0, cond_dev=cond, return_device=True)
+    torch.cuda.synchronize()
+    e0, e1 = _events(torch)
+    e0.record()
+    _, vids = eng.generate([41], x0_dev=x0, cond_dev=cond, return_device=True)
+    e1.record()
+    torch.cuda.synchronize()
+    el = e0.elapsed_time(e1) / 1e3
+    recs = [r_ for tv in eng.traces_of(vids) for r_ in tv if r_.layer != "head"]
+    frac = sum(r_.action == "recompute" for r_ in recs) / max(1, len(recs))
+    out = {"workload": f"C4 (extension: CFG): STDiT-XL/2 dims, 64 frames 512x512 (S={S}), "
+                       f"cond + uncond branches (guidance {cfg_scale}), DDPM T={T}, full "
+                       f"QuantCache per branch, 1 video on 1 GPU",
+           "value": 1.0 / el, "unit": "videos/s", "s_per_video": el,
+           "recompute_fraction": frac, "arena_gib": round(eng.arena.numel() * 4 / 2 ** 30, 2),
+           "thresholds": {"delta1": th.delta1, "delta2": th.delta2, "v_low": th.v_low,
+                          "v_high": th.v_high, "note": "target thresholds x (S ratio)^1.5 "
+                                                        "for delta, x S ratio for v"}}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
 def c2_microbench(torch, int8_peak, peaks):
     """BASELINE configs[1] (C2): the AIGQ quantized linear at M = 16,384 tokens
     (one 16-frame 512^2 video), K,N in {1152, 4608}: quantizer (rotation +
@@ -607,11 +660,17 @@ def c2_microbench(torch, int8_peak, peaks):
             tg = timed(lambda: Dv.gemm_u8(a, pw, out=out))
             tops = 2.0 * M * Nn * K / tg / 1e12
             gbs = (4 + 1) * M * K / tq / 1e9
-            res[f"K{K}_N{Nn}_W{wb}A{ab}"] = {
-                "gemm_us": round(tg * 1e6, 2), "gemm_tops": round(tops, 1),
-                "gemm_frac_int8_peak": round(tops / peak_tops, 4),
-                "quant_us": round(tq * 1e6, 2), "quant_gbs": round(gbs, 1),
-                "quant_frac_hbm": round(gbs / peaks["hbm"], 4)}
+            r = {"gemm_us": round(tg * 1e6, 2), "gemm_tops": round(tops, 1),
+                 "gemm_frac_int8_peak": round(tops / peak_tops, 4),
+                 "quant_us": round(tq * 1e6, 2), "quant_gbs": round(gbs, 1),
+                 "quant_frac_hbm": round(gbs / peaks["hbm"], 4)}
+            if wb <= 4:   # the nibble-packed weight operand (unpacked in shared memory)
+                pw4 = Dv.weight_prep(w, wb, c, signs, pack4=True)
+                t4 = timed(lambda: Dv.gemm_u8(a, pw4, out=out))
+                r["packed_w4_gemm_us"] = round(t4 * 1e6, 2)
+                r["packed_w4_gemm_tops"] = round(2.0 * M * Nn * K / t4 / 1e12, 1)
+                del pw4
+            res[f"K{K}_N{Nn}_W{wb}A{ab}"] = r
         del x, w
     del flush
     torch.cuda.empty_cache()
@@ -682,6 +741,9 @@ def run_ours(args):
         o = run_workload(torch, args, other, m2, absmax, world=1, rank=0, local=local,
                          int8_peak=int8_peak, peaks=peaks, traffic=traffic, headline=False)
         extra[other] = dict({"workload": WORKLOADS[other]["label"]}, **o)
+        tgt = head if args.workload == "target" else o
+        extra["c4_cfg"] = c4_cfg_line(torch, args, model, absmax, tgt["thresholds"],
+                                      model_dims("target")["tokens_per_frame"] * 16)
         print("extra:", json.dumps(extra, default=str)[:3000], file=sys.stderr, flush=True)
         extra["c2_gemm"] = c2_microbench(torch, int8_peak, peaks)
         extra["c1_latency"] = c1_latency(torch)

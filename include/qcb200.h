@@ -12,7 +12,8 @@
  *     TypeError, QCB_ERR_CUDA -> RuntimeError.
  *
  * Reference interfaces replaced (paths under /root/reference/pkg/src/ditrt):
- *   qcb_gemm_u8        tensor.py:68-112   matmul_int (+ model.py:187-198 epilogues)
+ *   qcb_gemm_u8        tensor.py:68-112   matmul_int
+ *   qcb_pack_w4        quant.py:206       W4 weights, nibble-packed GEMM operand (+ model.py:187-198 epilogues)
  *   qcb_gemm_f64       tensor.py:43-65    mm / matmul_fp (FP sites)
  *   qcb_head_gemm      model.py:228       mm(x, head_w) + head_b (certified int8)
  *   qcb_act_quant      quant.py:83-123,163-165  compute_minmax_params + quantize
@@ -22,6 +23,7 @@
  *   qcb_attention_f64  model.py:150-156, tensor.py:115-132  _mha / attention
  *   qcb_ln_mod         model.py:137-142 (+182,196)  _ln and modulation
  *   qcb_ddpm_step      sampler.py:59-88   reverse_step / final_step
+ *   qcb_cfg_combine    (extension)        classifier-free guidance of eps
  *   qcb_gelu_inplace   model.py:145-147   _gelu
  *   qcb_reduce_hlc     schedule.py:67-82  divergence_score partial sums
  *   qcb_reduce_srap    schedule.py:108-116 layer_similarity partial sums
@@ -95,9 +97,21 @@ typedef struct QcbGemm {
   long long out_rows;          /* rows of the output buffer (TMA bounds); 0 = M */
   long long resid_rows;        /* rows of the residual buffer (TMA bounds); 0 =  */
                                /* out_rows when resid == out, else M             */
+  const uint8_t* w_packed;     /* nullable: W4 weights, 2 codes per byte (low    */
+  long long ldwp;              /* nibble = even k), [N][ldwp], ldwp % 64 == 0,   */
+                               /* zero padded; replaces w_codes (qcb_pack_w4)    */
 } QcbGemm;
 
 int qcb_gemm_u8(const QcbGemm* g, void* stream);
+
+/* Nibble-pack <= 4-bit weight codes (quant.py:206 BIT_LEVELS 4, the paper's W4):
+ * packed[n][k/2] = codes[n][k] | codes[n][k+1] << 4 from the K-major [N][ldk]
+ * u8 codes, rows zero padded to ldwp (a multiple of 64 bytes).  The GEMM then
+ * streams half the weight bytes and unpacks them to u8 in shared memory in
+ * its producer warps (tcgen05 has no 4-bit integer MMA).  QCB_ERR_VALUE if a
+ * code exceeds 15. */
+int qcb_pack_w4(const uint8_t* codes, long long ldk, int N, int K, uint8_t* packed,
+                long long ldwp, void* stream);
 
 /* Plain f64-accumulating FP GEMM, ascending k (tensor.py:43-60), f32 out.
  * A [M][lda] f32 (rows via a_row0 per segment), W [K][ldw] f32 row-major. */
@@ -239,6 +253,14 @@ typedef struct QcbDdpm {
 } QcbDdpm;
 
 int qcb_ddpm_step(const QcbDdpm* d, void* stream);
+
+/* Classifier-free guidance (a labelled EXTENSION: the reference has no CFG,
+ * SPEC.md:468): out[i] = f32(eps_u[i] + scale * (eps_c[i] - eps_u[i])), one
+ * fused multiply-add per element, over n elements (16-byte aligned buffers use
+ * vector loads).  Feeds qcb_ddpm_step with the guided noise estimate of a
+ * video whose cond / uncond branches ran as two engine slots. */
+int qcb_cfg_combine(const float* eps_c, const float* eps_u, float scale, float* out,
+                    long long n, void* stream);
 
 /* In-place x = f32(gelu_f64(x)) with SciPy's erf (model.py:145-147) over a
  * [rows][ld] f32 buffer (cols valid columns); ld % 4 == 0, x 16-byte aligned. */

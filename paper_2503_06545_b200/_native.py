@@ -32,7 +32,8 @@ class QcbGemm(C.Structure):
                 ("w_zero", vp), ("w_colsum", vp), ("out", vp), ("ldo", i64),
                 ("out_row0", vp), ("resid", vp), ("ldr", i64), ("resid_row0", vp),
                 ("gate", vp), ("gate_scalar", f32), ("epilogue", i32), ("block_n", i32),
-                ("seg_active", vp), ("out_rows", i64), ("resid_rows", i64)]
+                ("seg_active", vp), ("out_rows", i64), ("resid_rows", i64),
+                ("w_packed", vp), ("ldwp", i64)]
 
 
 class QcbGemmF64(C.Structure):
@@ -135,6 +136,8 @@ def lib():
         "qcb_ln_mod": [P(QcbLnMod), vp],
         "qcb_attention_f64": [P(QcbAttention), vp],
         "qcb_ddpm_step": [P(QcbDdpm), vp],
+        "qcb_cfg_combine": [vp, vp, C.c_float, vp, i64, vp],
+        "qcb_pack_w4": [vp, i64, i32, i32, vp, i64, vp],
         "qcb_gelu_inplace": [vp, i64, i32, i32, vp],
         "qcb_reduce_hlc": [QcbFeat, QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp, vp],
         "qcb_reduce_srap": [QcbFeat, QcbFeat, i32, i32, i32, vp, vp, vp, vp, vp],
@@ -167,9 +170,9 @@ def lib():
     return h
 
 
-EXPORTED = ("qcb_gemm_u8", "qcb_gemm_f64", "qcb_head_gemm", "qcb_head_prep",
+EXPORTED = ("qcb_gemm_u8", "qcb_pack_w4", "qcb_gemm_f64", "qcb_head_gemm", "qcb_head_prep",
             "qcb_head_prep_bytes", "qcb_head_workspace_bytes", "qcb_act_quant", "qcb_act_quant_workspace_bytes", "qcb_weight_prep", "qcb_ln_mod",
-            "qcb_attention_f64", "qcb_ddpm_step", "qcb_gelu_inplace", "qcb_reduce_hlc", "qcb_reduce_srap",
+            "qcb_attention_f64", "qcb_ddpm_step", "qcb_cfg_combine", "qcb_gelu_inplace", "qcb_reduce_hlc", "qcb_reduce_srap",
             "qcb_reduce_l1", "qcb_reduce_l1_hist", "qcb_reduce_workspace_bytes", "qcb_copy_async", "qcb_col_absmax", "qcb_policy_plan_reuse",
             "qcb_policy_sim_mask", "qcb_policy_plan_finish", "qcb_policy_observe",
             "qcb_policy_observe_all",

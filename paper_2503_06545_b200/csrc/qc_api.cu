@@ -10,12 +10,18 @@ using namespace qc;
 static bool aligned16(long long v) { return (v % 16) == 0; }
 
 extern "C" int qcb_gemm_u8(const QcbGemm* g, void* stream) {
-  if (!g || !g->a_codes || !g->w_codes || !g->out || !g->a_scale || !g->a_zero ||
-      !g->a_rowsum || !g->w_scale || !g->w_zero || !g->w_colsum)
+  if (!g || !g->a_codes || (!g->w_codes && !g->w_packed) || !g->out || !g->a_scale ||
+      !g->a_zero || !g->a_rowsum || !g->w_scale || !g->w_zero || !g->w_colsum)
     return QCB_ERR_VALUE;
   if (g->M <= 0 || g->N <= 0 || g->K <= 0) return QCB_ERR_DIM;
-  if (g->lda < g->K || g->ldw < g->K || !aligned16(g->lda) || !aligned16(g->ldw))
+  if (g->lda < g->K || !aligned16(g->lda)) return QCB_ERR_DIM;
+  if (g->w_packed) {   // W4: [N][ldwp] nibbles, rows padded to whole 128-k blocks
+    if (g->ldwp % 64 || 2 * g->ldwp < g->K || reinterpret_cast<uintptr_t>(g->w_packed) % 16)
+      return QCB_ERR_DIM;
+  } else if (g->ldw < g->K || !aligned16(g->ldw) ||
+             reinterpret_cast<uintptr_t>(g->w_codes) % 16) {
     return QCB_ERR_DIM;
+  }
   if (g->ldo < g->N) return QCB_ERR_DIM;
   // u8 x u8 into a signed 32-bit accumulator: K * 255 * 255 must fit
   // (the reference guards its emulated accumulator the same way, tensor.py:91-98).
@@ -25,9 +31,15 @@ extern "C" int qcb_gemm_u8(const QcbGemm* g, void* stream) {
   if (g->epilogue < QCB_EPI_STORE || g->epilogue > QCB_EPI_STORE_BF16 ||
       g->epilogue == QCB_EPI_BIAS)
     return QCB_ERR_CONFIG;
-  if (reinterpret_cast<uintptr_t>(g->a_codes) % 16 || reinterpret_cast<uintptr_t>(g->w_codes) % 16)
-    return QCB_ERR_DIM;
+  if (reinterpret_cast<uintptr_t>(g->a_codes) % 16) return QCB_ERR_DIM;
   return gemm_u8_launch(g, (cudaStream_t)stream);
+}
+
+extern "C" int qcb_pack_w4(const uint8_t* codes, long long ldk, int N, int K, uint8_t* packed,
+                           long long ldwp, void* stream) {
+  if (!codes || !packed) return QCB_ERR_VALUE;
+  if (N <= 0 || K <= 0 || ldk < K || ldwp % 64 || 2 * ldwp < K) return QCB_ERR_DIM;
+  return pack_w4_launch(codes, ldk, N, K, packed, ldwp, (cudaStream_t)stream);
 }
 
 extern "C" int qcb_head_prep(const float* w, int K, int N, void* prep, void* stream) {
@@ -101,6 +113,13 @@ extern "C" int qcb_ddpm_step(const QcbDdpm* d, void* stream) {
   if (d->rc2 != 0.0 && d->rc2 * d->c2 != 1.0 && fabs(d->rc2 * d->c2 - 1.0) > 1e-15)
     return QCB_ERR_VALUE;   // rc2 must be RN(1 / c2)
   return ddpm_launch(d, (cudaStream_t)stream);
+}
+
+extern "C" int qcb_cfg_combine(const float* eps_c, const float* eps_u, float scale, float* out,
+                               long long n, void* stream) {
+  if (!eps_c || !eps_u || !out) return QCB_ERR_VALUE;
+  if (n <= 0) return QCB_ERR_DIM;
+  return cfg_combine_launch(eps_c, eps_u, scale, out, n, (cudaStream_t)stream);
 }
 
 extern "C" int qcb_gelu_inplace(float* x, long long ld, int rows, int cols, void* stream) {

@@ -88,5 +88,9 @@ int weight_prep_launch(const QcbWeightPrep* q, cudaStream_t st);
 int ln_mod_launch(const QcbLnMod* q, cudaStream_t st);
 int attention_f64_launch(const QcbAttention* a, cudaStream_t st);
 int ddpm_launch(const QcbDdpm* d, cudaStream_t st);
+int pack_w4_launch(const uint8_t* codes, long long ldk, int N, int K, uint8_t* packed,
+                   long long ldwp, cudaStream_t st);
+int cfg_combine_launch(const float* ec, const float* eu, float scale, float* out, long long n,
+                       cudaStream_t st);
 int gelu_launch(float* x, long long ld, int rows, int cols, cudaStream_t st);
 }  // namespace qc

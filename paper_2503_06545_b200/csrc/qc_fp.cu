@@ -634,6 +634,35 @@ __global__ void ddpm_k(const QcbDdpm d) {
   }
 }
 
+// classifier-free guidance: out = eps_u + scale * (eps_c - eps_u) (extension)
+__global__ void cfg_combine_k(const float* __restrict__ ec, const float* __restrict__ eu,
+                              float scale, float* __restrict__ out, long long n) {
+  pdl_wait();
+  pdl_trigger();
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= n) return;
+  if (i + 3 < n && ((reinterpret_cast<uintptr_t>(ec) | reinterpret_cast<uintptr_t>(eu) |
+                     reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    const float4 c = __ldcs(reinterpret_cast<const float4*>(ec + i));
+    const float4 u = __ldcs(reinterpret_cast<const float4*>(eu + i));
+    *reinterpret_cast<float4*>(out + i) =
+        make_float4(__fmaf_rn(scale, c.x - u.x, u.x), __fmaf_rn(scale, c.y - u.y, u.y),
+                    __fmaf_rn(scale, c.z - u.z, u.z), __fmaf_rn(scale, c.w - u.w, u.w));
+  } else {
+    for (int k = 0; k < 4 && i + k < n; ++k)
+      out[i + k] = __fmaf_rn(scale, ec[i + k] - eu[i + k], eu[i + k]);
+  }
+}
+
+int cfg_combine_launch(const float* ec, const float* eu, float scale, float* out, long long n,
+                       cudaStream_t st) {
+  const int th = 256;
+  const long long n4 = (n + 3) / 4;
+  launch_pdl(cfg_combine_k, dim3((unsigned)((n4 + th - 1) / th)), dim3(th), 0, st, ec, eu,
+             scale, out, n);
+  return launch_status();
+}
+
 int ddpm_launch(const QcbDdpm* d, cudaStream_t st) {
   const int th = 256;
   const long long n4 = (d->n + 3) / 4;

@@ -109,7 +109,24 @@ struct GemmParams {
   // (one launch for the head's digit diagonals, qc_head.cu).
   int group_n, group_k;
   long long rowsum_stride;
+  // W4 (nullable): nibble-packed weights [N][ldwp]; warps 2-3 unpack each
+  // k-block into the swizzled B stage instead of a TMA load
+  const uint8_t* wp;
+  long long ldwp;
 };
+
+// 16 packed bytes (byte j = code 2j | code 2j+1 << 4) -> 32 u8 codes in order
+QC_DEV void unpack_nibbles(uint4 p, uint4& lo, uint4& hi) {
+  auto sp = [](uint32_t x, uint32_t& a, uint32_t& b) {
+    const uint32_t l = x & 0x0F0F0F0Fu, h = (x >> 4) & 0x0F0F0F0Fu;
+    a = __byte_perm(l, h, 0x5140);   // l0 h0 l1 h1
+    b = __byte_perm(l, h, 0x7362);   // l2 h2 l3 h3
+  };
+  sp(p.x, lo.x, lo.y);
+  sp(p.y, lo.z, lo.w);
+  sp(p.z, hi.x, hi.y);
+  sp(p.w, hi.z, hi.w);
+}
 
 
 template <int BN, int MODE, bool PAIR>
@@ -137,7 +154,8 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
   uint64_t* tfull_bar = empty_bar + Cfg::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* res_bar = tempty_bar + 2;   // [kMaxEpiWarps][2] residual slab barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + 2 * kMaxEpiWarps);
+  uint64_t* raw_bar = res_bar + 2 * kMaxEpiWarps;   // W4: [kStages] TMA landed (A + packed B)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_bar + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -160,8 +178,9 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
     for (int s = 0; s < Cfg::kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
+      mbar_init(&full_bar[s], p.wp ? 2 : 1);   // W4: armed by the two unpack warps
       mbar_init(&empty_bar[s], 1);
+      mbar_init(&raw_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -209,6 +228,14 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
             tma_load_2d_pair(&map_a, bar, smem_a + stage * Cfg::kABytes, kb * kBlockK, m0);
             tma_load_2d_pair(&map_b, bar, smem_b + stage * Cfg::kBBytes, kb * kBlockK,
                              n0 + (int)rank * (BN / 2));
+          } else if (p.wp) {
+            // W4: A and the packed B rows (64 bytes each, into the upper half of
+            // the stage's B buffer) land on raw_bar; the unpack warps arm full_bar
+            mbar_arrive_expect_tx(&raw_bar[stage], Cfg::kABytes + BN * 64);
+            tma_load_2d(&map_a, &raw_bar[stage], smem_a + stage * Cfg::kABytes, kb * kBlockK,
+                        m0);
+            tma_load_2d(&map_b, &raw_bar[stage], smem_b + stage * Cfg::kBBytes + BN * 64,
+                        kb * 64, n0);
           } else {
             mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
             tma_load_2d(&map_a, &full_bar[stage], smem_a + stage * Cfg::kABytes, kb * kBlockK,
@@ -263,6 +290,44 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
+        }
+      }
+    }
+  } else if ((warp == 2 || warp == 3) && !PAIR && p.wp != nullptr) {
+    // ------------------------------------------------ W4 unpack (warps 2-3)
+    // Per stage: the packed rows (BN x 64 bytes, TMA-loaded into the upper half
+    // of the B buffer) -> registers -> both warps synced -> 128 u8 codes per row
+    // in the 128B-swizzled layout TMA would have written (16-byte chunk c of row
+    // r at c ^ (r & 7)) over the whole buffer -> async-proxy fence -> full_bar.
+    constexpr int kItems = BN * 4 / 64;   // 16-byte packed chunks per thread
+    const int ut = threadIdx.x - 64;      // 0..63
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = tile_start; tile < num_tiles; tile += tile_step) {
+      if (!tile_active(tile)) continue;
+      const int num_kb = tile_kb((tile % p.num_n_tiles) * BN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&raw_bar[stage], phase);
+        uint8_t* bs = smem_b + stage * Cfg::kBBytes;
+        uint4 pk[kItems];
+#pragma unroll
+        for (int i = 0; i < kItems; ++i)
+          pk[i] = *reinterpret_cast<const uint4*>(bs + BN * 64 + 16 * (ut + 64 * i));
+        named_bar_sync(3, 64);   // every packed byte read before the buffer is rewritten
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+          const int it = ut + 64 * i, r = it >> 2, q = it & 3;
+          uint4 lo, hi;
+          unpack_nibbles(pk[i], lo, hi);
+          *reinterpret_cast<uint4*>(bs + r * 128 + (((2 * q) ^ (r & 7)) << 4)) = lo;
+          *reinterpret_cast<uint4*>(bs + r * 128 + (((2 * q + 1) ^ (r & 7)) << 4)) = hi;
+        }
+        fence_proxy_async_smem();   // generic-proxy writes -> visible to the MMA (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_bar[stage]);
+        if (++stage == Cfg::kStages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -534,6 +599,22 @@ int make_map_u8(CUtensorMap* map, const void* base, int rows, int K, long long l
   return r == CUDA_SUCCESS ? QCB_OK : QCB_ERR_CUDA;
 }
 
+// W4 packed weights [rows][ld] bytes: box 64 bytes (128 codes) x box_rows, no
+// swizzle (the unpack warps read rows densely and write the SW128 layout).
+static int make_map_packed(CUtensorMap* map, const void* base, int rows, long long ld,
+                           int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return QCB_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? QCB_OK : QCB_ERR_CUDA;
+}
+
 // 2-D f32 output [rows][ld] (N valid columns), box 32 x 32, 128-byte swizzle.
 static int make_map_out(CUtensorMap* map, const void* base, long long rows, int N, long long ld) {
   auto enc = get_encode_fn();
@@ -580,8 +661,14 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   CUtensorMap ma, mb;
   int rc = make_map_u8(&ma, g->a_codes, g->M, g->K, g->lda, kBlockM);
   if (rc) return rc;
-  rc = make_map_u8(&mb, g->w_codes, g->N, g->K, g->ldw, PAIR ? BN / 2 : BN);
-  if (rc) return rc;
+  if (g->w_packed) {
+    if (PAIR) return QCB_ERR_CONFIG;
+    rc = make_map_packed(&mb, g->w_packed, g->N, g->ldwp, BN);
+    if (rc) return rc;
+  } else {
+    rc = make_map_u8(&mb, g->w_codes, g->N, g->K, g->ldw, PAIR ? BN / 2 : BN);
+    if (rc) return rc;
+  }
   GemmParams p{};
   p.M = g->M;
   p.N = g->N;
@@ -605,6 +692,8 @@ static int launch_bn(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {
   p.gate = g->gate;
   p.gate_scalar = g->gate_scalar;
   p.seg_active = g->seg_active;
+  p.wp = g->w_packed;
+  p.ldwp = g->ldwp;
   if (grp) {
     p.group_n = grp->n;
     p.group_k = grp->k;
@@ -700,7 +789,8 @@ static bool use_pair(const QcbGemm* g, int bn) {
     const char* e = getenv("QCB_GEMM_PAIR");
     env = e ? atoi(e) : 0;
   }
-  return env != 0 && g->seg_active == nullptr && g->M >= 2 * kBlockM && bn >= 64;
+  return env != 0 && g->seg_active == nullptr && g->M >= 2 * kBlockM && bn >= 64 &&
+         g->w_packed == nullptr;
 }
 
 template <int BN>
@@ -741,12 +831,37 @@ __global__ void __launch_bounds__(32 * kSmallWarps) gemm_u8_small_m(const QcbGem
   __syncthreads();
   const int n = blockIdx.x * kSmallWarps + warp;
   if (n >= g.N) return;
-  const uint8_t* wc = g.w_codes + (long long)n * g.ldw;
   uint32_t acc[kSmallM];
 #pragma unroll
   for (int m = 0; m < kSmallM; ++m) acc[m] = 0u;
+  if (g.w_packed) {   // W4: 16 packed bytes = 32 codes = two A chunks
+    const uint8_t* wp = g.w_packed + (long long)n * g.ldwp;
+    for (int pc = lane; 32 * pc < Kp; pc += 32) {
+      uint4 lo, hi;
+      unpack_nibbles(__ldcs(reinterpret_cast<const uint4*>(wp + 16 * pc)), lo, hi);
+      const bool two = 32 * pc + 16 < Kp;
+#pragma unroll
+      for (int m = 0; m < kSmallM; ++m) {
+        if (m < M) {
+          const uint4 a = *reinterpret_cast<const uint4*>(a_sm + m * Kp + 32 * pc);
+          acc[m] = __dp4a(a.x, lo.x, acc[m]);
+          acc[m] = __dp4a(a.y, lo.y, acc[m]);
+          acc[m] = __dp4a(a.z, lo.z, acc[m]);
+          acc[m] = __dp4a(a.w, lo.w, acc[m]);
+          if (two) {
+            const uint4 b = *reinterpret_cast<const uint4*>(a_sm + m * Kp + 32 * pc + 16);
+            acc[m] = __dp4a(b.x, hi.x, acc[m]);
+            acc[m] = __dp4a(b.y, hi.y, acc[m]);
+            acc[m] = __dp4a(b.z, hi.z, acc[m]);
+            acc[m] = __dp4a(b.w, hi.w, acc[m]);
+          }
+        }
+      }
+    }
+  }
+  const uint8_t* wc = g.w_packed ? nullptr : g.w_codes + (long long)n * g.ldw;
   constexpr int kBatch = 8;   // 16-byte weight loads in flight per lane
-  for (int c0 = lane; c0 < Kp / 16; c0 += 32 * kBatch) {
+  for (int c0 = lane; wc != nullptr && c0 < Kp / 16; c0 += 32 * kBatch) {
     uint4 w[kBatch];
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
@@ -805,6 +920,37 @@ __global__ void __launch_bounds__(32 * kSmallWarps) gemm_u8_small_m(const QcbGem
     }
   }
   g.out[orow * g.ldo + n] = y;
+}
+
+// W4 weight packing (qcb_pack_w4): one thread per 16 packed bytes (32 codes)
+__global__ void pack_w4_k(const uint8_t* codes, long long ldk, int N, int K, uint8_t* packed,
+                          long long ldwp) {
+  const long long per_row = ldwp / 16;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= per_row * N) return;
+  const int n = (int)(i / per_row), c = (int)(i - (long long)n * per_row);
+  const uint8_t* src = codes + (long long)n * ldk + 32 * c;
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int k = 32 * c + 8 * j + 2 * b;
+      const uint32_t lo = k < K ? (src[8 * j + 2 * b] & 0xFu) : 0u;
+      const uint32_t hi = k + 1 < K ? (src[8 * j + 2 * b + 1] & 0xFu) : 0u;
+      v |= (lo | (hi << 4)) << (8 * b);
+    }
+    w[j] = v;
+  }
+  *reinterpret_cast<uint4*>(packed + (long long)n * ldwp + 16 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+int pack_w4_launch(const uint8_t* codes, long long ldk, int N, int K, uint8_t* packed,
+                   long long ldwp, cudaStream_t st) {
+  const long long n = (ldwp / 16) * N;
+  pack_w4_k<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(codes, ldk, N, K, packed, ldwp);
+  return launch_status();
 }
 
 int gemm_u8_launch(const QcbGemm* g, cudaStream_t st, const GemmGroup* grp) {

@@ -64,11 +64,27 @@ class PackedWeight:
     w_deq: Optional[torch.Tensor] = None        # f32 [K][N] dequantized (weight-only mode)
     w_eff: Optional[torch.Tensor] = None
     chan_recip: Optional[torch.Tensor] = None   # f64 [K] 1/c (quantizer fast path)
+    packed: Optional[torch.Tensor] = None       # u8 [N][ldwp] W4 nibbles (bits <= 4)
+
+
+def pack_w4(codes: torch.Tensor, K: int, stream=None) -> torch.Tensor:
+    """Nibble-pack <= 4-bit K-major codes [N][ldk] -> [N][ldwp] (qcb_pack_w4)."""
+    Nn = codes.shape[0]
+    ldwp = (((K + 1) // 2) + 63) // 64 * 64
+    out = torch.zeros((Nn, ldwp), dtype=torch.uint8, device=codes.device)
+    N.check(N.lib().qcb_pack_w4(N.ptr(codes), codes.stride(0), Nn, K, N.ptr(out), ldwp,
+                                N.stream_ptr(stream)), "pack_w4")
+    count(1)
+    return out
 
 
 def weight_prep(w: torch.Tensor, bits: int, chan_scale: Optional[torch.Tensor] = None,
                 signs: Optional[torch.Tensor] = None, keep_deq: bool = False,
-                keep_eff: bool = False, stream=None) -> PackedWeight:
+                keep_eff: bool = False, stream=None, pack4: bool = False) -> PackedWeight:
+    """Per-channel weight codes (runtime.py:40-61).  pack4 (bits <= 4) also
+    stores the codes nibble-packed; the u8 GEMM then streams half the weight
+    bytes and unpacks them in shared memory (slower than the u8 operand when
+    the weights are L2-resident, as at STDiT sizes: a memory-footprint option)."""
     dev = _dev()
     w = w.to(dev, torch.float32).contiguous()
     K, Nn = w.shape
@@ -89,8 +105,11 @@ def weight_prep(w: torch.Tensor, bits: int, chan_scale: Optional[torch.Tensor] =
                         N.ptr(w_deq), N.ptr(rc))
     N.check(N.lib().qcb_weight_prep(C.byref(d), N.stream_ptr(stream)), "weight_prep")
     count(1)
+    if pack4 and bits > 4:
+        raise ValueError("nibble packing needs codes of at most 4 bits")
+    packed = pack_w4(codes, K, stream) if pack4 else None
     return PackedWeight(codes, scale, zero, colsum, K, Nn, bits, chan_scale, signs, w_deq, w_eff,
-                        rc)
+                        rc, packed)
 
 
 @dataclass
@@ -211,6 +230,8 @@ def gemm_u8(a: ActCodes, w: PackedWeight, M: Optional[int] = None, out=None,
     g.a_codes, g.lda = N.ptr(a.codes), a.codes.stride(0)
     g.a_scale, g.a_zero, g.a_rowsum = N.ptr(a.scale), N.ptr(a.zero), N.ptr(a.rowsum)
     g.w_codes, g.ldw = N.ptr(w.codes), w.codes.stride(0)
+    if w.packed is not None:
+        g.w_packed, g.ldwp = N.ptr(w.packed), w.packed.stride(0)
     g.w_scale, g.w_zero, g.w_colsum = N.ptr(w.scale), N.ptr(w.zero), N.ptr(w.colsum)
     g.out, g.ldo = N.ptr(out), ldo if ldo is not None else out.stride(0)
     g.out_row0, g.resid, g.resid_row0 = N.ptr(out_row0), N.ptr(resid), N.ptr(resid_row0)
@@ -338,6 +359,20 @@ def ddpm(x, eps, c1: float, c2: float, noise=None, c3: float = 0.0, out=None, st
     d = N.QcbDdpm(N.ptr(x), N.ptr(eps), N.ptr(noise), N.ptr(out), x.numel(), c1, c2, c3,
                   1.0 / float(c2), int(seed), int(off), 1 if noise_gen is not None else 0)
     N.check(N.lib().qcb_ddpm_step(C.byref(d), N.stream_ptr(stream)), "ddpm_step")
+    count(1)
+    return out
+
+
+def cfg_combine(eps_c: torch.Tensor, eps_u: torch.Tensor, scale: float, out=None,
+                stream=None) -> torch.Tensor:
+    """Classifier-free guidance eps_u + scale * (eps_c - eps_u) (extension)."""
+    if out is None:
+        out = torch.empty_like(eps_c)
+    n = eps_c.numel()
+    if eps_u.numel() != n or out.numel() != n:
+        raise DimensionError("cfg_combine operands must share a size")
+    N.check(N.lib().qcb_cfg_combine(N.ptr(eps_c), N.ptr(eps_u), float(scale), N.ptr(out), n,
+                                    N.stream_ptr(stream)), "cfg_combine")
     count(1)
     return out
 

@@ -149,6 +149,10 @@ class EngineOptions:
                                    # both give the reference's mm bit for bit
     decisions: str = "per_video"   # "per_video" (reference semantics) | "synchronized"
                                    # (one policy for the whole batch, all ranks)
+    pack_w4: bool = False               # W4 layers' weights nibble-packed (footprint option)
+    cfg_scale: Optional[float] = None   # classifier-free guidance (EXTENSION, no reference:
+                                        # SPEC.md:468): each video runs a cond and an
+                                        # uncond (null cond) branch as two slots
     record_features: bool = False
 
 
@@ -217,6 +221,10 @@ class QuantCacheEngine:
         if self.opts.decisions not in ("per_video", "synchronized"):
             raise ValueError("decisions must be 'per_video' or 'synchronized'")
         self.sync = self.opts.decisions == "synchronized"
+        self.cfg_scale = self.opts.cfg_scale
+        if self.cfg_scale is not None and (self.sync or max_videos % 2):
+            raise ValueError("CFG needs per-video decisions and an even slot count "
+                             "(2 branches per video)")
         self.sync_group = None    # process group of the synchronised mode (None: default)
         self._upload_weights(act_absmax or {})
         self._alloc()
@@ -251,7 +259,8 @@ class QuantCacheEngine:
                     else:
                         tr = (None, None)
                     pk[site] = Dv.weight_prep(self._t(w), self.weight_bits[l], tr[0], tr[1],
-                                              keep_deq=not tog.aigq_acts)
+                                              keep_deq=not tog.aigq_acts,
+                                              pack4=self.opts.pack_w4 and self.weight_bits[l] <= 4)
             self.fpw.append(fp)
             self.packed.append(pk)
         self.head_w = self._t(m.head_w)
@@ -283,6 +292,9 @@ class QuantCacheEngine:
         self.xe = torch.zeros((rows, K4), dtype=torch.float32, device=dev)
         self.hid = torch.zeros((rows, K4), dtype=torch.float32, device=dev)
         self.eps = torch.zeros((rows, d), dtype=torch.float32, device=dev)
+        # guided eps per video (CFG extension)
+        self.eps_cfg = torch.zeros((nv // 2, self.S, d), dtype=torch.float32, device=dev) \
+            if self.opts.cfg_scale is not None else None
         self.q2 = torch.zeros_like(self.q)
         # bf16 q/k/v written by the integer GEMMs' epilogue for the bf16 attention
         self.qkv16 = [torch.zeros((rows, d), dtype=torch.bfloat16, device=dev) for _ in range(3)] \
@@ -611,10 +623,17 @@ class QuantCacheEngine:
         (t, x_t [nv,S,d], [block outputs [nv,S,d] per layer]) host copies, like
         the reference's generate(collect_features=...) (sampler.py:113-126).
         Returns (latents f32 [nv][F][T][d] on host, or a CUDA tensor with
-        return_device, and traces per video)."""
-        nv = len(seeds)
+        return_device, and traces per video).
+
+        With EngineOptions.cfg_scale (classifier-free guidance, an extension)
+        every video occupies two slots, its cond and its uncond (zero cond)
+        branch, each with its own cache / prune / bit decisions; the returned
+        traces are per slot (cond, uncond, cond, ...), the latents per video."""
+        cfgm = self.cfg_scale is not None
+        n_videos = len(seeds)
+        nv = 2 * n_videos if cfgm else n_videos
         if nv > self.nv:
-            raise ValueError(f"engine sized for {self.nv} videos")
+            raise ValueError(f"engine sized for {self.nv} slots")
         L, S, d, T = self.L, self.S, self.d, self.T
         F, Tk = self.cfg.frames, self.cfg.tokens_per_frame
         # every launch, copy, event and synchronize of this call goes to the
@@ -622,15 +641,19 @@ class QuantCacheEngine:
         st = self.stream = torch.cuda.current_stream(self.dev)
         self.pol.zero_()
         vids = []
-        for v, seed in enumerate(seeds):
-            vs = VideoState(SlotPool(v * self.P, self.P), np.random.default_rng(seed),
+        for v in range(nv):
+            i = v // 2 if cfgm else v          # video of slot v
+            vs = VideoState(SlotPool(v * self.P, self.P), np.random.default_rng(seeds[i]),
                             cache=[None] * L, prev=[None] * L)
             vs.x = vs.pool.alloc()
-            if x0_dev is not None:
+            if cfgm and v % 2:                # uncond branch: the cond branch's x0, null cond
+                self.slot_view(vs.x).copy_(self.slot_view(vids[v - 1].x))
+                self.cond[v].zero_()
+            elif x0_dev is not None:
                 # async from pinned host memory (the first decision sync of the
                 # loop orders it before generate() returns); device sources too
-                self.slot_view(vs.x).copy_(x0_dev[v].reshape(S, d), non_blocking=True)
-                self.cond[v].copy_(cond_dev[v], non_blocking=True)
+                self.slot_view(vs.x).copy_(x0_dev[i].reshape(S, d), non_blocking=True)
+                self.cond[v].copy_(cond_dev[i], non_blocking=True)
             else:
                 x0 = vs.rng.standard_normal((F, Tk, d)).astype(np.float32)
                 cond = vs.rng.standard_normal(self.c).astype(np.float32)
@@ -688,8 +711,9 @@ class QuantCacheEngine:
             for vs in vids:
                 vs.seen += 1
             self._run_step(t, vids, act_tab, abits_of, collect_features, gen)
+        outv = vids[::2] if cfgm else vids   # the latent of each video
         if return_device:
-            out = torch.stack([self.slot_view(vs.x) for vs in vids]).reshape(nv, F, Tk, d)
+            out = torch.stack([self.slot_view(vs.x) for vs in outv]).reshape(len(outv), F, Tk, d)
             st.synchronize()
             self._trace_steps(traces, range(t_built, -1, -1))
             for vs, tr in zip(vids, traces):
@@ -699,14 +723,14 @@ class QuantCacheEngine:
         # (a new array per call, reused only once the caller drops it) filled by
         # async per-video D2H copies on the engine stream (a pageable .cpu() of
         # the stacked latents ran at ~2 GB/s: 36 ms for 4 C3 videos)
-        host = torch.empty((nv, S, d), dtype=torch.float32, pin_memory=True)
-        for v, vs in enumerate(vids):
+        host = torch.empty((len(outv), S, d), dtype=torch.float32, pin_memory=True)
+        for v, vs in enumerate(outv):
             host[v].copy_(self.slot_view(vs.x), non_blocking=True)
         st.synchronize()
         self._trace_steps(traces, range(t_built, -1, -1))
         for vs, tr in zip(vids, traces):
             vs.trace = tr
-        return host.numpy().reshape(nv, F, Tk, d), traces
+        return host.numpy().reshape(len(outv), F, Tk, d), traces
 
     def _plan_step(self, t: int, vids):
         """Per-video plan of step t: V reductions, plan_reuse + SRAP (unless the
@@ -927,16 +951,26 @@ class QuantCacheEngine:
                 vs.pool.dec(vs.head_src)
                 vs.head_src = vs.pool.inc(cur[v])
         with self._ph("sampler"):
+            # CFG (extension): slots (2i, 2i+1) are video i's cond / uncond
+            # branches; one DDPM update per video from the guided eps, its
+            # result copied into the uncond branch's own slot
+            step = 2 if self.cfg_scale is not None else 1
             if t > 0 and self.opts.noise == "numpy":
-                for v, vs in enumerate(vids):
-                    self.noise_host[v].numpy()[:] = vs.rng.standard_normal(
+                for i, v in enumerate(range(0, nv, step)):
+                    self.noise_host[i].numpy()[:] = vids[v].rng.standard_normal(
                         (F, Tk, d)).astype(np.float32).reshape(S, d)
-                self.noise_dev[:nv].copy_(self.noise_host[:nv], non_blocking=True)
+                self.noise_dev[:nv // step].copy_(self.noise_host[:nv // step], non_blocking=True)
             quads = (S * d + 3) // 4
             a_t = self.ab[t]
             for v, vs in enumerate(vids):
+                if v % step:
+                    continue   # an uncond branch: updated with its cond branch below
+                i = v // step   # video index (noise stream, guided eps)
                 new = vs.pool.alloc()
                 eps_v = self.eps[v * self.Sp: v * self.Sp + S]
+                if step == 2:
+                    eps_v = Dv.cfg_combine(eps_v, self.eps[(v + 1) * self.Sp:(v + 1) * self.Sp + S],
+                                           self.cfg_scale, out=self.eps_cfg[i])
                 if t > 0:
                     a_p = self.ab[t - 1]
                     alpha = a_t / a_p
@@ -945,18 +979,28 @@ class QuantCacheEngine:
                     dev_noise = gen is not None and t > 1
                     Dv.ddpm(self.slot_view(vs.x), eps_v, float(beta / np.sqrt(1.0 - a_t)),
                             float(np.sqrt(alpha)),
-                            self.noise_dev[v] if (t > 1 and not dev_noise) else None, c3,
+                            self.noise_dev[i] if (t > 1 and not dev_noise) else None, c3,
                             out=self.slot_view(new),
-                            noise_gen=(gen[v], t * quads) if dev_noise else None)
+                            noise_gen=(gen[i], t * quads) if dev_noise else None)
                 else:
                     Dv.ddpm(self.slot_view(vs.x), eps_v, float(np.sqrt(1.0 - self.ab[0])),
                             float(np.sqrt(self.ab[0])), out=self.slot_view(new))
-                vs.pool.dec(cur[v])
-                # finalize_step: latent history window (schedule.py:353-357)
-                vs.hist.append(vs.x)
-                if len(vs.hist) > self.th.history_k:
-                    vs.pool.dec(vs.hist.pop(0))
-                vs.x = new
+                news = [(v, new)]
+                if step == 2:
+                    vu = vids[v + 1]
+                    new_u = vu.pool.alloc()
+                    N.check(N.lib().qcb_copy_async(N.ptr(self.slot_view(new_u)),
+                                                   N.ptr(self.slot_view(new)), S * d * 4, sp),
+                            "copy_async")
+                    news.append((v + 1, new_u))
+                for w, nw in news:
+                    ws = vids[w]
+                    ws.pool.dec(cur[w])
+                    # finalize_step: latent history window (schedule.py:353-357)
+                    ws.hist.append(ws.x)
+                    if len(ws.hist) > self.th.history_k:
+                        ws.pool.dec(ws.hist.pop(0))
+                    ws.x = nw
         if fast:
             # prev references of the step (schedule.py:349-351): a reused layer's
             # output is its cache entry, a pruned layer passes its input through

@@ -275,3 +275,58 @@ class TestLayerNormOrder:
             for o, c in enumerate(cs):
                 check_quant(res[o], O.rotate_act_fwht(h, c, 0), v, slice(v * S, (v + 1) * S),
                             K, 8, o)
+
+
+class TestPackedW4:
+    """W4 weights stored nibble-packed ([N][K/2], quant.py:206 BIT_LEVELS 4) and
+    unpacked to u8 in shared memory by the GEMM's producer warps (tcgen05 has no
+    4-bit integer MMA): accumulators and outputs identical to the u8 operand."""
+
+    @pytest.mark.parametrize("M,K,N,ab", [(16384, 1152, 1152, 8), (16384, 4608, 1152, 6),
+                                          (4096, 1152, 4608, 8), (300, 200, 72, 8),
+                                          (5, 200, 72, 8), (16, 1152, 300, 6)])
+    def test_packed_equals_u8(self, D, M, K, N, ab):
+        from paper_2503_06545_b200 import _native as Nat
+        rng = np.random.default_rng(M + K + N)
+        ca = rng.integers(0, 2 ** ab, size=(M, K)).astype(np.uint8)
+        cw = rng.integers(0, 16, size=(K, N)).astype(np.uint8)
+        sa = O.scale_up16(rng.uniform(1e-3, 3e-2, size=1))
+        za = rng.integers(0, 2 ** ab, size=1).astype(np.int32)
+        sw = O.scale_up16(rng.uniform(1e-3, 1e-2, size=N))
+        zw = rng.integers(0, 16, size=N).astype(np.int32)
+        a = D.ActCodes(t(np.pad(ca, ((0, 0), (0, D.round16(K) - K)))),
+                       t(ca.astype(np.int64).sum(1).astype(np.int32)), t(sa), t(za), K)
+        cwp = np.zeros((N, D.round16(K)), np.uint8)
+        cwp[:, :K] = cw.T
+        w8 = D.PackedWeight(t(cwp), t(sw), t(zw), t(cw.astype(np.int64).sum(0).astype(np.int32)),
+                            K, N, 4)
+        packed = D.pack_w4(w8.codes, K)
+        # the packed bytes: low nibble = even k, high nibble = odd k, zero padding
+        pk = packed.cpu().numpy()
+        assert pk.shape[1] % 64 == 0
+        un = np.zeros((N, 2 * pk.shape[1]), np.uint8)
+        un[:, 0::2], un[:, 1::2] = pk & 15, pk >> 4
+        assert np.array_equal(un[:, :K], cw.T) and not un[:, K:].any()
+        w4 = D.PackedWeight(w8.codes, w8.scale, w8.zero, w8.colsum, K, N, 4, packed=packed)
+        acc = exact_acc(ca, np.repeat(za, M), cw, zw)
+        got = D.gemm_u8(a, w4, epilogue=Nat.EPI_ACC)
+        assert torch.equal(got.to(torch.float64), acc)
+        for mode in (Nat.EPI_STORE, Nat.EPI_GATE_RESID):
+            resid = torch.randn((M, N), generator=torch.Generator().manual_seed(3)).cuda()
+            o4 = D.gemm_u8(a, w4, epilogue=mode, resid=resid, gate=np.float32(0.5))
+            o8 = D.gemm_u8(a, w8, epilogue=mode, resid=resid, gate=np.float32(0.5))
+            assert torch.equal(o4, o8), mode
+
+    def test_weight_prep_packs_w4(self, D):
+        rng = np.random.default_rng(8)
+        w = (rng.standard_normal((1152, 384)) / 34).astype(np.float32)
+        c = np.exp(0.3 * rng.standard_normal(1152))
+        pw = D.weight_prep(t(w), 4, t(c), t(D.sign_vector(0, 1024)), pack4=True)
+        assert pw.packed is not None
+        pk = pw.packed.cpu().numpy()
+        un = np.zeros((384, 2 * pk.shape[1]), np.uint8)
+        un[:, 0::2], un[:, 1::2] = pk & 15, pk >> 4
+        assert np.array_equal(un[:, :1152], pw.codes.cpu().numpy()[:, :1152])
+        assert D.weight_prep(t(w), 4).packed is None
+        with pytest.raises(ValueError):
+            D.weight_prep(t(w), 6, pack4=True)
