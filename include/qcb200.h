@@ -63,7 +63,9 @@ enum {
 };
 
 /* Activation prologues. */
-enum { QCB_PRO_NONE = 0, QCB_PRO_LN_MOD = 1, QCB_PRO_GELU = 2 /* f32(gelu_f64(x)), model.py:197 */ };
+enum { QCB_PRO_NONE = 0, QCB_PRO_LN_MOD = 1, QCB_PRO_GELU = 2 /* f32(gelu_f64(x)), model.py:197 */,
+       QCB_PRO_BF16 = 3 /* x holds bf16 rows (ldx in bf16 elements), widened exactly;
+                           K = 1024 + tail, rows 16-byte aligned */ };
 
 #define QCB_MAX_LAYERS 64
 #define QCB_MAX_HIST 8

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqcb200.so")
 QCB_OK, QCB_ERR_DIM, QCB_ERR_CONFIG, QCB_ERR_OVERFLOW, QCB_ERR_VALUE, QCB_ERR_TYPE, \
     QCB_ERR_CUDA = range(7)
 EPI_STORE, EPI_GELU, EPI_GATE_RESID, EPI_RESID, EPI_ACC, EPI_BIAS, EPI_STORE_BF16 = range(7)
-PRO_NONE, PRO_LN_MOD, PRO_GELU = 0, 1, 2
+PRO_NONE, PRO_LN_MOD, PRO_GELU, PRO_BF16 = 0, 1, 2, 3
 ACT_RECOMPUTE, ACT_REUSE, ACT_PRUNE = 0, 1, 2
 MAX_LAYERS = 64
 

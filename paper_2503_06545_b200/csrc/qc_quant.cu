@@ -840,6 +840,11 @@ struct V4Smem {
   double red[2][kV4Threads / 32]; // LN partial sums (mean, variance)
 };
 
+// element e of a bf16 row held in a float-typed shared buffer, widened (exact)
+QC_DEV float bf16_at(const float* row, int e) {
+  return __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(row)[e] << 16);
+}
+
 // Radix-2^Q butterflies over groups of 2^Q consecutive registers.
 template <int Q>
 QC_DEV void fwht_regs(double (&v)[16]) {
@@ -878,7 +883,8 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rl = tid / TPR, lt = tid % TPR;
   const int K = p.K, T = K - B;
-  const uint32_t row_bytes = (uint32_t)K * 4u;
+  // kPro 3: bf16 input rows (the attention output), widened exactly to f32
+  const uint32_t row_bytes = (uint32_t)K * (kPro == 3 ? 2u : 4u);
   double* const fa = sm.f[rl] + lt + (lt >> 4);
   double* const fb = sm.f[rl] + 17 * lt;
   double* const fc = sm.f[rl] + (lt & 15) + 17 * GS * (lt >> 4);
@@ -910,7 +916,11 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas)
     long long in_row, out_row;
     v2_row_index(p, gr, seg, mrow, in_row, out_row);
     mbar_arrive_expect_tx(&sm.full[rl][k % kV4Bufs], row_bytes);
-    bulk_load_hint(sm.xrow[rl][k % kV4Bufs], p.x + in_row * p.ldx, row_bytes,
+    bulk_load_hint(sm.xrow[rl][k % kV4Bufs],
+                   kPro == 3 ? static_cast<const void*>(reinterpret_cast<const uint16_t*>(p.x) +
+                                                        in_row * p.ldx)
+                             : static_cast<const void*>(p.x + in_row * p.ldx),
+                   row_bytes,
                    &sm.full[rl][k % kV4Bufs],
                    pol_stream);
   };
@@ -965,11 +975,11 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas)
     const float* xs = sm.xrow[rl][k % kV4Bufs];
     float h[16], ht[kV4Tail];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) h[j] = xs[lt + TPR * j];
+    for (int j = 0; j < 16; ++j) h[j] = kPro == 3 ? bf16_at(xs, lt + TPR * j) : xs[lt + TPR * j];
 #pragma unroll
     for (int i = 0; i < kV4Tail; ++i) {
       const int t = lt + TPR * i;
-      ht[i] = (t < T) ? xs[B + t] : 0.f;
+      ht[i] = (t < T) ? (kPro == 3 ? bf16_at(xs, B + t) : xs[B + t]) : 0.f;
     }
     if (kPro == 1) {
       // mean and variance in numpy's pairwise order (qc_pairwise.cuh) by the
@@ -1533,6 +1543,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
   const int wpr = b / 1024;
   const bool v2 = (b == 1024 || b == 2048 || b == 4096) && (q->K - b) <= 8 * 32 * wpr &&
                   (q->K % 4 == 0) && (q->ldx % 4 == 0) && (q->ldc % 4 == 0 || !q->codes[0]);
+  if (q->prologue == QCB_PRO_BF16 && !v2) return QCB_ERR_CONFIG;
   if (v2) {
     uint8_t* ws = reinterpret_cast<uint8_t*>(q->workspace);
     size_t off = align256((size_t)8 * 3 * q->nseg);
@@ -1546,6 +1557,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
     // signed reciprocal table (qcb_weight_prep's chan_recip_out), v3 the plain one
     const bool v4 = (q->K - b) <= kV4Tail * (b / 16) &&
                     (reinterpret_cast<uintptr_t>(q->x) & 15) == 0;
+    if (q->prologue == QCB_PRO_BF16 && !v4) return QCB_ERR_CONFIG;
     for (int o = 0; o < q->n_out; ++o) {
       a.rc[o] = rcbuf + (size_t)o * q->K;
       if (q->chan_scale[o] && q->chan_recip[o] && v4) {
@@ -1576,11 +1588,13 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
       // 2 CTAs per SM (128 registers) for every prologue: at 3 CTAs per SM the
       // 85-register cap spills (measured 10-15% slower)
       const bool ln = q->prologue == QCB_PRO_LN_MOD;
-      const int pro = ln ? 1 : (q->prologue == QCB_PRO_GELU ? 2 : 0);
+      const int pro = ln ? 1 : (q->prologue == QCB_PRO_GELU ? 2 :
+                                (q->prologue == QCB_PRO_BF16 ? 3 : 0));
+      if (pro == 3 && (b != 1024 || (q->ldx % 8))) return QCB_ERR_CONFIG;
       const size_t ln_bytes = ln ? (size_t)16 * q->K : 0;
       const int cap = num_sms() * 2;
       if (b1 > cap) b1 = cap;
-      static bool a41g = false, a42g = false, a44g = false;
+      static bool a41g = false, a42g = false, a44g = false, a41b = false;
       switch (b * 4 + pro) {
 #define QC_AQ4(BB, P2, MC, PRO, FLAG)                                                          \
   allow_max_smem(aq4_pass1<BB, P2, MC, PRO>, FLAG);                                            \
@@ -1590,6 +1604,7 @@ int act_quant_launch(const QcbActQuant* q, cudaStream_t st) {
         case 4096: QC_AQ4(1024, true, 2, 0, a41)
         case 4097: QC_AQ4(1024, true, 2, 1, a41l)
         case 4098: QC_AQ4(1024, true, 2, 2, a41g)
+        case 4099: QC_AQ4(1024, true, 2, 3, a41b)
         case 8192: QC_AQ4(2048, false, 2, 0, a42)
         case 8193: QC_AQ4(2048, false, 2, 1, a42l)
         case 8194: QC_AQ4(2048, false, 2, 2, a42g)

@@ -151,7 +151,10 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
     transforms[o] = (chan_scale f64 [K], signs f32 [b]) or None (no transform).
     ln = (gamma, beta) enables the LN prologue (None = raw rows)."""
     dev = _dev()
-    assert x.dtype == torch.float32 and x.is_cuda
+    assert x.dtype in (torch.float32, torch.bfloat16) and x.is_cuda
+    bf16_in = x.dtype == torch.bfloat16   # rows widened exactly (no prologue)
+    if bf16_in and (ln is not None or gelu):
+        raise ValueError("bf16 input rows take no prologue")
     K = x.shape[-1]
     ldx = x.stride(0) if x.dim() == 2 else K
     rows_total = x.shape[0] if x.dim() == 2 else x.numel() // K
@@ -181,6 +184,8 @@ def act_quant(x: torch.Tensor, bits: int, transforms: Sequence[Optional[tuple]],
         q.ln_g, q.ln_b = N.ptr(ln[0]), N.ptr(ln[1])
     elif gelu:
         q.prologue = N.PRO_GELU   # f32(gelu_f64(x)) applied to the input rows
+    elif bf16_in:
+        q.prologue = N.PRO_BF16
     else:
         q.prologue = N.PRO_NONE
     q.mod_scale1, q.mod_shift = float(mod[0]), float(mod[1])

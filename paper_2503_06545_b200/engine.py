@@ -211,6 +211,7 @@ class QuantCacheEngine:
         self.quant_profile: Optional[list] = None  # set to [] to time every act_quant
         self.phase_profile: Optional[list] = None  # set to [] to time the other phases
         self.att_flops = 0.0                       # self-attention flops while phase-profiled
+        self.attn_bf16_direct = True               # sta_o quantizer reads the bf16 SDPA rows
         self.head_calls = 0                        # video-steps whose eps was needed
         self.head_skipped = 0                      # ... of which the held eps was exact
         self.host_profile: Optional[list] = None   # set to []: host s from plan sync to the
@@ -485,6 +486,8 @@ class QuantCacheEngine:
         return h, None
 
     def _attention(self, q, k, v, out, nseg, Skv, kv_stride):
+        """Returns None, or (bf16 rows [nseg * S][d], their per-segment first-row
+        table) when the fast path's output can feed the next quantizer directly."""
         S, Sp, d, H = self.S, self.Sp, self.d, self.H
         if self.opts.attention == "fast" and Skv > 1:
             dh = d // H
@@ -495,8 +498,15 @@ class QuantCacheEngine:
             o = torch.nn.functional.scaled_dot_product_attention(
                 qq if qq.dtype == bf else qq.to(bf), kk if kk.dtype == bf else kk.to(bf),
                 vv if vv.dtype == bf else vv.to(bf))
-            out[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].copy_(o.permute(0, 2, 1, 3))
-            return
+            ob = o.permute(0, 2, 1, 3)
+            if (self.attn_bf16_direct and self.tog.aigq_weights and self.tog.aigq_acts
+                    and ob.is_contiguous() and d % 8 == 0 and ob.data_ptr() % 16 == 0):
+                # the sta_o quantizer widens the bf16 rows itself (exact): no
+                # bf16 -> f32 copy pass
+                rows = ob.reshape(nseg * S, d)
+                return rows, self._upload_idx([[v * S for v in range(nseg)]])[0]
+            out[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].copy_(ob)
+            return None
         a = N.QcbAttention(N.ptr(q), q.stride(0), N.ptr(k), k.stride(0), N.ptr(v), v.stride(0),
                            N.ptr(out), out.stride(0), S, Skv, H, d // H, nseg, Sp, kv_stride,
                            Sp, S)
@@ -520,11 +530,18 @@ class QuantCacheEngine:
                    outs=qkv, sites=("sta_q", "sta_k", "sta_v"),
                    epi=N.EPI_STORE_BF16 if qkv is self.qkv16 else N.EPI_STORE)
         with self._ph("attention"):
-            self._attention(qkv[0], qkv[1], qkv[2], self.att, n, self.S, self.Sp)
+            ob = self._attention(qkv[0], qkv[1], qkv[2], self.att, n, self.S, self.Sp)
         if self.phase_profile is not None:   # 4 S^2 d flops per video (QK^T and PV)
             self.att_flops += 4.0 * self.S * self.S * self.d * n
-        self._site(l, "sta_o", bits, self.att, n, epi=N.EPI_GATE_RESID, out=A,
-                   out_row0=out_row0, resid=A, resid_row0=xin_row0, gate=g1)
+        if ob is not None and int_path:   # quantizer input: the bf16 attention rows
+            self._site(l, "sta_o", bits, ob[0], n, x_row0=ob[1], epi=N.EPI_GATE_RESID, out=A,
+                       out_row0=out_row0, resid=A, resid_row0=xin_row0, gate=g1)
+        else:
+            if ob is not None:
+                self.att[:n * self.Sp].view(n, self.Sp, self.d)[:, :self.S].copy_(
+                    ob[0].view(n, self.S, self.d))
+            self._site(l, "sta_o", bits, self.att, n, epi=N.EPI_GATE_RESID, out=A,
+                       out_row0=out_row0, resid=A, resid_row0=xin_row0, gate=g1)
         # cross-attention on the single cond token
         self._site(l, "ca_q", bits, A, n, x_row0=out_row0, ln=(ln2g, ln2b), out=self.q2)
         k2, v2 = self._cond_kv(l, bits, vids, cond_row0)

@@ -330,3 +330,51 @@ class TestPackedW4:
         assert D.weight_prep(t(w), 4).packed is None
         with pytest.raises(ValueError):
             D.weight_prep(t(w), 6, pack4=True)
+
+
+class TestBf16Input:
+    def test_bf16_rows_widened_exactly(self, D):
+        """The sta_o quantizer reading the bf16 attention output directly
+        (QCB_PRO_BF16, rows through a per-segment table) == the f32 path on the
+        widened rows == the oracle."""
+        rng = np.random.default_rng(12)
+        K, S, Sp, nseg = 1152, 4000, 4096, 4
+        xb = torch.as_tensor(residual_rows(rng, nseg * S, K)).cuda().to(torch.bfloat16)
+        c = np.exp(0.5 * rng.standard_normal(K))
+        tr = [(t(c), t(D.sign_vector(0, 1024)))]
+        row0 = t(np.arange(nseg, dtype=np.int64) * S)
+        (rb,) = D.act_quant(xb, 8, tr, seg_rows=Sp, seg_valid=S, nseg=nseg, x_row0=row0)
+        xf = xb.float()
+        (rf,) = D.act_quant(xf, 8, tr, seg_rows=Sp, seg_valid=S, nseg=nseg, x_row0=row0)
+        xh = xf.cpu().numpy()
+        for v in range(nseg):
+            sl = slice(v * Sp, v * Sp + S)
+            assert torch.equal(rb.codes[sl], rf.codes[sl]) and float(rb.scale[v]) == float(rf.scale[v])
+            check_quant(rb, O.rotate_act_fwht(xh[v * S:(v + 1) * S], c, 0), v, sl, K, 8, 0)
+
+    def test_engine_fast_attention_direct_equals_copy(self, D):
+        """bench mode (bf16 SDPA): the bf16-direct sta_o input gives the same
+        latents and decisions as the f32 copy of the attention output."""
+        from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
+        from paper_2503_06545_b200.model import DiTConfig, init_model
+        from paper_2503_06545_b200.sampler import linear_beta_schedule
+        from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles
+        cfg = DiTConfig(num_blocks=2, model_dim=1152, num_heads=16, tokens_per_frame=64,
+                        frames=2, cond_dim=64, seed=1)
+        model = init_model(cfg)
+        absmax = {l: {s: np.abs(getattr(b, s)).max(axis=1).astype(np.float64) * 2.0
+                      for s in ("sta_q", "sta_k", "sta_v", "sta_o", "ca_q", "ca_k", "ca_v",
+                                "ca_o", "ffn1", "ffn2")} for l, b in enumerate(model.blocks)}
+        sched = linear_beta_schedule(6)
+        outs = []
+        for direct in (True, False):
+            eng = QuantCacheEngine(model, sched.alpha_bar,
+                                   Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=True),
+                                   ThresholdConfig(delta1=1e3, delta2=1e6), {0: 6, 1: 6}, absmax,
+                                   max_videos=2, options=EngineOptions(attention="fast",
+                                                                       noise="device"))
+            eng.attn_bf16_direct = direct
+            lat, tr = eng.generate([5, 6])
+            outs.append((lat, [[r.to_json_obj() for r in x] for x in tr]))
+        assert np.array_equal(outs[0][0], outs[1][0])
+        assert outs[0][1] == outs[1][1]
