@@ -1333,23 +1333,36 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2_hot(const ActQuantParams
   const int K = p.K, n_out = p.n_out;
   const float topf = (float)((1 << p.bits) - 1);
   const int nb = (K + 128 * kP2HBatch - 1) / (128 * kP2HBatch);   // items per (row, output)
-  const int per_row = nb * n_out;
-  const long long W = (long long)gridDim.x * (kV2Threads / 32);
-  const long long w = (long long)blockIdx.x * (kV2Threads / 32) + warp;
-  // item u of this warp -> stash pointer of its first float4 (nullptr: no item)
-  auto item_src = [&](long long u, const float*& src, int& jbase, long long& orow, int& o,
-                      int& b, int& seg) -> bool {
-    const long long k = u / per_row;
-    const int rem = (int)(u - k * per_row);
-    o = rem / nb;
-    b = rem - o * nb;
-    const long long gr = w + k * W;
-    if (gr >= a.total_rows) return false;
-    seg = (int)(gr / p.seg_valid);
-    const int mrow = (int)(gr - (long long)seg * p.seg_valid);
-    orow = (long long)seg * p.seg_rows + mrow;
+  const int W = gridDim.x * (kV2Threads / 32);
+  const int w = blockIdx.x * (kV2Threads / 32) + warp;
+  // the warp's items in order: rows gr = w, w + W, ...; per row the outputs o;
+  // per output the batches b of 128 * kP2HBatch columns.  Advanced
+  // incrementally (one 32-bit division per new row, none per item).
+  int it_gr = w, it_o = 0, it_b = 0, it_seg = 0;
+  long long it_orow = 0;
+  auto row_setup = [&]() {
+    it_seg = it_gr / p.seg_valid;
+    it_orow = (long long)it_seg * p.seg_rows + (it_gr - it_seg * p.seg_valid);
+  };
+  if (it_gr < a.total_rows) row_setup();
+  // the current item's stash pointer etc.; false past the warp's last row
+  auto item_src = [&](const float*& src, int& jbase, long long& orow, int& o, int& b,
+                      int& seg) -> bool {
+    if (it_gr >= a.total_rows) return false;
+    o = it_o;
+    b = it_b;
+    seg = it_seg;
+    orow = it_orow;
     jbase = lane * 4 + b * 128 * kP2HBatch;
     src = a.stash[o] + orow * a.ld_stash;
+    if (++it_b == nb) {
+      it_b = 0;
+      if (++it_o == n_out) {
+        it_o = 0;
+        it_gr += W;
+        if (it_gr < a.total_rows) row_setup();
+      }
+    }
     return true;
   };
   auto load_item = [&](const float* src, int jbase, float4 (&v)[kP2HBatch]) {
@@ -1363,7 +1376,7 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2_hot(const ActQuantParams
   const float* src;
   int jb, o, b, seg;
   long long orow;
-  bool have = item_src(0, src, jb, orow, o, b, seg);
+  bool have = item_src(src, jb, orow, o, b, seg);
   if (have) load_item(src, jb, cur);
   // (s, z) per (output, segment): quantize's minmax parameters (quant.py:83-123)
   const double top = (double)((1 << p.bits) - 1);
@@ -1394,11 +1407,11 @@ __global__ void __launch_bounds__(kV2Threads) aq2_pass2_hot(const ActQuantParams
   const float2 m1 = make_float2(-1.0f, -1.0f);
   const float2 b23 = make_float2(8388608.0f, 8388608.0f);
   int rs = 0;
-  for (long long u = 0; have; ++u) {
+  while (have) {
     const float* nsrc;
     int njb, no, nbb, nseg_;
     long long norow;
-    const bool nhave = item_src(u + 1, nsrc, njb, norow, no, nbb, nseg_);
+    const bool nhave = item_src(nsrc, njb, norow, no, nbb, nseg_);
     if (nhave) load_item(nsrc, njb, nxt);
     const int t = o * p.nseg + seg;
     const float inv_sf = t_inv[t], zf = t_z[t];
