@@ -681,6 +681,43 @@ def c2_microbench(torch, int8_peak, peaks):
             "hbm_peak_gbs": peaks["hbm"], "results": res}
 
 
+def attention_microbench(torch, peaks):
+    """The STDiT self-attention at the target shape (4 videos x 16 heads x
+    S = 16384, dh = 72, bf16): our tcgen05 kernel (qcb_attention_bf16) against
+    the library SDPA the headline uses, CUDA events, median of 5."""
+    import torch.nn.functional as F
+    from paper_2503_06545_b200 import device as Dv
+    H, dh, S, B = 16, 72, 16384, 4
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    q, k, v = (torch.randn((B * S, H * dh), device="cuda", generator=g).to(torch.bfloat16)
+               for _ in range(3))
+    out = torch.empty_like(q)
+    qq, kk, vv = (t.view(B, S, H, dh).permute(0, 2, 1, 3) for t in (q, k, v))
+    res = {}
+    for name, fn in (("tcgen05_ours", lambda: Dv.attention_bf16(q, k, v, H, S, nseg=B, out=out)),
+                     ("sdpa_library", lambda: F.scaled_dot_product_attention(qq, kk, vv))):
+        fn()
+        ts = []
+        for _ in range(5):
+            e0, e1 = _events(torch)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        tf = 4.0 * B * H * S * S * dh / ms / 1e9
+        res[name] = {"ms": round(ms, 3), "tflops_dh72": round(tf, 1),
+                     "frac_bf16_peak": round(tf / peaks["bf16"], 4)}
+    del q, k, v, out
+    torch.cuda.empty_cache()
+    return {"workload": "self-attention at the north_star target: 4 videos x 16 heads x "
+                        "S=16384, dh=72, bf16 operands, f32 softmax/accumulation",
+            "bf16_peak_tflops": peaks["bf16"], "results": res,
+            "engine_default": "sdpa_library (faster); attention='tcgen05' selects ours"}
+
+
 def c1_latency(torch):
     """BASELINE configs[0] (C1): the reference's tiny configs (small seed 3,
     default seed 7) with full QuantCache and the reference's calibration, exact
@@ -747,6 +784,7 @@ def run_ours(args):
         print("extra:", json.dumps(extra, default=str)[:3000], file=sys.stderr, flush=True)
         extra["c2_gemm"] = c2_microbench(torch, int8_peak, peaks)
         extra["c1_latency"] = c1_latency(torch)
+        extra["attention"] = attention_microbench(torch, peaks)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c = cpu_sample_line(args.workload, 1, 0, 1, args.timesteps, args.wbits)

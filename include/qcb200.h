@@ -21,6 +21,7 @@
  *                      LN/modulation prologue of model.py:182,189,196
  *   qcb_weight_prep    runtime.py:40-61   QuantRuntime.__init__ weight prep
  *   qcb_attention_f64  model.py:150-156, tensor.py:115-132  _mha / attention
+ *   qcb_attention_bf16 model.py:150-156                     _mha, bf16 fast mode
  *   qcb_ln_mod         model.py:137-142 (+182,196)  _ln and modulation
  *   qcb_ddpm_step      sampler.py:59-88   reverse_step / final_step
  *   qcb_cfg_combine    (extension)        classifier-free guidance of eps
@@ -241,6 +242,26 @@ typedef struct QcbAttention {
 } QcbAttention;
 
 int qcb_attention_f64(const QcbAttention* a, void* stream);
+
+/* Fast attention for the benchmarked bf16 path (the reference computes _mha in
+ * f64, model.py:150-156; this mode trades that for bf16 operands like any
+ * library SDPA it replaces): out = softmax(scale q k^T) v per head and segment
+ * on the tcgen05 tensor cores (S and O accumulate in f32 in TMEM, P is bf16).
+ * q, k, v, out: bf16 [nseg * seg_stride][ld] with head h at columns
+ * [h*dh, (h+1)*dh); segment s owns rows [s*seg_stride, s*seg_stride + S).
+ * dh % 8 == 0 and dh <= 128; ld* % 8 == 0; pointers 16-byte aligned;
+ * S <= seg_stride.  scale = 0 means 1/sqrt(dh). */
+typedef struct QcbAttentionBf16 {
+  const void* q; long long ldq;
+  const void* k; long long ldk;
+  const void* v; long long ldv;
+  void* out; long long ldo;
+  int S, heads, dh, nseg;
+  long long seg_stride;
+  float scale;
+} QcbAttentionBf16;
+
+int qcb_attention_bf16(const QcbAttentionBf16* a, void* stream);
 
 /* x_{t-1} = f32((x - c1*eps)/c2 + c3*noise) in f64 (c3 = 0: no noise). */
 typedef struct QcbDdpm {

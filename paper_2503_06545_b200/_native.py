@@ -80,6 +80,12 @@ class QcbAttention(C.Structure):
                 ("o_seg_stride", i64), ("seg_valid", i32)]
 
 
+class QcbAttentionBf16(C.Structure):
+    _fields_ = [("q", vp), ("ldq", i64), ("k", vp), ("ldk", i64), ("v", vp), ("ldv", i64),
+                ("out", vp), ("ldo", i64), ("S", i32), ("heads", i32), ("dh", i32),
+                ("nseg", i32), ("seg_stride", i64), ("scale", C.c_float)]
+
+
 class QcbDdpm(C.Structure):
     _fields_ = [("x", vp), ("eps", vp), ("noise", vp), ("out", vp), ("n", i64),
                 ("c1", f64), ("c2", f64), ("c3", f64), ("rc2", f64), ("noise_seed", u64),
@@ -135,6 +141,7 @@ def lib():
         "qcb_weight_prep": [P(QcbWeightPrep), vp],
         "qcb_ln_mod": [P(QcbLnMod), vp],
         "qcb_attention_f64": [P(QcbAttention), vp],
+        "qcb_attention_bf16": [P(QcbAttentionBf16), vp],
         "qcb_ddpm_step": [P(QcbDdpm), vp],
         "qcb_cfg_combine": [vp, vp, C.c_float, vp, i64, vp],
         "qcb_pack_w4": [vp, i64, i32, i32, vp, i64, vp],
@@ -172,7 +179,7 @@ def lib():
 
 EXPORTED = ("qcb_gemm_u8", "qcb_pack_w4", "qcb_gemm_f64", "qcb_head_gemm", "qcb_head_prep",
             "qcb_head_prep_bytes", "qcb_head_workspace_bytes", "qcb_act_quant", "qcb_act_quant_workspace_bytes", "qcb_weight_prep", "qcb_ln_mod",
-            "qcb_attention_f64", "qcb_ddpm_step", "qcb_cfg_combine", "qcb_gelu_inplace", "qcb_reduce_hlc", "qcb_reduce_srap",
+            "qcb_attention_f64", "qcb_attention_bf16", "qcb_ddpm_step", "qcb_cfg_combine", "qcb_gelu_inplace", "qcb_reduce_hlc", "qcb_reduce_srap",
             "qcb_reduce_l1", "qcb_reduce_l1_hist", "qcb_reduce_workspace_bytes", "qcb_copy_async", "qcb_col_absmax", "qcb_policy_plan_reuse",
             "qcb_policy_sim_mask", "qcb_policy_plan_finish", "qcb_policy_observe",
             "qcb_policy_observe_all",

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT, "libqcb200.so")
-SOURCES = ["qc_gemm.cu", "qc_quant.cu", "qc_reduce.cu", "qc_fp.cu", "qc_head.cu", "qc_api.cu"]
+SOURCES = ["qc_gemm.cu", "qc_quant.cu", "qc_reduce.cu", "qc_fp.cu", "qc_head.cu", "qc_fmha.cu", "qc_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]

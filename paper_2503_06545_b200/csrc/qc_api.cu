@@ -107,6 +107,10 @@ extern "C" int qcb_attention_f64(const QcbAttention* a, void* stream) {
   return attention_f64_launch(a, (cudaStream_t)stream);
 }
 
+extern "C" int qcb_attention_bf16(const QcbAttentionBf16* a, void* stream) {
+  return attention_bf16_launch(a, (cudaStream_t)stream);
+}
+
 extern "C" int qcb_ddpm_step(const QcbDdpm* d, void* stream) {
   if (!d || !d->x || !d->eps || !d->out) return QCB_ERR_VALUE;
   if (d->n <= 0) return QCB_ERR_DIM;

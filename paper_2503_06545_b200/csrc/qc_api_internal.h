@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "../../include/qcb200.h"
 
@@ -70,6 +71,9 @@ inline void allow_max_smem(K kernel, bool& done) {
 }
 
 int num_sms();
+// cuTensorMapEncodeTiled from the driver (nullptr when unavailable)
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn();
+int attention_bf16_launch(const QcbAttentionBf16* a, cudaStream_t st);
 int pick_block_n(int N);
 // Grouped launch: output column group j (group n columns) reduces over
 // K_j = (j+1)*k with row sums a_rowsum + j*rowsum_stride.

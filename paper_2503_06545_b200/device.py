@@ -354,6 +354,30 @@ def attention_f64(q, k, v, heads: int, out=None, nseg: int = 1, S=None, Skv=None
     return out
 
 
+def attention_bf16(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int, S: int,
+                   nseg: int = 1, seg_stride: Optional[int] = None, out=None,
+                   scale: float = 0.0, stream=None) -> torch.Tensor:
+    """Fast attention (bf16 operands, f32 softmax / accumulation) on the
+    tcgen05 tensor cores: per segment s and head h, rows [s*seg_stride,
+    s*seg_stride + S) of q / k / v (bf16 [rows][heads*dh]) -> out (bf16, same
+    layout).  The bench-mode replacement of library SDPA for model.py:150-156."""
+    seg_stride = seg_stride or S
+    d = q.shape[1]
+    if out is None:
+        out = torch.empty((nseg * seg_stride, d), dtype=torch.bfloat16, device=q.device)
+    for t in (q, k, v, out):
+        if t.dtype != torch.bfloat16 or t.stride(1) != 1:
+            raise TypeError("attention_bf16 takes row-major bf16 tensors")
+        if t.shape[0] < nseg * seg_stride:
+            raise DimensionError("attention_bf16: fewer rows than nseg * seg_stride")
+    a = N.QcbAttentionBf16(N.ptr(q), q.stride(0), N.ptr(k), k.stride(0), N.ptr(v), v.stride(0),
+                           N.ptr(out), out.stride(0), S, heads, d // heads, nseg, seg_stride,
+                           float(scale))
+    N.check(N.lib().qcb_attention_bf16(C.byref(a), N.stream_ptr(stream)), "attention_bf16")
+    count(1)
+    return out
+
+
 def ddpm(x, eps, c1: float, c2: float, noise=None, c3: float = 0.0, out=None, stream=None,
          noise_gen=None):
     """reverse_step / final_step (sampler.py:59-88).  noise: a tensor, or

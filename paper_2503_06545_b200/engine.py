@@ -143,7 +143,8 @@ class VideoState:
 
 @dataclass
 class EngineOptions:
-    attention: str = "precise"     # "precise" (f64 softmax kernel) | "fast" (bf16 SDPA)
+    attention: str = "precise"     # "precise" (f64 softmax kernel) | "fast" (bf16 library
+                                   # SDPA) | "tcgen05" (bf16, our qcb_attention_bf16)
     noise: str = "numpy"           # "numpy" (reference RNG stream) | "device" (Philox)
     head: str = "int8"             # "int8" (certified digit GEMMs) | "f64" (FMA chains);
                                    # both give the reference's mm bit for bit
@@ -298,8 +299,12 @@ class QuantCacheEngine:
             if self.opts.cfg_scale is not None else None
         self.q2 = torch.zeros_like(self.q)
         # bf16 q/k/v written by the integer GEMMs' epilogue for the bf16 attention
+        bf16_att = self.opts.attention in ("fast", "tcgen05")
         self.qkv16 = [torch.zeros((rows, d), dtype=torch.bfloat16, device=dev) for _ in range(3)] \
-            if self.opts.attention == "fast" else None
+            if bf16_att else None
+        # bf16 attention output of the tcgen05 kernel (read by the sta_o quantizer)
+        self.att16 = torch.zeros((rows, d), dtype=torch.bfloat16, device=dev) \
+            if self.opts.attention == "tcgen05" else None
         self.cond = torch.zeros((nv, self.c), dtype=torch.float32, device=dev)
         self.ac = [Dv.ActCodes(self.codes[o][:, :Dv.round16(d)],
                                torch.zeros(rows, dtype=torch.int32, device=dev),
@@ -489,6 +494,14 @@ class QuantCacheEngine:
         """Returns None, or (bf16 rows [nseg * S][d], their per-segment first-row
         table) when the fast path's output can feed the next quantizer directly."""
         S, Sp, d, H = self.S, self.Sp, self.d, self.H
+        if self.opts.attention == "tcgen05" and Skv > 1:
+            bf = torch.bfloat16
+            qq, kk, vv = (t if t.dtype == bf else t.to(bf) for t in (q, k, v))
+            Dv.attention_bf16(qq, kk, vv, H, S, nseg=nseg, seg_stride=Sp, out=self.att16)
+            if self.tog.aigq_weights and self.tog.aigq_acts:
+                return self.att16, self._upload_idx([[v_ * Sp for v_ in range(nseg)]])[0]
+            out[:nseg * Sp].copy_(self.att16[:nseg * Sp])
+            return None
         if self.opts.attention == "fast" and Skv > 1:
             dh = d // H
             qq = q[:nseg * Sp].view(nseg, Sp, H, dh)[:, :S].permute(0, 2, 1, 3)

@@ -39,7 +39,7 @@ def test_every_declared_symbol_is_exported(lib):
 def test_struct_layouts_match_header(tmp_path):
     """Compile a tiny C program printing sizeof/offsetof of the ABI structs."""
     structs = ["QcbGemm", "QcbGemmF64", "QcbHeadGemm", "QcbActQuant", "QcbWeightPrep", "QcbLnMod",
-               "QcbAttention", "QcbDdpm", "QcbFeat", "QcbThresholds", "QcbPolicyVideo"]
+               "QcbAttention", "QcbAttentionBf16", "QcbDdpm", "QcbFeat", "QcbThresholds", "QcbPolicyVideo"]
     prog = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"',
             "int main(void){"]
     for s in structs:
