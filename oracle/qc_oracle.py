@@ -41,18 +41,44 @@ SITES = ("sta_q", "sta_k", "sta_v", "sta_o", "ca_q", "ca_k", "ca_v", "ca_o",
 # ---------------------------------------------------------------------------
 # L0: deterministic dense products (tensor.py)
 
+def _lsb_exp(x64: np.ndarray) -> np.ndarray:
+    """Exponent of the lowest set bit of each (f32-representable) value; a
+    large sentinel for zeros."""
+    m, e = np.frexp(x64)
+    mi = np.abs(m * 2.0 ** 24).astype(np.int64)
+    low = mi & -mi
+    tz = np.where(low > 0, np.log2(np.maximum(low, 1)).astype(np.int64), 0)
+    return np.where(x64 != 0, e.astype(np.int64) - 24 + tz, 1 << 20)
+
+
 def seq_mm(a, b) -> np.ndarray:
     """f32(sum_k f64(a[:,k]) * f64(b[k,:])) accumulated in ascending k.
 
-    Restates tensor.py:43-60 (`mm`)."""
+    Restates tensor.py:43-60 (`mm`).  Shortcut with the same result: for an
+    output (i, n) whose every partial sum is exact in f64 -- all terms are
+    multiples of 2^L with L >= lsb(a[i,:]) + lsb(b[:,n]) and sum_k |term| <
+    2^(L + 53) -- the ascending-k sum is the exact sum, which any exact
+    summation (f64 BLAS: each intermediate is such a partial sum) returns too.
+    The remaining columns take the explicit loop."""
     a64 = np.asarray(a).astype(np.float64)
     b64 = np.asarray(b).astype(np.float64)
     if a64.ndim != 2 or b64.ndim != 2 or a64.shape[1] != b64.shape[0]:
         raise ValueError(f"matmul shapes {a64.shape} x {b64.shape}")
-    acc = np.zeros((a64.shape[0], b64.shape[1]), dtype=np.float64)
-    for k in range(a64.shape[1]):
-        acc += a64[:, k:k + 1] * b64[k:k + 1, :]
-    return acc.astype(np.float32)
+    out = a64 @ b64
+    if a64.size and b64.size:
+        L = _lsb_exp(a64).min(axis=1)[:, None] + _lsb_exp(b64).min(axis=0)[None, :]
+        bound = (np.abs(a64) @ np.abs(b64)) * (1.0 + 2.0 ** -30)
+        ok = (bound < np.ldexp(1.0, np.minimum(L + 53, 1000))) | (bound == 0)
+    else:
+        ok = np.ones(out.shape, dtype=bool)
+    cols = np.nonzero(~ok.all(axis=0))[0]
+    if cols.size:
+        bc = b64[:, cols]
+        acc = np.zeros((a64.shape[0], cols.size), dtype=np.float64)
+        for k in range(a64.shape[1]):
+            acc += a64[:, k:k + 1] * bc[k:k + 1, :]
+        out[:, cols] = acc
+    return out.astype(np.float32)
 
 
 def int_acc(codes_a, za, codes_w, zw) -> np.ndarray:
@@ -68,10 +94,23 @@ def int_acc(codes_a, za, codes_w, zw) -> np.ndarray:
 def matmul_int_seq(codes_a, sa, za, codes_w, sw, zw) -> np.ndarray:
     """Reference integer GEMM: joint scale applied per k, f64 ascending-k sum.
 
-    Restates tensor.py:100-112."""
+    Restates tensor.py:100-112.  Shortcut with the same result: when every
+    partial sum joint[n] * sum_{k<K'} (a-za)(w-zw) is exact in f64 (the
+    integer sum of |terms| below 2^(53 - significand bits of joint[n])), the
+    ascending-k f64 sum equals the exact value, which is also the one
+    rounding of joint * (exact integer accumulator) -- computed directly."""
     a = np.asarray(codes_a, dtype=np.int64) - int(za)
     w = np.asarray(codes_w, dtype=np.int64) - np.asarray(zw, dtype=np.int64)
     joint = float(sa) * np.atleast_1d(np.asarray(sw, dtype=np.float64))
+    m, _ = np.frexp(joint)
+    sig = np.array([53 - (int(np.round(v * 2.0 ** 53)) & -int(np.round(v * 2.0 ** 53))).bit_length()
+                    + 1 if v != 0 else 0 for v in np.abs(m)], dtype=np.int64)
+    # integer products below 2^16 and K < 2^20: f64 BLAS sums are exact here
+    bound = np.abs(a).astype(np.float64) @ np.abs(w).astype(np.float64)   # >= |partial sums|
+    if a.shape[1] < (1 << 20) and (bound.max(axis=0, initial=0) <
+                                   np.left_shift(1, 53 - sig).astype(np.float64)).all():
+        acc = a.astype(np.float64) @ w.astype(np.float64)
+        return (np.broadcast_to(joint[None, :], acc.shape) * acc).astype(np.float32)
     acc = np.zeros((a.shape[0], w.shape[1]), dtype=np.float64)
     for k in range(a.shape[1]):
         acc += joint[None, :] * (a[:, k:k + 1] * w[k:k + 1, :])

@@ -210,3 +210,58 @@ class TestSampler:
         solo, _ = O.sample(dims, 10, seed=seed + 8, **kw)
         assert not np.array_equal(out[1], out[0])
         assert np.isfinite(out).all() and np.isfinite(solo).all()
+
+
+def test_matmul_int_seq_shortcut_equals_the_loop():
+    """matmul_int_seq's exact-partial-sum shortcut returns what the explicit
+    ascending-k f64 loop of tensor.py:100-112 returns (random codes, zero
+    points, 16-bit-significand scales, K up to 2000)."""
+    import numpy as np
+    from oracle import qc_oracle as O
+    rng = np.random.default_rng(7)
+
+    def loop(a_, sa, za, w_, sw, zw):
+        a = np.asarray(a_, np.int64) - za
+        w = np.asarray(w_, np.int64) - np.asarray(zw, np.int64)
+        joint = float(sa) * np.atleast_1d(np.asarray(sw, np.float64))
+        acc = np.zeros((a.shape[0], w.shape[1]))
+        for k in range(a.shape[1]):
+            acc += joint[None, :] * (a[:, k:k + 1] * w[k:k + 1, :])
+        return acc.astype(np.float32)
+    for _ in range(40):
+        M, K, N = rng.integers(1, 24), rng.integers(1, 2000), rng.integers(1, 24)
+        ab, wb = int(rng.choice([6, 8])), int(rng.choice([4, 6, 8]))
+        a = rng.integers(0, 2 ** ab, (M, K))
+        w = rng.integers(0, 2 ** wb, (K, N))
+        za, zw = int(rng.integers(0, 2 ** ab)), rng.integers(0, 2 ** wb, N)
+        sa, sw = O.scale_up16(rng.uniform(1e-3, 1)), O.scale_up16(rng.uniform(1e-3, 1, N))
+        assert np.array_equal(O.matmul_int_seq(a, sa, za, w, sw, zw), loop(a, sa, za, w, sw, zw))
+
+
+def test_seq_mm_shortcut_equals_the_loop():
+    """seq_mm's exact-partial-sum shortcut returns what the ascending-k f64
+    loop of tensor.py:43-60 returns: random f32 operands (mostly the loop),
+    rotation matrices (the shortcut) and coarse dyadic values (exact sums)."""
+    import numpy as np
+    from oracle import qc_oracle as O
+    rng = np.random.default_rng(3)
+
+    def loop(a, b):
+        a64, b64 = np.asarray(a, np.float64), np.asarray(b, np.float64)
+        acc = np.zeros((a64.shape[0], b64.shape[1]))
+        for k in range(a64.shape[1]):
+            acc += a64[:, k:k + 1] * b64[k:k + 1, :]
+        return acc.astype(np.float32)
+    for t in range(30):
+        M, K, N = rng.integers(1, 24), rng.integers(1, 1200), rng.integers(1, 24)
+        if t % 3 == 0:
+            a = rng.standard_normal((M, K)).astype(np.float32)
+            b = rng.standard_normal((K, N)).astype(np.float32)
+        elif t % 3 == 1:
+            K2 = 1 << int(np.log2(max(K, 2)))
+            a = (rng.standard_normal((M, K2)) * np.exp(rng.standard_normal(K2))).astype(np.float32)
+            b = O.rotation_dense(K2, t).astype(np.float32)
+        else:
+            a = (rng.integers(-8, 8, (M, K)) * 2.0 ** -3).astype(np.float32)
+            b = (rng.integers(-8, 8, (K, N)) * 2.0 ** -4).astype(np.float32)
+        assert np.array_equal(O.seq_mm(a, b), loop(a, b))
