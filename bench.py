@@ -396,7 +396,7 @@ def _rank_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def _calibrated_thresholds(torch, model, sched, wbits, absmax, T):
+def _calibrated_thresholds(torch, model, sched, wbits, absmax, T, sampler="ddpm"):
     """Threshold calibration pass (harness.py:319-345 on the quantized path):
     every block recomputed (HLC with delta = 0), D/V recorded, delta = p33/p66 of
     D, v = p25/p75 of V.  The same calibration video on every rank."""
@@ -406,7 +406,8 @@ def _calibrated_thresholds(torch, model, sched, wbits, absmax, T):
     eng = QuantCacheEngine(model, sched.alpha_bar, tog_cal,
                            ThresholdConfig(delta1=0.0, delta2=0.0), wbits, absmax,
                            sign_seed=0, prune_seed=0, max_videos=1,
-                           options=EngineOptions(attention="fast", noise="device"))
+                           options=EngineOptions(attention="fast", noise="device",
+                                                 sampler=sampler))
     _, tr = eng.generate([1000])
     ds = [r.d for r in tr[0] if r.d is not None]
     vs = [r.v for r in tr[0] if r.layer == 0 and r.v is not None and r.v > 0]
@@ -618,6 +619,57 @@ def c4_cfg_line(torch, args, model, absmax, th_target, S_target, cfg_scale=4.5):
     return out
 
 
+def c5_rf_line(torch, args, model, absmax, batches=(1, 8, 32, 64), steps=30):
+    """BASELINE configs[4] (C5, an EXTENSION: the reference has no flow sampler,
+    SPEC.md:474): rectified-flow sampling (head output = velocity, 30 Euler
+    steps) at STDiT-XL/2 dims, 16 frames 256x256 (S = 4096, the C3 size), full
+    QuantCache with per-video decisions, batch sweep of videos per GPU.
+    Thresholds from an all-recompute flow calibration pass at this size."""
+    from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
+    from paper_2503_06545_b200.model import DiTConfig, DiTModel
+    from paper_2503_06545_b200.sampler import linear_beta_schedule
+    from paper_2503_06545_b200.schedule import Toggles
+    cfg = DiTConfig(seed=0, **model_dims("c3"))
+    m5 = DiTModel(cfg, model.blocks, model.head_w, model.head_b)
+    S, d = cfg.seq_len, cfg.model_dim
+    wbits = {l: args.wbits for l in range(cfg.num_blocks)}
+    sched = linear_beta_schedule(steps)
+    th = _calibrated_thresholds(torch, m5, sched, wbits, absmax, steps, sampler="rf")
+    res = {}
+    for B in batches:
+        eng = QuantCacheEngine(m5, sched.alpha_bar,
+                               Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=True),
+                               th, wbits, absmax, sign_seed=0, prune_seed=0, max_videos=B,
+                               options=EngineOptions(attention="fast", noise="device",
+                                                     sampler="rf"))
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(5)
+        x0 = torch.randn((B, S, d), device="cuda", generator=gen)
+        cond = torch.randn((B, cfg.cond_dim), device="cuda", generator=gen)
+        eng.generate(list(range(100, 100 + B)), x0_dev=x0, cond_dev=cond, return_device=True)
+        torch.cuda.synchronize()
+        e0, e1 = _events(torch)
+        e0.record()
+        _, vids = eng.generate(list(range(200, 200 + B)), x0_dev=x0, cond_dev=cond,
+                               return_device=True)
+        e1.record()
+        torch.cuda.synchronize()
+        el = e0.elapsed_time(e1) / 1e3
+        recs = [r_ for tv in eng.traces_of(vids) for r_ in tv if r_.layer != "head"]
+        frac = sum(r_.action == "recompute" for r_ in recs) / max(1, len(recs))
+        res[str(B)] = {"videos_per_s": round(B / el, 3), "s_per_video": round(el / B, 4),
+                       "recompute_fraction": round(frac, 4),
+                       "arena_gib": round(eng.arena.numel() * 4 / 2 ** 30, 2)}
+        del eng, x0, cond
+        torch.cuda.empty_cache()
+    return {"workload": f"C5 (extension: rectified flow, no reference sampler): STDiT-XL/2 "
+                        f"dims, 16 frames 256x256 (S={S}), {steps} Euler steps, full "
+                        f"QuantCache, per-video decisions, batch sweep on 1 GPU",
+            "unit": "videos/s", "results": res,
+            "thresholds": {"delta1": th.delta1, "delta2": th.delta2, "v_low": th.v_low,
+                           "v_high": th.v_high}}
+
+
 def c2_microbench(torch, int8_peak, peaks):
     """BASELINE configs[1] (C2): the AIGQ quantized linear at M = 16,384 tokens
     (one 16-frame 512^2 video), K,N in {1152, 4608}: quantizer (rotation +
@@ -785,6 +837,7 @@ def run_ours(args):
         extra["c2_gemm"] = c2_microbench(torch, int8_peak, peaks)
         extra["c1_latency"] = c1_latency(torch)
         extra["attention"] = attention_microbench(torch, peaks)
+        extra["c5_rf"] = c5_rf_line(torch, args, model, absmax)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c = cpu_sample_line(args.workload, 1, 0, 1, args.timesteps, args.wbits)

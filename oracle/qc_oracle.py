@@ -635,6 +635,14 @@ def ddpm_step(x, t: int, eps, ab: np.ndarray, noise) -> np.ndarray:
     return mean.astype(np.float32)
 
 
+def rf_step(x, v, dt: float) -> np.ndarray:
+    """Rectified-flow Euler step x - dt * v in f64, one rounding to f32.  An
+    EXTENSION (C5): the reference has no flow sampler; it reuses
+    the DDPM update's arithmetic with c1 = dt, c2 = 1."""
+    return ((np.asarray(x).astype(np.float64) - dt * np.asarray(v).astype(np.float64))
+            / 1.0).astype(np.float32)
+
+
 def ddpm_final(x, eps, ab: np.ndarray) -> np.ndarray:
     """Clean-data estimate at t = 0 (sampler.py:83-88)."""
     a0 = ab[0]
@@ -698,9 +706,13 @@ def block_costs(dims: ModelDims) -> Tuple[int, int, int]:
 def sample(dims: ModelDims, steps: int, th: Optional[Thresholds] = None,
            toggles=(False, False, False, False), seed: int = 0, prune_seed: int = 0,
            weight_bits=None, act_absmax=None, sign_seed: int = 0,
-           b0: float = 1e-4, b1: float = 2e-2, weights=None, record=None):
+           b0: float = 1e-4, b1: float = 2e-2, weights=None, record=None,
+           sampler: str = "ddpm"):
     """`generate` + `run_single` wiring restated (sampler.py:91-162,
     harness.py:416-441). toggles = (hlc, aigq_w, aigq_a, srap).
+    sampler="rf": the rectified-flow EXTENSION (C5, no reference sampler):
+    the head output is a velocity, one Euler step x - v / steps per timestep,
+    no noise draws; every QuantCache policy runs unchanged.
 
     Returns (final latent f32 (F, T, d), PolicyState)."""
     hlc, aw, aa, srap = toggles
@@ -735,7 +747,9 @@ def sample(dims: ModelDims, steps: int, th: Optional[Thresholds] = None,
         st.finalize(t, x, dec)
         if record is not None:
             record.append((t, x, outs, eps, dec))
-        if t > 0:
+        if sampler == "rf":
+            x = rf_step(x, eps, 1.0 / steps)
+        elif t > 0:
             noise = rng.standard_normal(shape).astype(np.float32)
             x = ddpm_step(x, t, eps, ab, noise)
         else:

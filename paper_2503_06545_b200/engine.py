@@ -36,6 +36,7 @@ import torch
 
 from . import _native as N
 from . import device as Dv
+from .errors import ConfigurationError
 from .model import QUANT_SITES, DiTModel, block_mac_cost, head_mac_cost, timestep_embedding
 from .schedule import FP_BITS, ThresholdConfig, Toggles, TraceRecord, billed_macs, \
     prune_draw_table
@@ -154,6 +155,9 @@ class EngineOptions:
     cfg_scale: Optional[float] = None   # classifier-free guidance (EXTENSION, no reference:
                                         # SPEC.md:468): each video runs a cond and an
                                         # uncond (null cond) branch as two slots
+    sampler: str = "ddpm"          # "ddpm" (reference) | "rf": rectified flow, EXTENSION
+                                   # (C5; no reference sampler): the head
+                                   # output is a velocity, x <- x - v / T, no noise
     record_features: bool = False
 
 
@@ -194,6 +198,8 @@ class QuantCacheEngine:
         self.tog, self.th = toggles, thresholds
         self.thc = Dv.thresholds_struct(thresholds, toggles)
         self.ab = np.asarray(alpha_bar, np.float64)
+        if self.opts.sampler not in ("ddpm", "rf"):
+            raise ConfigurationError("sampler must be 'ddpm' or 'rf'")
         self.T = len(self.ab)
         self.L = self.cfg.num_blocks
         if self.L > N.MAX_LAYERS:
@@ -985,7 +991,8 @@ class QuantCacheEngine:
             # branches; one DDPM update per video from the guided eps, its
             # result copied into the uncond branch's own slot
             step = 2 if self.cfg_scale is not None else 1
-            if t > 0 and self.opts.noise == "numpy":
+            rf = self.opts.sampler == "rf"
+            if t > 0 and self.opts.noise == "numpy" and not rf:
                 for i, v in enumerate(range(0, nv, step)):
                     self.noise_host[i].numpy()[:] = vids[v].rng.standard_normal(
                         (F, Tk, d)).astype(np.float32).reshape(S, d)
@@ -1001,7 +1008,10 @@ class QuantCacheEngine:
                 if step == 2:
                     eps_v = Dv.cfg_combine(eps_v, self.eps[(v + 1) * self.Sp:(v + 1) * self.Sp + S],
                                            self.cfg_scale, out=self.eps_cfg[i])
-                if t > 0:
+                if rf:   # Euler step of the flow ODE: f32(x - (1/T) v) in f64
+                    Dv.ddpm(self.slot_view(vs.x), eps_v, 1.0 / self.T, 1.0,
+                            out=self.slot_view(new))
+                elif t > 0:
                     a_p = self.ab[t - 1]
                     alpha = a_t / a_p
                     beta = 1.0 - alpha

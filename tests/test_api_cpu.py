@@ -26,7 +26,8 @@ class TestConfig:  # test_harness.py:45-116
         cfg = harness.parse_config({"seed": 7})
         assert cfg.seeds == {"model": 7, "sampling": 7, "prune": 7}
         assert cfg.model["num_blocks"] == 8 and cfg.schedule["steps"] == 50
-        assert cfg.device == {"attention": "precise", "noise": "numpy", "decisions": "per_video"}
+        assert cfg.device == {"attention": "precise", "noise": "numpy", "decisions": "per_video",
+                              "sampler": "ddpm"}
 
     @pytest.mark.parametrize("obj", [{"bogus": 1}, {"model": {"bogus": 1}},
                                      {"thresholds": {"nope": 1}}, {"device": {"x": 1}}])
