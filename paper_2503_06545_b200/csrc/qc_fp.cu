@@ -476,22 +476,29 @@ __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, in
   pdl_wait();
   pdl_trigger();
   __shared__ float q_val[8][256];
-  __shared__ int q_row[8][256];
-  __shared__ int q_col[8][256];
+  __shared__ long long q_off[8][256];   // element offset from x of each queued element
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cpr = (cols + 255) / 256;   // 256-column chunks per row (8 per lane)
-  const long long nchunks = (long long)rows * cpr;
-  for (long long ch = (long long)blockIdx.x * 8 + warp; ch < nchunks;
-       ch += (long long)gridDim.x * 8) {
-    const int row = (int)(ch / cpr);
-    const int c0 = (int)(ch - (long long)row * cpr) * 256;
-    float* xr = x + row * ld;
+  // grid-stride over chunks with incremental (row, chunk) indices: no 64-bit
+  // division per chunk
+  const long long first = (long long)blockIdx.x * 8 + warp;
+  const long long stride = (long long)gridDim.x * 8;
+  const int row_step = (int)(stride / cpr), cc_step = (int)(stride % cpr);
+  int row = (int)(first / cpr), cc = (int)(first % cpr);
+  for (; row < rows; row += row_step, cc += cc_step) {
+    if (cc >= cpr) {
+      cc -= cpr;
+      ++row;
+      if (row >= rows) break;
+    }
+    const int c0 = cc * 256;
+    float* xr = x + (long long)row * ld;
+    const bool full = c0 + 256 <= cols;
     float v[8];
-    uint32_t hard = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = c0 + h * 128 + lane * 4;
-      if (c + 3 < cols) {
+      if (full || c + 3 < cols) {
         const float4 t4 = *reinterpret_cast<const float4*>(xr + c);
         v[4 * h] = t4.x; v[4 * h + 1] = t4.y; v[4 * h + 2] = t4.z; v[4 * h + 3] = t4.w;
       } else {
@@ -499,16 +506,19 @@ __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, in
         for (int e = 0; e < 4; ++e) v[4 * h + e] = (c + e < cols) ? xr[c + e] : 0.f;
       }
     }
-    float y[8];
-    uint32_t valid = 0;
+    uint32_t valid = 0xFFu;
+    if (!full) {
+      valid = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (c0 + (i >> 2) * 128 + lane * 4 + (i & 3) < cols) valid |= 1u << i;
-    hard = gelu_phase_a8(v, y, valid);
+      for (int i = 0; i < 8; ++i)
+        if (c0 + (i >> 2) * 128 + lane * 4 + (i & 3) < cols) valid |= 1u << i;
+    }
+    float y[8];
+    const uint32_t hard = gelu_phase_a8(v, y, valid);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = c0 + h * 128 + lane * 4;
-      if (c + 3 < cols) {
+      if (full || c + 3 < cols) {
         *reinterpret_cast<float4*>(xr + c) =
             make_float4(y[4 * h], y[4 * h + 1], y[4 * h + 2], y[4 * h + 3]);
       } else {
@@ -526,23 +536,24 @@ __global__ void __launch_bounds__(256) gelu_inplace_k(float* x, long long ld, in
       if (lane >= d) off += n;
     }
     const int total = __shfl_sync(0xffffffffu, off, 31);
-    off -= cnt;
     if (total == 0) continue;
+    off -= cnt;
+    const long long base = (long long)row * ld + c0 + lane * 4;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       if ((hard >> i) & 1u) {
         q_val[warp][off] = v[i];
-        q_row[warp][off] = row;
-        q_col[warp][off] = c0 + (i >> 2) * 128 + lane * 4 + (i & 3);
+        q_off[warp][off] = base + (i >> 2) * 128 + (i & 3);
         ++off;
       }
     __syncwarp();
     for (int i = lane; i < total; i += 32) {
       // certified erfc branch on full warps; the exact replica only where it
       // cannot decide (near ties, far tails)
+      const float xv = q_val[warp][i];
       float yv;
-      if (!gelu_fast_b(q_val[warp][i], yv)) yv = gelu_f32_ref(q_val[warp][i]);
-      x[q_row[warp][i] * ld + q_col[warp][i]] = yv;
+      if (!gelu_fast_b(xv, yv)) yv = gelu_f32_ref(xv);
+      x[q_off[warp][i]] = yv;
     }
     __syncwarp();
   }
