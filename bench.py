@@ -803,9 +803,18 @@ def run_ours(args):
     from paper_2503_06545_b200.model import DiTConfig, DiTModel
 
     world, rank, local = _rank_env()
+    # QCB_BENCH_SHARED_GPU=1: a functional check of the multi-rank code path on
+    # a one-GPU box (every rank on cuda:0, gloo); its numbers are not a
+    # measurement.  Per-video ranks never wait on one another's kernels.
+    shared = os.environ.get("QCB_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = _peaks()
     traffic = _ncu_traffic()
     int8_peak = measured_int8_peak(torch) if rank == 0 else {"tops": None}
