@@ -451,6 +451,16 @@ QC_DEV uint32_t f32_round_risk(double q) {
   return (uint32_t)(nonzero & (range | tie));
 }
 
+// f32_round_risk without the zero exemption, in fewer integer instructions
+// (the range test on the masked exponent field, no field extraction): zero is
+// reported as a risk and takes the exact path, which returns it unchanged.
+QC_DEV bool f32_round_risk_z(double q) {
+  const uint32_t lo = (uint32_t)__double2loint(q), hi = (uint32_t)__double2hiint(q);
+  const bool range = ((hi & 0x7FF00000u) - ((1023u - 125u) << 20)) > (251u << 20);
+  const bool tie = ((lo & 0x1FFFFFFFu) - ((1u << 28) - 63u)) < 127u;
+  return range | tie;
+}
+
 // q rounded to a 24-bit significand by round-half-up on the magnitude: equal
 // to (double)(float)q whenever f32_round_risk(q) == 0 (ties never reach it).
 QC_DEV double d_round24_fast(double q) {

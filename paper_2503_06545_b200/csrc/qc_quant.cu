@@ -1063,19 +1063,21 @@ __global__ void __launch_bounds__(kV4Threads, kMinCtas)
         const double* rc = a.rc[o];
         // ---- balance (exact f32(h / c), held in f64) + sign, stage A
         double v[16];
-        uint32_t slow = 0;
+        bool slow = false;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {   // rc carries the rotation sign
           const double q = __dmul_rn((double)h[j], __ldg(rc + lt + TPR * j));
-          slow |= f32_round_risk(q) << j;
+          slow |= f32_round_risk_z(q);
           v[j] = d_round24_fast(q);
         }
         if (slow) {   // exact IEEE division next to an f32 rounding boundary (rare)
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if ((slow >> j) & 1u)
+          for (int j = 0; j < 16; ++j) {
+            const double r = __ldg(rc + lt + TPR * j);
+            if (f32_round_risk_z(__dmul_rn((double)h[j], r)))
               v[j] = flip_sign(div_exact_f32((double)h[j], c[lt + TPR * j]),
-                               __ldg(rc + lt + TPR * j) < 0.0);   // rc carries the sign
+                               r < 0.0);   // rc carries the sign
+          }
         }
         fwht_regs<4>(v);
 #pragma unroll
