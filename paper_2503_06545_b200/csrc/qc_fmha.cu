@@ -123,6 +123,23 @@ QC_DEV float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Blackwell packed f32x2 arithmetic (FFMA2 / FADD2): two lanes per instruction
+QC_DEV unsigned long long f2_bits(float lo, float hi) {
+  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+QC_DEV unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+QC_DEV unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+QC_DEV float f2_lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
+QC_DEV float f2_hi(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
 QC_DEV uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);   // .x (low half) = lo
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -189,7 +206,7 @@ __global__ void __launch_bounds__(kFmThreads, 1)
   uint64_t* kv_full = bars + 6;    // [ST]
   uint64_t* kv_empty = kv_full + ST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + ST);
-  float* xch = reinterpret_cast<float*>(kv_empty + ST + 2);   // [2 tiles][2 halves][128 rows]
+  __shared__ float xch[2 * 2 * 2 * 128];   // [block parity][tile][half][row] (shared, not generic)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = blockIdx.y;
@@ -317,7 +334,7 @@ __global__ void __launch_bounds__(kFmThreads, 1)
     const int nch = a.dhp >> 4;                                   // 16-column O chunks
     const int ch0 = hf ? (nch + 1) / 2 : 0, ch1 = hf ? nch : (nch + 1) / 2;
     const float c = a.c;
-    float* xm = xch + (2 * i) * 128;                              // [half][row]
+    float* const xm0 = xch + (2 * i) * 128;                       // [parity][.][half][row]
     float m = -INFINITY, l0 = 0.f, l1 = 0.f;
     auto masked = [&](uint32_t (&s)[32], int col0, int valid) {
       if (valid < 128) {
@@ -380,10 +397,12 @@ __global__ void __launch_bounds__(kFmThreads, 1)
         mx3 = fmaxf(mx3, __uint_as_float(s1[t + 1]));
       }
       // the row's max over both halves (exchange through shared memory)
+      // (slots alternate with the block parity: a slot is rewritten two blocks
+      // later, after the next exchange barrier, so one barrier per block)
+      float* const xm = xm0 + (j & 1) * 512;
       xm[hf * 128 + r] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
       named_bar_sync(3 + i, 256);
       const float mblk = fmaxf(xm[r], xm[128 + r]) * c;
-      named_bar_sync(3 + i, 256);                    // both read before the next write
       // lazy rescale, warp-uniform (tcgen05.ld / st are warp-collective) and
       // identical in the row's two halves: only when some row's max grew by
       // more than 2^8 (first block: m = -inf)
@@ -407,34 +426,39 @@ __global__ void __launch_bounds__(kFmThreads, 1)
       // P = exp2(s c - m) as bf16 pairs: this half's 64 scores -> 32 packed
       // columns at 32 hf.  Half 1's P lands in [32, 64), scores of half 0,
       // which half 0 read before the exchange barrier above.
-      const float nm = -m;
+      // packed pairs: one FFMA2 for two scaled scores, one FADD2 for two sums
+      const unsigned long long c2 = f2_bits(c, c), nm2 = f2_bits(-m, -m);
+      unsigned long long acc2 = f2_bits(l0, l1);
       uint32_t pk[16];
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
-        const float p0 = ex2_approx(fmaf(__uint_as_float(s0[2 * t]), c, nm));
-        const float p1 = ex2_approx(fmaf(__uint_as_float(s0[2 * t + 1]), c, nm));
-        l0 += p0;
-        l1 += p1;
+        const unsigned long long x2 =
+            ffma2(((unsigned long long)s0[2 * t + 1] << 32) | s0[2 * t], c2, nm2);
+        const float p0 = ex2_approx(f2_lo(x2)), p1 = ex2_approx(f2_hi(x2));
+        acc2 = fadd2(acc2, f2_bits(p0, p1));
         pk[t] = pack_bf16(p0, p1);
       }
       tmem_st16(p_addr, pk);
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
-        const float p0 = ex2_approx(fmaf(__uint_as_float(s1[2 * t]), c, nm));
-        const float p1 = ex2_approx(fmaf(__uint_as_float(s1[2 * t + 1]), c, nm));
-        l0 += p0;
-        l1 += p1;
+        const unsigned long long x2 =
+            ffma2(((unsigned long long)s1[2 * t + 1] << 32) | s1[2 * t], c2, nm2);
+        const float p0 = ex2_approx(f2_lo(x2)), p1 = ex2_approx(f2_hi(x2));
+        acc2 = fadd2(acc2, f2_bits(p0, p1));
         pk[t] = pack_bf16(p0, p1);
       }
+      l0 = f2_lo(acc2);
+      l1 = f2_hi(acc2);
       tmem_st16(p_addr + 16, pk);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[i]);
     }
     // ---- epilogue: O / l -> bf16 rows (each half stores its O chunks)
-    xm[hf * 128 + r] = l0 + l1;
+    float* const xl = xm0 + (nkb & 1) * 512;   // the slot no thread can still be reading
+    xl[hf * 128 + r] = l0 + l1;
     named_bar_sync(3 + i, 256);
-    const float rl = 1.0f / (xm[r] + xm[128 + r]);
+    const float rl = 1.0f / (xl[r] + xl[128 + r]);
     mbar_wait(o_full, 0);
     tc_fence_after();
     const int row = q0 + 128 * i + r;
