@@ -362,6 +362,7 @@ def profile_call(torch, eng, seeds, x0, cond, S, d, H, int8_peak, peaks, traffic
             "bound": "hbm", "achieved": qgbs, "peak": peaks["hbm"], "unit": "GB/s",
             "frac": (qgbs / peaks["hbm"]) if qgbs else None,
             "traffic": traffic.get("act_quant"),
+            "traffic_call": (traffic.get("notes") or {}).get("act_quant"),
             "kernel": "act_quant (aq4_pass1 + aq2_pass2_hot + init_keys)",
             "peak_source": peaks["source"] + " hbm_gbs (burst copy)",
             "share_of_step": q_time / step if step else None,
@@ -372,6 +373,7 @@ def profile_call(torch, eng, seeds, x0, cond, S, d, H, int8_peak, peaks, traffic
             "bound": "tensor", "achieved": tops, "peak": peak_tops, "unit": "TOP/s",
             "frac": (tops / peak_tops) if tops else None,
             "traffic": traffic.get("gemm_u8_tcgen05"),
+            "traffic_call": (traffic.get("notes") or {}).get("gemm_u8_tcgen05"),
             "kernel": "gemm_u8_tcgen05 (+ gemm_u8_small_m for the cond token)",
             "peak_source": int8_peak.get("source"), "nominal_int8_dense_tops": NOMINAL_INT8_TOPS,
             "share_of_step": g_time / step if step else None,
