@@ -10,7 +10,7 @@ sys.path.insert(0, ".")
 from paper_2503_06545_b200 import device as D  # noqa: E402
 
 import os
-H, dh, S = 16, int(os.environ.get("DH", "72")), 16384
+H, dh, S = 16, int(os.environ.get("DH", "72")), int(os.environ.get("S", "16384"))
 for B in (1, 4):
     d = H * dh
     q, k, v = (torch.randn((B * S, d), device="cuda").to(torch.bfloat16) for _ in range(3))

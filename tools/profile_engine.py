@@ -1,57 +1,41 @@
-"""Per-phase device/host timing of one C3 QuantCache generation (profiling aid).
-
-Uses bench.py's C3 model and synthetic calibration with fixed thresholds taken
-from a bench calibration pass, so the run is short enough for an ncu launch list."""
-import argparse
-import json
+"""Host-side profile of one C3 QuantCache generation (4 videos, T = 100):
+cProfile of generate() plus the device time, to find the Python work on the
+critical path between a step's decision sync and its first launch."""
+import cProfile
+import pstats
 import sys
 import time
 
-import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-import bench
-from paper_2503_06545_b200 import device as Dv
-from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine
-from paper_2503_06545_b200.model import DiTConfig
-from paper_2503_06545_b200.sampler import linear_beta_schedule
-from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles
+import bench  # noqa: E402
+from paper_2503_06545_b200.engine import EngineOptions, QuantCacheEngine  # noqa: E402
+from paper_2503_06545_b200.model import DiTConfig  # noqa: E402
+from paper_2503_06545_b200.sampler import linear_beta_schedule  # noqa: E402
+from paper_2503_06545_b200.schedule import ThresholdConfig, Toggles  # noqa: E402
 
-ap = argparse.ArgumentParser()
-ap.add_argument("--timesteps", type=int, default=20)
-ap.add_argument("--videos", type=int, default=1)
-ap.add_argument("--recompute-all", action="store_true")
-args = ap.parse_args()
-cfg = DiTConfig(seed=0, **bench.C3)
-model = bench.fast_model(torch, cfg)
-absmax = {l: {s: np.abs(getattr(b, s)).max(axis=1).astype(np.float64)
-              for s in ("sta_q", "sta_k", "sta_v", "sta_o", "ca_q", "ca_k", "ca_v", "ca_o",
-                        "ffn1", "ffn2")} for l, b in enumerate(model.blocks)}
-sched = linear_beta_schedule(args.timesteps)
-if args.recompute_all:
-    th = ThresholdConfig(delta1=0.0, delta2=0.0)
-    tog = Toggles(hlc=True, aigq_weights=True, aigq_acts=True, srap=False)
-else:
-    th = ThresholdConfig(delta1=1.17e10, delta2=2.54e10, v_low=6.8e6, v_high=1.3e7)
-    tog = Toggles(True, True, True, True)
-eng = QuantCacheEngine(model, sched.alpha_bar, tog, th, {l: 6 for l in range(28)}, absmax,
-                       max_videos=args.videos,
+cfg = DiTConfig(seed=0, **bench.model_dims("c3"))
+model = bench.fast_model(cfg)
+absmax = bench.synthetic_absmax(model)
+sched = linear_beta_schedule(100)
+th = ThresholdConfig(delta1=11740291439.2, delta2=25524842316.4, v_low=9995031.5,
+                     v_high=18937808.3)
+eng = QuantCacheEngine(model, sched.alpha_bar, Toggles(True, True, True, True), th,
+                       {l: 6 for l in range(28)}, absmax, max_videos=4,
                        options=EngineOptions(attention="fast", noise="device"))
-seeds = list(range(args.videos))
-eng.generate(seeds, device_noise_seed=0, return_device=True)   # warm-up
+g = torch.Generator(device="cuda").manual_seed(1)
+x0 = torch.randn((4, cfg.seq_len, cfg.model_dim), device="cuda", generator=g)
+cond = torch.randn((4, cfg.cond_dim), device="cuda", generator=g)
+eng.generate([1, 2, 3, 4], x0_dev=x0, cond_dev=cond, return_device=True)
 torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-l0 = Dv.LAUNCHES[0]
 t0 = time.perf_counter()
-e0.record()
-_, vids = eng.generate(seeds, device_noise_seed=1, return_device=True)
-e1.record()
+eng.generate([5, 6, 7, 8], x0_dev=x0, cond_dev=cond, return_device=True)
 torch.cuda.synchronize()
-wall = time.perf_counter() - t0
-tr = eng.traces_of(vids)
-rec = sum(r.action == "recompute" for t in tr for r in t if r.layer != "head")
-print(json.dumps({"timesteps": args.timesteps, "videos": args.videos,
-                  "device_ms": e0.elapsed_time(e1), "wall_ms": wall * 1e3,
-                  "launches": Dv.LAUNCHES[0] - l0, "recomputed_blocks": rec,
-                  "blocks": args.timesteps * 28 * args.videos}))
+print("wall ms", (time.perf_counter() - t0) * 1e3)
+pr = cProfile.Profile()
+pr.enable()
+eng.generate([9, 10, 11, 12], x0_dev=x0, cond_dev=cond, return_device=True)
+torch.cuda.synchronize()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(25)
