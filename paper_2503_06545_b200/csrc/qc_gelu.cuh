@@ -81,6 +81,16 @@ QC_DEV bool gelu_fast_a(float xf, float& y) {
   return true;
 }
 
+// 1/u from the MUFU seed and ONE Newton step: relative error below 2^-40
+// (seed error below 2^-20), for the phase-A path whose certificate window is
+// widened to match
+QC_DEV double fast_rcp1(double u) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  const double e = fma(-u, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Phase A for 8 elements without branches: every element runs the same
 // straight-line code and the certificate becomes a select (per-element early
 // exits cost more than the shared arithmetic).  Returns the hard mask.
@@ -98,14 +108,16 @@ QC_DEV uint32_t gelu_phase_a8(const float (&v)[8], float (&y)[8], uint32_t valid
     double u = z + kErfU[0];
 #pragma unroll
     for (int k = 1; k < 5; ++k) u = fma(u, z, kErfU[k]);
-    double r = (at * tt) * fast_rcp(u);
+    double r = (at * tt) * fast_rcp1(u);
     r = t < 0.0 ? -r : r;
     const double g = (0.5 * x) * (1.0 + r);
-    // certificate: f32-normal range and >= 256 ulp64 from an f32 tie, as integers
+    // certificate: f32-normal range and >= 2^14 ulp64 from an f32 tie (the
+    // one-step reciprocal's < 2^-40 error amplified at most ~6x by 1 + erf,
+    // plus the rational's own error), as integers
     const unsigned long long gb = (unsigned long long)__double_as_longlong(g);
     const unsigned ex = (unsigned)((gb >> 52) & 0x7FF);
     const int dd = abs((int)((unsigned)gb & 0x1FFFFFFFu) - (1 << 28));
-    const bool ok = (at < 1.0 - 0x1p-40) && (ex - (1023u - 125u)) <= 251u && dd > 256;
+    const bool ok = (at < 1.0 - 0x1p-40) && (ex - (1023u - 125u)) <= 251u && dd > 16384;
     const bool big = v[i] >= 6.0f, zero = v[i] == 0.0f;
     y[i] = big ? v[i] : __double2float_rn(g);   // g = +-0 for x = +-0
     if (((valid >> i) & 1u) && !big && !zero && !ok) hard |= 1u << i;
