@@ -62,3 +62,27 @@ def test_rf_draws_no_noise(golden_dir, cuda_dev):
                                       options=EngineOptions(noise=noise, sampler="rf"))
         outs.append(eng.generate([4, 9])[0])
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_rf_with_cfg_scale_zero_is_the_uncond_run(golden_dir, cuda_dev):
+    """The two extensions together: rectified flow with guidance 0 equals the
+    plain flow run whose cond is zero (latents and the uncond branch's trace)."""
+    from paper_2503_06545_b200 import harness
+    from paper_2503_06545_b200.engine import EngineOptions
+    cfg = harness.parse_config(dict(SMALL, toggles=dict(hlc=True, aigq_weights=True,
+                                                        aigq_acts=True, srap=True),
+                                    calibration=os.path.join(golden_dir, "calib_small.json")))
+    calib = harness.load_calibration(cfg.calibration)
+    tog = cfg.toggles_obj()
+    rng = np.random.default_rng(9)
+    x0 = torch.as_tensor(rng.standard_normal((2, 8, 16)).astype(np.float32)).cuda()
+    cond = torch.as_tensor(rng.standard_normal((2, 8)).astype(np.float32)).cuda()
+    eng, _ = harness.build_engine(cfg, tog, calib, max_videos=4,
+                                  options=EngineOptions(sampler="rf", cfg_scale=0.0))
+    got, tr = eng.generate([31, 32], x0_dev=x0, cond_dev=cond)
+    plain, _ = harness.build_engine(cfg, tog, calib, max_videos=2,
+                                    options=EngineOptions(sampler="rf"))
+    want, trp = plain.generate([31, 32], x0_dev=x0, cond_dev=torch.zeros_like(cond))
+    assert np.array_equal(got, want)
+    for i in range(2):
+        assert [r.to_json_obj() for r in tr[2 * i + 1]] == [r.to_json_obj() for r in trp[i]]
